@@ -1,0 +1,454 @@
+#!/usr/bin/env python3
+"""bench.py — conv fwd+bwd GFLOP/s of the sm_100a SpatialConvolutionMM path.
+
+Metric (BASELINE.json): "conv fwd+bwd GFLOP/s (convnet-benchmarks L1-L5)". One step =
+one fwd + bwd pass (updateOutput, updateGradInput, accGradParameters incl. gradBias)
+of every layer of the workload over one synthetic batch; FLOPs = 3 * 2*N*K*CRS*oH*oW
+per layer (fprop + dgrad + wgrad; bias work excluded).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload convnet|alexnet|...]
+  python bench.py --impl reference ...   # the CPU reference path (oracle port), same metric
+
+Multi-GPU (torchrun, one rank per GPU): each rank runs the same per-GPU batch (weak
+scaling, batch-sharded data parallelism) and gradWeight/gradBias are all-reduced with
+NCCL per layer on a communication stream overlapping the next layer's backward.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# (name, N, C, H, W, K, kH, kW, padH, padW, strideH, strideW)
+WORKLOADS = {
+    "convnet": [  # convnet-benchmarks layerwise suite (pad 0), BASELINE.json configs[1]
+        ("L1", 128, 3, 128, 128, 96, 11, 11, 0, 0, 1, 1),
+        ("L2", 128, 64, 64, 64, 128, 9, 9, 0, 0, 1, 1),
+        ("L3", 128, 128, 32, 32, 128, 9, 9, 0, 0, 1, 1),
+        ("L4", 128, 128, 16, 16, 128, 7, 7, 0, 0, 1, 1),
+        ("L5", 128, 384, 13, 13, 384, 3, 3, 0, 0, 1, 1),
+    ],
+    "cfg1": [("cfg1", 16, 3, 32, 32, 64, 3, 3, 1, 1, 1, 1)],
+    "alexnet": [  # OWT AlexNet conv stack, batch 128, 224x224 (configs[2])
+        ("c1", 128, 3, 224, 224, 64, 11, 11, 2, 2, 4, 4),
+        ("c2", 128, 64, 27, 27, 192, 5, 5, 2, 2, 1, 1),
+        ("c3", 128, 192, 13, 13, 384, 3, 3, 1, 1, 1, 1),
+        ("c4", 128, 384, 13, 13, 256, 3, 3, 1, 1, 1, 1),
+        ("c5", 128, 256, 13, 13, 256, 3, 3, 1, 1, 1, 1),
+    ],
+    "overfeat": [  # Overfeat-fast, batch 128, 231x231 (configs[3])
+        ("c1", 128, 3, 231, 231, 96, 11, 11, 0, 0, 4, 4),
+        ("c2", 128, 96, 24, 24, 256, 5, 5, 0, 0, 1, 1),
+        ("c3", 128, 256, 12, 12, 512, 3, 3, 1, 1, 1, 1),
+        ("c4", 128, 512, 12, 12, 1024, 3, 3, 1, 1, 1, 1),
+        ("c5", 128, 1024, 12, 12, 1024, 3, 3, 1, 1, 1, 1),
+    ],
+    "vgga": [  # VGG-A conv stack, batch 64, 224x224 (configs[4])
+        ("c1", 64, 3, 224, 224, 64, 3, 3, 1, 1, 1, 1),
+        ("c2", 64, 64, 112, 112, 128, 3, 3, 1, 1, 1, 1),
+        ("c3", 64, 128, 56, 56, 256, 3, 3, 1, 1, 1, 1),
+        ("c4", 64, 256, 56, 56, 256, 3, 3, 1, 1, 1, 1),
+        ("c5", 64, 256, 28, 28, 512, 3, 3, 1, 1, 1, 1),
+        ("c6", 64, 512, 28, 28, 512, 3, 3, 1, 1, 1, 1),
+        ("c7", 64, 512, 14, 14, 512, 3, 3, 1, 1, 1, 1),
+        ("c8", 64, 512, 14, 14, 512, 3, 3, 1, 1, 1, 1),
+    ],
+}
+METRIC = "conv fwd+bwd GFLOP/s (convnet-benchmarks L1-L5)"
+
+
+def layer_flops(l) -> float:
+    _, N, C, H, W, K, kH, kW, pH, pW, sH, sW = l
+    oH = (H + 2 * pH - kH) // sH + 1
+    oW = (W + 2 * pW - kW) // sW + 1
+    return 3.0 * 2.0 * N * K * C * kH * kW * oH * oW
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="convnet", choices=list(WORKLOADS))
+    ap.add_argument("--math", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        top = max(sm)
+        loaded = [s for s in sm if s >= 0.5 * top] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------- peaks
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def measure_cublas_tf32(torch):
+    """cuBLAS TF32 8192^3 (burst, best of 5) — the on-box TF32 dense denominator."""
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = True
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        for _ in range(3):
+            a @ b
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            a @ b
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        torch.cuda.empty_cache()
+        return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- CPU legs
+def cpu_sample_run(layers, batch, threads):
+    """One fwd+bwd of every layer at `batch` images through the oracle port (im2col +
+    blocked SGEMM + col2im). Returns (seconds, flops)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    t = 0.0
+    fl = 0.0
+    for l in layers:
+        _, N, C, H, W, K, kH, kW, pH, pW, sH, sW = l
+        g = po.geom(batch, C, H, W, K, kH, kW, pH, pW, sH, sW)
+        oh, ow = po.out_hw(g)
+        x = po.uniform((batch, C, H, W), 1)
+        w = po.uniform((K, C, kH, kW), 2, -0.1, 0.1)
+        b = po.uniform((K,), 3, -0.1, 0.1)
+        gy = po.uniform((batch, K, oh, ow), 4)
+        t0 = time.perf_counter()
+        po.conv_forward(g, x, w, b, chunk=1, threads=threads)
+        po.conv_backward_input(g, gy, w, threads=threads)
+        po.conv_backward_weight(g, x, gy, threads=threads)
+        t += time.perf_counter() - t0
+        fl += layer_flops((l[0], batch) + tuple(l[2:]))
+    return t, fl
+
+
+def cpu_baseline(layers, budget_s):
+    threads = os.cpu_count() or 1
+    t1, f1 = cpu_sample_run(layers, 1, threads)
+    batch = 1
+    if t1 > 0 and t1 < budget_s / 2:
+        batch = max(1, min(layers[0][1], int(budget_s / t1)))
+        t1, f1 = cpu_sample_run(layers, batch, threads)
+    return {"value": f1 / t1 / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"{batch} image(s) per layer, fwd+bwd of every layer, oracle im2col+"
+                      f"blocked SGEMM+col2im (oracle/oracle.c), {threads} OpenMP threads, "
+                      f"{t1:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    layers = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    # bounded sample per step: 1 image per layer (the full batch would take many minutes)
+    for _ in range(args.warmup):
+        cpu_sample_run(layers, 1, threads)
+    tt, ff = 0.0, 0.0
+    for _ in range(args.steps):
+        t, f = cpu_sample_run(layers, 1, threads)
+        tt += t
+        ff += f
+    v = ff / tt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic (counter-based uniform)",
+        "config": {"workload": args.workload, "layers": [l[0] for l in layers],
+                   "sample_batch_per_layer": 1, "full_batch": layers[0][1]},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": "1 image per layer per step, fwd+bwd, oracle port "
+                                   "(im2col + blocked SGEMM + col2im); the reference ships no "
+                                   "conv implementation (SURVEY.md §0)"},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1606_04884_b200 as pt
+    from paper_1606_04884_b200 import _lib as L
+
+    layers = WORKLOADS[args.workload]
+    dev = torch.device("cuda", local)
+    st = []
+    for i, l in enumerate(layers):
+        name, N, C, H, W, K, kH, kW, pH, pW, sH, sW = l
+        g = pt.ConvGeometry(N, C, H, W, K, kH, kW, pH, pW, sH, sW)
+        seed = 0x5EED + 101 * i + 7919 * rank
+        x = pt.fill_uniform(torch.empty(g.input_shape(), device=dev), seed + 1)
+        s = 1.0 / (C * kH * kW) ** 0.5
+        w = pt.fill_uniform(torch.empty(g.weight_shape(), device=dev), seed + 2, -s, s)
+        b = pt.fill_uniform(torch.empty((K,), device=dev), seed + 3, -0.1, 0.1)
+        gy = pt.fill_uniform(torch.empty(g.output_shape(), device=dev), seed + 4)
+        st.append(dict(g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
+                       gx=torch.empty(g.input_shape(), device=dev),
+                       gw=torch.empty(g.weight_shape(), device=dev),
+                       gb=torch.empty((K,), device=dev)))
+    comm = torch.cuda.Stream(device=dev) if world > 1 else None
+
+    def step():
+        cur = torch.cuda.current_stream()
+        for s in st:
+            g = s["g"]
+            pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math)
+            pt.conv_backward_input(g, s["gy"], s["w"], s["gx"], math=args.math)
+            pt.conv_backward_weight(g, s["x"], s["gy"], s["gw"], s["gb"], math=args.math)
+            if comm is not None:  # batch-sharded DP: allreduce(sum) gradW/gradB, overlapped
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                comm.wait_event(ev)
+                with torch.cuda.stream(comm):
+                    dist.all_reduce(s["gw"])
+                    dist.all_reduce(s["gb"])
+        if comm is not None:
+            cur.wait_stream(comm)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    peaks, peak_kind = load_peaks()
+    clocks = ClockSampler(local)
+    L.lib().pt_b200_profile_enable(1)
+    L.lib().pt_b200_profile_reset()
+    launches0 = pt.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = pt.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    prof = {c: L.profile_read(c) for c in ("umma_conv", "umma_wgrad", "simt_conv", "layout")}
+    L.lib().pt_b200_profile_enable(0)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    flops_step = sum(layer_flops(l) for l in layers)
+    value = flops_step * world / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel class (by device time inside the timed region)
+    dom = max(prof, key=lambda c: prof[c][0])
+    dms, dn, dfl, dby = prof[dom]
+    tf32_cublas = measure_cublas_tf32(torch) if rank == 0 else None
+    tf32_derived = peaks.get("bf16_tflops", 1590.0) / 2.0
+    if dom == "layout":
+        roof = {"bound": "hbm", "achieved": dby / (dms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s"}
+    else:
+        peak_tf = max(tf32_derived, tf32_cublas or 0.0)
+        roof = {"bound": "tensor", "achieved": dfl / (dms * 1e-3) / 1e12, "peak": peak_tf,
+                "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = dom
+    roof["launches"] = dn
+    roof["share_of_step"] = dms / ms if ms > 0 else None
+    roof["peak_source"] = (f"max(cuBLAS TF32 8192^3 on this box = {tf32_cublas}, "
+                           f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})"
+                           if roof["bound"] == "tensor" else f"{peak_kind} hbm_gbs")
+
+    result = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "tf32" if args.math == "tf32" else "fp32",
+        "data": "synthetic (counter-based uniform, device-generated)",
+        "config": {"workload": args.workload, "layers": [l[0] for l in layers],
+                   "global_batch": layers[0][1] * world, "per_gpu_batch": layers[0][1],
+                   "parallelism": f"dp{world}", "math": args.math,
+                   "l2": "no flush: per-step working set "
+                         f"{sum(4*(s['x'].numel()+s['y'].numel()+s['gy'].numel()+s['gx'].numel()) for s in st)/1e9:.2f} GB > 126 MB L2"},
+        "clocks": clk, "gpu_launches": launches, "roofline": roof,
+        "kernels": {c: {"ms": v[0], "launches": v[1], "tflops": (v[2] / (v[0] * 1e-3) / 1e12)
+                        if v[0] > 0 and v[2] > 0 else None,
+                        "gbs": (v[3] / (v[0] * 1e-3) / 1e9) if v[0] > 0 and v[3] > 0 else None}
+                    for c, v in prof.items()},
+    }
+
+    # e2e through the public API with HOST buffers (pinned), copies inside the timed region
+    if not args.no_e2e:
+        result["e2e"] = e2e(args, pt, torch, layers, dev, world, rank, dist)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            result["cpu_baseline"] = cpu_baseline(layers, args.cpu_seconds)
+        except Exception as ex:  # pragma: no cover
+            result["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e(args, pt, torch, layers, dev, world, rank, dist):
+    host = []
+    for i, l in enumerate(layers):
+        name, N, C, H, W, K, kH, kW, pH, pW, sH, sW = l
+        g = pt.ConvGeometry(N, C, H, W, K, kH, kW, pH, pW, sH, sW)
+        d = {k: torch.empty(shape, pin_memory=True) for k, shape in
+             (("x", g.input_shape()), ("w", g.weight_shape()), ("b", (K,)),
+              ("gy", g.output_shape()), ("y", g.output_shape()), ("gx", g.input_shape()),
+              ("gw", g.weight_shape()), ("gb", (K,)))}
+        for k in ("x", "w", "b", "gy"):
+            d[k].uniform_(-1, 1)
+        d["g"] = g
+        host.append(d)
+    h2d = sum(4 * (d["x"].numel() + d["w"].numel() + d["b"].numel() + d["gy"].numel())
+              for d in host)
+    d2h = sum(4 * (d["y"].numel() + d["gx"].numel() + d["gw"].numel() + d["gb"].numel())
+              for d in host)
+
+    def step():
+        for d in host:
+            g = d["g"]
+            x = d["x"].to(dev, non_blocking=True)
+            w = d["w"].to(dev, non_blocking=True)
+            b = d["b"].to(dev, non_blocking=True)
+            gy = d["gy"].to(dev, non_blocking=True)
+            y = pt.conv_forward(g, x, w, b, math=args.math)
+            gx = pt.conv_backward_input(g, gy, w, math=args.math)
+            gw, gb = pt.conv_backward_weight(g, x, gy, math=args.math)
+            if world > 1:
+                dist.all_reduce(gw)
+                dist.all_reduce(gb)
+            d["y"].copy_(y, non_blocking=True)
+            d["gx"].copy_(gx, non_blocking=True)
+            d["gw"].copy_(gw, non_blocking=True)
+            d["gb"].copy_(gb, non_blocking=True)
+        torch.cuda.synchronize()
+
+    step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.e2e_steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops_step = sum(layer_flops(l) for l in layers) * world
+    return {"value": flops_step / (ms / args.e2e_steps * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+            "path": "paper_1606_04884_b200.conv_* (C ABI) on pinned host tensors, "
+                    "H2D inputs + D2H outputs/gradients inside the timed region"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * pt_b200.h — C ABI of libpt_b200.so, the sm_100a SpatialConvolutionMM hot path.
+ *
+ * This is the drop-in boundary. Plain pointers, sizes and an
+ * opaque stream handle only: no C++ or torch types cross it, no exceptions
+ * escape it. Every entry point is stream-ordered on `stream` (a cudaStream_t
+ * passed as void*; NULL = legacy default stream) and reentrant across
+ * streams; only the per-device plan cache (TMA descriptors, tile choice) is
+ * global, under a mutex.
+ *
+ * Return codes mirror the reference's error classes / CLI exit codes
+ * (proj/include/portten/errors.hpp:24-40):
+ *   PT_OK (0), PT_EVALIDATION (2) = ValidationError, PT_EBACKEND (3) = BackendError.
+ * The message of the last failure on the calling thread is pt_b200_last_error().
+ *
+ * Device tensors are float32, dense, row-major (NCHW activations, KCRS weights),
+ * 16-byte aligned. The C++ wrapper (include/portten/ headers) rethrows the codes as
+ * portten::ValidationError / portten::BackendError.
+ */
+#ifndef PT_B200_H
+#define PT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PT_B200_ABI_VERSION 1
+
+enum pt_status { PT_OK = 0, PT_EVALIDATION = 2, PT_EBACKEND = 3 };
+
+/* Conv problem descriptor. Field order == conv::ConvGeometry
+ * (proj/include/portten/conv_geometry.hpp:29-39): batch, inChannels, inHeight,
+ * inWidth, outChannels, kernelH, kernelW, padH, padW, strideH, strideW.
+ * Output dims use the floor rule of conv_geometry.hpp:41-46. */
+typedef struct pt_conv_geom {
+    int64_t N, C, H, W, K, kH, kW, padH, padW, strideH, strideW;
+} pt_conv_geom;
+
+/* Contraction mode. TF32: tcgen05 tensor cores, operands rounded to TF32
+ * (cvt.rna), FP32 accumulate in TMEM. FP32: CUDA-core FFMA implicit GEMM,
+ * the tight-tolerance mode (north_star "FP32-FFMA mode for tight checks"). */
+enum pt_math { PT_MATH_TF32 = 0, PT_MATH_FP32 = 1 };
+
+/* Which conv pass a workspace query is for. */
+enum pt_conv_op { PT_CONV_FWD = 0, PT_CONV_BWD_DATA = 1, PT_CONV_BWD_FILTER = 2 };
+
+/* Strided view (Tensor sizes/strides/storageOffset, proj/include/portten/tensor.hpp:56-120).
+ * Rank 1..8 (kMaxDims, tensor.hpp:29); strides in elements, non-negative. */
+typedef struct pt_view {
+    int32_t ndim;
+    int64_t sizes[8];
+    int64_t strides[8];
+    int64_t offset;
+} pt_view;
+
+/* Reduction op, same order as codegen::ReduceOp (proj/include/portten/kernel_codegen.hpp:70). */
+enum pt_reduce_op { PT_REDUCE_SUM = 0, PT_REDUCE_MAX = 1, PT_REDUCE_MIN = 2 };
+
+/* Apply bytecode: the RPN form of expr::Program (proj/src/expression.cpp:340-402).
+ * One int32 per instruction (low byte = opcode); PT_OP_CONST is followed by one
+ * int32 holding the float bit pattern. Max stack depth 32 (expression.cpp track()). */
+enum pt_apply_op {
+    PT_OP_CONST = 0, PT_OP_X = 1, PT_OP_Y = 2, PT_OP_Z = 3, PT_OP_S = 4,
+    PT_OP_ADD = 5, PT_OP_SUB = 6, PT_OP_MUL = 7, PT_OP_DIV = 8, PT_OP_NEG = 9,
+    PT_OP_ABS = 10, PT_OP_EXP = 11, PT_OP_LOG = 12, PT_OP_SQRT = 13, PT_OP_TANH = 14,
+    PT_OP_MAX = 15, PT_OP_MIN = 16
+};
+
+/* Device capability record (BackendDescriptor, proj/include/portten/backend.hpp:35-40). */
+typedef struct pt_device_desc {
+    char name[64];            /* "b200:<ordinal>" */
+    int32_t maxWorkgroupSize; /* max threads per block */
+    int64_t localMemBytes;    /* max opt-in shared memory per block */
+    int32_t smCount;
+    int32_t ccMajor, ccMinor;
+    int64_t globalMemBytes;
+} pt_device_desc;
+
+/* ---- library / device plumbing (replaces opencl_probe_devices, proj/src/opencl_backend.hpp:29) ---- */
+int pt_b200_abi_version(void);
+const char* pt_b200_last_error(void);
+/* Number of usable sm_100 devices; 0 when no driver/GPU (never an error). */
+int pt_b200_device_count(void);
+int pt_b200_device_info(int device, pt_device_desc* out);
+int pt_b200_set_device(int device);
+int pt_b200_malloc(void** ptr, size_t bytes);
+int pt_b200_free(void* ptr);
+/* device_upload / device_download (proj/src/backend.cpp:163-181): contiguous staging copies. */
+int pt_b200_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int pt_b200_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int pt_b200_stream_sync(void* stream);
+/* Same generator as oracle or_fill_uniform (counter-based splitmix64). */
+int pt_b200_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream);
+
+/* ---- convolution (Torch SpatialConvolutionMM) ---- */
+/* Validates like conv::ConvGeometry::validate (conv_geometry.hpp:53-63). */
+int pt_b200_conv_validate(const pt_conv_geom* g);
+/* Bytes of device scratch the pass needs (caller allocates; 0 is possible). */
+size_t pt_b200_conv_workspace_bytes(const pt_conv_geom* g, int op, int math);
+/* updateOutput == conv_im2col_forward: y = W (K x CRS) * im2col(x) + b.
+ * b may be NULL (no bias). */
+int pt_b200_conv_fwd(const pt_conv_geom* g, const float* x, const float* w, const float* b,
+                     float* y, int math, void* ws, size_t ws_bytes, void* stream);
+/* updateGradInput == conv_backward_input: gx = col2im(W^T * gy). */
+int pt_b200_conv_bwd_data(const pt_conv_geom* g, const float* gy, const float* w, float* gx,
+                          int math, void* ws, size_t ws_bytes, void* stream);
+/* accGradParameters == conv_backward_weight + gradBias:
+ * gw (+)= scale * sum_n gy[n] im2col(x[n])^T ; gb (+)= scale * sum gy. accumulate=0
+ * overwrites (SPEC's fresh gradients), 1 accumulates (Torch). gb may be NULL. */
+int pt_b200_conv_bwd_filter(const pt_conv_geom* g, const float* x, const float* gy, float* gw,
+                            float* gb, float scale, int accumulate, int math, void* ws,
+                            size_t ws_bytes, void* stream);
+/* Standalone unfold of ONE image, bit-exact with proj/templates/im2col.kt.tmpl:9-21. */
+int pt_b200_im2col(const pt_conv_geom* g, const float* img, float* col, void* stream);
+/* Batched unfold: images [n0, n0+count) into (CRS) x (count*oHW). */
+int pt_b200_im2col_batched(const pt_conv_geom* g, const float* x, int64_t n0, int64_t count,
+                           float* col, void* stream);
+/* Scatter-add inverse of im2col for ONE image. img is overwritten. */
+int pt_b200_col2im(const pt_conv_geom* g, const float* col, float* img, void* stream);
+/* SPEC gemm, row-major, device pointers:
+ * C <- alpha*op(A)*op(B) + beta*C. */
+int pt_b200_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float alpha,
+                 const float* A, int64_t lda, const float* B, int64_t ldb, float beta, float* C,
+                 int64_t ldc, int math, void* stream);
+
+/* ---- pointwise apply / reduce on the conv path (Backend::runApply / runReduce*) ---- */
+/* Elementwise program over 1..3 same-shaped strided views; bases[0]/views[0] is x
+ * (the destination). Mirrors ReferenceBackend::runApply (proj/src/reference_backend.cpp:80-113). */
+int pt_b200_apply(const int32_t* code, int32_t ncode, int arity, float* const* bases,
+                  const pt_view* views, float scalar, void* stream);
+/* Per-channel bias add over an NCHW tensor: y[n,k,:,:] += b[k] (the conv-path
+ * "x = x + s" on y.narrow(1,k,1), as one launch). */
+int pt_b200_bias_add(float* y, const float* b, int64_t N, int64_t K, int64_t HW, void* stream);
+/* Reduce-all into *out_dev (device float). Tree order; <=1e-5 rel of the sequential fold. */
+int pt_b200_reduce_all(int op, const float* base, const pt_view* view, float* out_dev,
+                       void* stream);
+/* Reduce along `dim` into a contiguous tensor with sizes[dim]=1 (reference_backend.cpp:129-156). */
+int pt_b200_reduce_dim(int op, const float* base, const pt_view* view, int dim, float* out,
+                       void* stream);
+
+/* ---- data-parallel helpers (batch sharding) ---- */
+/* Number of kernels this library launched on the calling process (bench gpu_launches). */
+int64_t pt_b200_launch_count(void);
+
+/* ---- live kernel timing (bench.py roofline) ----
+ * When enabled, the library brackets each launch of its hot kernels with CUDA events
+ * on the launching stream and records the algorithmic work of that launch. Reading
+ * synchronises the recorded events. Kernel classes: "umma_conv" (tcgen05 fprop/dgrad),
+ * "umma_wgrad" (tcgen05 wgrad), "simt_conv" (FFMA passes), "layout" (NHWC/pack passes). */
+int pt_b200_profile_enable(int on);
+int pt_b200_profile_reset(void);
+/* total_ms = summed event durations, launches = count, flops = algorithmic FLOPs,
+ * bytes = algorithmic HBM bytes (for memory-bound classes). */
+int pt_b200_profile_read(const char* kernel_class, double* total_ms, int64_t* launches,
+                         double* flops, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

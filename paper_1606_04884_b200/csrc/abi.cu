@@ -1,0 +1,379 @@
+// abi.cu — the extern "C" boundary of libpt_b200.so (include/pt_b200.h).
+// Validation mirrors the reference's checks (conv_geometry.hpp:53-63,
+// backend.cpp:115-161); every exception is converted to a status code here.
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace ptb {
+
+std::atomic<int64_t> g_launches{0};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PT_OK;
+    } catch (const AbiError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return PT_EBACKEND;
+    }
+}
+
+std::string geom_str(const pt_conv_geom& g) {
+    char b[256];
+    snprintf(b, sizeof b, "N%lld C%lld H%lld W%lld K%lld k%lldx%lld p%lldx%lld s%lldx%lld",
+             (long long)g.N, (long long)g.C, (long long)g.H, (long long)g.W, (long long)g.K,
+             (long long)g.kH, (long long)g.kW, (long long)g.padH, (long long)g.padW,
+             (long long)g.strideH, (long long)g.strideW);
+    return b;
+}
+
+void require_math(int math) {
+    PTB_REQUIRE(math == PT_MATH_TF32 || math == PT_MATH_FP32,
+                "conv: unknown math mode " + std::to_string(math));
+}
+
+void require_ptr(const void* p, const char* what) {
+    PTB_REQUIRE(p != nullptr, std::string("conv: null ") + what);
+}
+
+void require_view(const pt_view& v, const char* what) {
+    PTB_REQUIRE(v.ndim >= 1 && v.ndim <= 8, std::string(what) + ": rank must be 1..8");
+    for (int d = 0; d < v.ndim; ++d) {
+        PTB_REQUIRE(v.sizes[d] >= 1, std::string(what) + ": sizes must be >= 1");
+        PTB_REQUIRE(v.strides[d] >= 0, std::string(what) + ": negative strides unsupported");
+    }
+    PTB_REQUIRE(v.offset >= 0, std::string(what) + ": negative storage offset");
+}
+
+size_t fwd_ws(const Geo& g, int math) {
+    if (math == PT_MATH_TF32) {
+        const UmmaPlan pl = umma_plan(g, false);
+        if (pl.ok) return pl.ws_bytes;
+    }
+    return 0;
+}
+size_t bwd_data_ws(const Geo& g, int math) {
+    if (math == PT_MATH_TF32) {
+        const UmmaPlan pl = umma_plan(g, true);
+        if (pl.ok) return pl.ws_bytes;
+    }
+    return 0;
+}
+size_t bwd_filter_ws(const Geo& g, int) {
+    return align_up(simt_wgrad_workspace(g), 256) + align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256);
+}
+
+void require_ws(size_t have, size_t need, const void* ws) {
+    PTB_REQUIRE(have >= need && (need == 0 || ws != nullptr),
+                "conv: workspace too small (" + std::to_string(have) + " < " +
+                    std::to_string(need) + " bytes)");
+    PTB_REQUIRE((reinterpret_cast<uintptr_t>(ws) & 255) == 0, "conv: workspace must be 256-byte aligned");
+}
+
+}  // namespace
+
+void validate_geom(const pt_conv_geom* gp) {
+    PTB_REQUIRE(gp != nullptr, "conv geometry: null");
+    const pt_conv_geom& g = *gp;
+    PTB_REQUIRE(g.N >= 1 && g.C >= 1 && g.H >= 1 && g.W >= 1 && g.K >= 1 && g.kH >= 1 &&
+                    g.kW >= 1 && g.strideH >= 1 && g.strideW >= 1,
+                "conv geometry: counts, dims, kernel and stride must be >= 1");
+    PTB_REQUIRE(g.padH >= 0 && g.padW >= 0, "conv geometry: padding must be >= 0");
+    PTB_REQUIRE(g.kH <= g.H + 2 * g.padH && g.kW <= g.W + 2 * g.padW,
+                "conv geometry: kernel exceeds padded input (" + geom_str(g) + ")");
+    const Geo d(g);
+    PTB_REQUIRE(d.oH >= 1 && d.oW >= 1, "conv geometry: empty output (" + geom_str(g) + ")");
+    // device kernels index spatial/channel extents in 32-bit
+    PTB_REQUIRE(g.C < (1 << 24) && g.K < (1 << 24) && g.H < (1 << 20) && g.W < (1 << 20) &&
+                    g.kH < 4096 && g.kW < 4096 && d.M < (1ll << 31),
+                "conv geometry: extents exceed device limits (" + geom_str(g) + ")");
+}
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+    int n = 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+    if (dev >= 0 && dev < 64) cached[dev] = n;
+    return n;
+}
+
+}  // namespace ptb
+
+using namespace ptb;
+
+extern "C" {
+
+int pt_b200_abi_version(void) { return PT_B200_ABI_VERSION; }
+
+const char* pt_b200_last_error(void) { return g_last_error.c_str(); }
+
+int pt_b200_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int usable = 0;
+    for (int i = 0; i < n; ++i) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10 && p.minor == 0) ++usable;
+    }
+    return usable;
+}
+
+int pt_b200_device_info(int device, pt_device_desc* out) {
+    return guarded([&] {
+        PTB_REQUIRE(out != nullptr, "device_info: null output");
+        cudaDeviceProp p;
+        PTB_CUDA(cudaGetDeviceProperties(&p, device));
+        memset(out, 0, sizeof *out);
+        snprintf(out->name, sizeof out->name, "b200:%d", device);
+        out->maxWorkgroupSize = p.maxThreadsPerBlock;
+        out->localMemBytes = (int64_t)p.sharedMemPerBlockOptin;
+        out->smCount = p.multiProcessorCount;
+        out->ccMajor = p.major;
+        out->ccMinor = p.minor;
+        out->globalMemBytes = (int64_t)p.totalGlobalMem;
+    });
+}
+
+int pt_b200_set_device(int device) { return guarded([&] { PTB_CUDA(cudaSetDevice(device)); }); }
+
+int pt_b200_malloc(void** ptr, size_t bytes) {
+    return guarded([&] {
+        PTB_REQUIRE(ptr != nullptr, "malloc: null output");
+        *ptr = nullptr;
+        if (bytes) PTB_CUDA(cudaMalloc(ptr, bytes));
+    });
+}
+
+int pt_b200_free(void* ptr) { return guarded([&] { if (ptr) PTB_CUDA(cudaFree(ptr)); }); }
+
+int pt_b200_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+    return guarded([&] {
+        if (bytes) PTB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+    });
+}
+
+int pt_b200_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
+    return guarded([&] {
+        if (bytes) PTB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+    });
+}
+
+int pt_b200_stream_sync(void* stream) {
+    return guarded([&] { PTB_CUDA(cudaStreamSynchronize(as_stream(stream))); });
+}
+
+int pt_b200_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(n >= 0 && (n == 0 || dst), "fill_uniform: bad arguments");
+        fill_uniform(dst, n, seed, lo, hi, as_stream(stream));
+    });
+}
+
+int pt_b200_conv_validate(const pt_conv_geom* g) { return guarded([&] { validate_geom(g); }); }
+
+size_t pt_b200_conv_workspace_bytes(const pt_conv_geom* gp, int op, int math) {
+    size_t r = 0;
+    const int st = guarded([&] {
+        validate_geom(gp);
+        require_math(math);
+        const Geo g(*gp);
+        switch (op) {
+            case PT_CONV_FWD: r = fwd_ws(g, math); break;
+            case PT_CONV_BWD_DATA: r = bwd_data_ws(g, math); break;
+            case PT_CONV_BWD_FILTER: r = bwd_filter_ws(g, math); break;
+            default: fail_validation("workspace: unknown conv op " + std::to_string(op));
+        }
+    });
+    return st == PT_OK ? r : (size_t)-1;
+}
+
+int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, const float* b,
+                     float* y, int math, void* ws, size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_math(math);
+        require_ptr(x, "input");
+        require_ptr(w, "weight");
+        require_ptr(y, "output");
+        const Geo g(*gp);
+        cudaStream_t st = as_stream(stream);
+        if (math == PT_MATH_TF32) {
+            const UmmaPlan pl = umma_plan(g, false);
+            if (pl.ok) {
+                require_ws(ws_bytes, pl.ws_bytes, ws);
+                umma_conv_fwd(g, pl, x, w, b, y, ws, st);
+                return;
+            }
+        }
+        simt_conv_fwd(g, x, w, b, y, st);
+    });
+}
+
+int pt_b200_conv_bwd_data(const pt_conv_geom* gp, const float* gy, const float* w, float* gx,
+                          int math, void* ws, size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_math(math);
+        require_ptr(gy, "gradOutput");
+        require_ptr(w, "weight");
+        require_ptr(gx, "gradInput");
+        const Geo g(*gp);
+        cudaStream_t st = as_stream(stream);
+        if (math == PT_MATH_TF32) {
+            const UmmaPlan pl = umma_plan(g, true);
+            if (pl.ok) {
+                require_ws(ws_bytes, pl.ws_bytes, ws);
+                umma_conv_bwd_data(g, pl, gy, w, gx, ws, st);
+                return;
+            }
+        }
+        simt_conv_bwd_data(g, gy, w, gx, st);
+    });
+}
+
+int pt_b200_conv_bwd_filter(const pt_conv_geom* gp, const float* x, const float* gy, float* gw,
+                            float* gb, float scale, int accumulate, int math, void* ws,
+                            size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_math(math);
+        require_ptr(x, "input");
+        require_ptr(gy, "gradOutput");
+        require_ptr(gw, "gradWeight");
+        const Geo g(*gp);
+        cudaStream_t st = as_stream(stream);
+        const size_t need = bwd_filter_ws(g, math);
+        require_ws(ws_bytes, need, ws);
+        float* wsf = reinterpret_cast<float*>(ws);
+        simt_conv_bwd_filter(g, x, gy, gw, scale, accumulate, wsf, st);
+        if (gb) {
+            float* bws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
+                                                  align_up(simt_wgrad_workspace(g), 256));
+            bias_grad(gy, gb, g.N, g.K, g.oHW, scale, accumulate, bws,
+                      align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256), st);
+        }
+    });
+}
+
+int pt_b200_im2col(const pt_conv_geom* gp, const float* img, float* col, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_ptr(img, "image");
+        require_ptr(col, "columns");
+        im2col_launch(Geo(*gp), img, 0, 1, col, as_stream(stream));
+    });
+}
+
+int pt_b200_im2col_batched(const pt_conv_geom* gp, const float* x, int64_t n0, int64_t count,
+                           float* col, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_ptr(x, "input");
+        require_ptr(col, "columns");
+        PTB_REQUIRE(count >= 1 && n0 >= 0 && n0 + count <= gp->N,
+                    "im2col_batched: invalid batch chunk");
+        im2col_launch(Geo(*gp), x, n0, count, col, as_stream(stream));
+    });
+}
+
+int pt_b200_col2im(const pt_conv_geom* gp, const float* col, float* img, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_ptr(img, "image");
+        require_ptr(col, "columns");
+        col2im_launch(Geo(*gp), col, img, as_stream(stream));
+    });
+}
+
+int pt_b200_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float alpha,
+                 const float* A, int64_t lda, const float* B, int64_t ldb, float beta, float* C,
+                 int64_t ldc, int math, void* stream) {
+    return guarded([&] {
+        require_math(math);
+        PTB_REQUIRE(M >= 1 && N >= 1 && K >= 1, "gemm: dims must be >= 1");
+        PTB_REQUIRE(lda >= (transA ? M : K) && ldb >= (transB ? K : N) && ldc >= N,
+                    "gemm: leading dimensions smaller than the matrix extent");
+        PTB_REQUIRE(A && B && C, "gemm: null matrix");
+        PTB_REQUIRE(M < (1ll << 31) / 64 * 64, "gemm: M too large");
+        simt_gemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, as_stream(stream));
+    });
+}
+
+int pt_b200_apply(const int32_t* code, int32_t ncode, int arity, float* const* bases,
+                  const pt_view* views, float scalar, void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(arity >= 1 && arity <= 3, "apply takes 1..3 operands, got " + std::to_string(arity));
+        PTB_REQUIRE(code && bases && views, "apply: null argument");
+        for (int t = 0; t < arity; ++t) {
+            require_view(views[t], "apply operand");
+            PTB_REQUIRE(bases[t] != nullptr, "apply operand is undefined");
+            PTB_REQUIRE(views[t].ndim == views[0].ndim, "apply operands must share sizes");
+            for (int d = 0; d < views[0].ndim; ++d)
+                PTB_REQUIRE(views[t].sizes[d] == views[0].sizes[d], "apply operands must share sizes");
+        }
+        // stack discipline check (the program must leave exactly one value)
+        int depth = 0;
+        for (int32_t pc = 0; pc < ncode; ++pc) {
+            const int op = code[pc] & 0xff;
+            if (op == PT_OP_CONST) { ++depth; ++pc; }
+            else if (op >= PT_OP_X && op <= PT_OP_S) {
+                PTB_REQUIRE(op - PT_OP_X < arity || op == PT_OP_S, "apply: operand beyond arity");
+                ++depth;
+            } else if (op == PT_OP_ADD || op == PT_OP_SUB || op == PT_OP_MUL || op == PT_OP_DIV ||
+                       op == PT_OP_MAX || op == PT_OP_MIN) --depth;
+            else PTB_REQUIRE(op >= PT_OP_NEG && op <= PT_OP_TANH, "apply: bad opcode");
+            PTB_REQUIRE(depth >= 1 && depth <= 32, "apply: malformed program");
+        }
+        PTB_REQUIRE(depth == 1, "apply: malformed program");
+        apply_launch(code, ncode, arity, bases, views, scalar, as_stream(stream));
+    });
+}
+
+int pt_b200_bias_add(float* y, const float* b, int64_t N, int64_t K, int64_t HW, void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(y && b && N >= 1 && K >= 1 && HW >= 1, "bias_add: bad arguments");
+        bias_add_launch(y, b, N, K, HW, as_stream(stream));
+    });
+}
+
+int pt_b200_reduce_all(int op, const float* base, const pt_view* view, float* out_dev, void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(op >= 0 && op <= 2, "reduce: unknown op");
+        PTB_REQUIRE(base && view && out_dev, "reduce on an undefined tensor");
+        require_view(*view, "reduce");
+        reduce_all_launch(op, base, *view, out_dev, as_stream(stream));
+    });
+}
+
+int pt_b200_reduce_dim(int op, const float* base, const pt_view* view, int dim, float* out,
+                       void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(op >= 0 && op <= 2, "reduce: unknown op");
+        PTB_REQUIRE(base && view && out, "reduce on an undefined tensor");
+        require_view(*view, "reduce");
+        PTB_REQUIRE(dim >= 0 && dim < view->ndim,
+                    "reduce dim " + std::to_string(dim) + " out of range for rank " +
+                        std::to_string(view->ndim));
+        reduce_dim_launch(op, base, *view, dim, out, as_stream(stream));
+    });
+}
+
+int64_t pt_b200_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+// kernels.cuh — internal (C++) entry points shared between the .cu files of
+// libpt_b200.so. None of these cross the ABI; include/pt_b200.h is the boundary.
+#pragma once
+
+#include "common.cuh"
+
+namespace ptb {
+
+// ---- simt_conv.cu: FP32-FFMA implicit GEMM on NCHW / KCRS ----
+void simt_conv_fwd(const Geo& g, const float* x, const float* w, const float* b, float* y,
+                   cudaStream_t st);
+void simt_conv_bwd_data(const Geo& g, const float* gy, const float* w, float* gx, cudaStream_t st);
+int simt_wgrad_splits(const Geo& g);
+size_t simt_wgrad_workspace(const Geo& g);
+void simt_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* gw, float scale,
+                          int accumulate, float* ws, cudaStream_t st);
+void simt_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float alpha,
+               const float* A, int64_t lda, const float* B, int64_t ldb, float beta, float* C,
+               int64_t ldc, cudaStream_t st);
+
+// ---- layout.cu: HBM layout transforms feeding the tensor-core path ----
+// NCHW [N][C][HW] -> NHWC [N][HW][Cp] (channels zero-padded to Cp), optionally
+// rounded to TF32 (cvt.rna).
+void nchw_to_nhwc(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
+                  bool round_tf32, cudaStream_t st);
+// Weight packing for the implicit GEMM B operand. W is KCRS [K][C][kH][kW].
+//  flip=false (fprop): row n = k, tap (r,s),            channel = c   (cin = C)
+//  flip=true  (dgrad): row n = c, tap (kH-1-r,kW-1-s),  channel = k   (cin = K)
+// layout 32: B[n_pad][taps][cin_p]           (Kdim-contiguous rows, SW128 tiles)
+// layout 4 : B[slots_p][n_pad][4], slot = tap*(cin_p/4) + chunk (core-matrix tiles)
+void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW,
+                  bool flip, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
+                  bool round_tf32, cudaStream_t st);
+// gb[k] = (acc ? gb[k] : 0) + scale * sum_{n,p} gy[n][k][p] (fixed-order, deterministic).
+void bias_grad(const float* gy, float* gb, int64_t N, int64_t K, int64_t HW, float scale,
+               int accumulate, float* ws, size_t ws_bytes, cudaStream_t st);
+size_t bias_grad_workspace(int64_t N, int64_t K, int64_t HW);
+
+// ---- umma_conv.cu: tcgen05 kind::tf32 implicit GEMM (fprop, stride-1 dgrad) ----
+struct UmmaPlan {
+    bool ok = false;      // geometry supported by the tensor-core path
+    int cb = 32;          // channel chunk per TMA im2col box (32: SW128, 4: no swizzle)
+    int64_t cin_p = 0;    // padded input channels of the NHWC operand
+    int64_t taps = 0;     // kH*kW
+    int64_t slots_p = 0;  // layout-4 slot count padded to 8
+    int64_t n_rows = 0;   // GEMM N (output channels)
+    int bn = 0;           // N tile
+    int n_tiles = 0;
+    int64_t n_pad = 0;    // n_tiles * bn
+    int64_t act_elems = 0, wt_elems = 0;  // workspace floats
+    size_t ws_bytes = 0;
+};
+// fprop: act = x (C channels, HxW), n_rows = K.  dgrad: act = gy (K channels, oHxoW),
+// n_rows = C, flipped weights, pad' = k-1-pad (stride 1 only).
+UmmaPlan umma_plan(const Geo& g, bool dgrad);
+void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float* w,
+                   const float* b, float* y, void* ws, cudaStream_t st);
+void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
+                        float* gx, void* ws, cudaStream_t st);
+
+// ---- unfold.cu ----
+void im2col_launch(const Geo& g, const float* x, int64_t n0, int64_t count, float* col,
+                   cudaStream_t st);
+void col2im_launch(const Geo& g, const float* col, float* img, cudaStream_t st);
+
+// ---- pointwise.cu ----
+void fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, cudaStream_t st);
+void apply_launch(const int32_t* code, int32_t ncode, int arity, float* const* bases,
+                  const pt_view* views, float scalar, cudaStream_t st);
+void bias_add_launch(float* y, const float* b, int64_t N, int64_t K, int64_t HW, cudaStream_t st);
+void reduce_all_launch(int op, const float* base, const pt_view& v, float* out, cudaStream_t st);
+void reduce_dim_launch(int op, const float* base, const pt_view& v, int dim, float* out,
+                       cudaStream_t st);
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace ptb

@@ -1,0 +1,190 @@
+// layout.cu — HBM-bound layout passes around the tensor-core convolution:
+//   * NCHW -> NHWC (channels-innermost, the layout TMA im2col mode gathers from),
+//     zero-padding channels and rounding to TF32 in the same pass;
+//   * weight packing (KCRS -> implicit-GEMM B operand, optionally flipped for dgrad);
+//   * gradBias, a per-channel reduction of gradOutput (the reference's
+//     reduce over gy.select(1,k), proj/src/reference_backend.cpp:115-127).
+#include "kernels.cuh"
+
+namespace ptb {
+
+namespace {
+
+__device__ __forceinline__ float to_tf32(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+}
+
+// 32x32 tile transpose through smem: reads coalesced along pixels, writes coalesced
+// along channels. grid = (ceil(HW/32), ceil(Cp/32), N), block = 32x8.
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                    int64_t C, int64_t HW, int64_t Cp, int round_tf32) {
+    __shared__ float tile[32][33];
+    const int64_t n = blockIdx.z;
+    const int64_t p0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    const float* s = src + n * C * HW;
+    float* d = dst + n * HW * Cp;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t c = c0 + threadIdx.y + i, p = p0 + threadIdx.x;
+        float v = 0.f;
+        if (c < C && p < HW) v = __ldg(s + c * HW + p);
+        tile[threadIdx.y + i][threadIdx.x] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+        const int64_t p = p0 + threadIdx.y + i, c = c0 + threadIdx.x;
+        if (p < HW && c < Cp) {
+            float v = tile[threadIdx.x][threadIdx.y + i];
+            d[p * Cp + c] = round_tf32 ? to_tf32(v) : v;
+        }
+    }
+}
+
+// Small-channel variant (Cp <= 8): one thread per pixel writes its Cp-vector.
+__global__ void nchw_to_nhwc_small_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                          int64_t N, int64_t C, int64_t HW, int64_t Cp,
+                                          int round_tf32) {
+    const int64_t total = N * HW;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = i / HW, p = i - n * HW;
+        const float* s = src + n * C * HW + p;
+        float* d = dst + i * Cp;
+        for (int64_t c = 0; c < Cp; ++c) {
+            float v = c < C ? __ldg(s + c * HW) : 0.f;
+            d[c] = round_tf32 ? to_tf32(v) : v;
+        }
+    }
+}
+
+__global__ void pack_weights_kernel(const float* __restrict__ w, float* __restrict__ dst,
+                                    int64_t K, int64_t C, int64_t kH, int64_t kW, int flip,
+                                    int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
+                                    int round_tf32) {
+    const int64_t taps = kH * kW;
+    const int64_t total = layout == 32 ? n_pad * taps * cin_p : slots_p * n_pad * 4;
+    const int64_t n_real = flip ? C : K, cin_real = flip ? K : C;
+    const int64_t chunks = cin_p / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t row, tap, ch;
+        if (layout == 32) {
+            ch = i % cin_p;
+            tap = (i / cin_p) % taps;
+            row = i / (cin_p * taps);
+        } else {
+            const int64_t e = i % 4;
+            row = (i / 4) % n_pad;
+            const int64_t slot = i / (4 * n_pad);
+            tap = slot / chunks;
+            ch = (slot % chunks) * 4 + e;
+        }
+        float v = 0.f;
+        if (row < n_real && ch < cin_real && tap < taps) {
+            const int64_t r = tap / kW, s = tap % kW;
+            if (!flip) {
+                v = __ldg(w + ((row * C + ch) * kH + r) * kW + s);
+            } else {  // B[c][(r',s')][k] = W[k][c][kH-1-r'][kW-1-s']
+                v = __ldg(w + ((ch * C + row) * kH + (kH - 1 - r)) * kW + (kW - 1 - s));
+            }
+        }
+        dst[i] = round_tf32 ? to_tf32(v) : v;
+    }
+}
+
+// Stage 1: block (k, split) sums its contiguous share of the N*HW run of channel k.
+__global__ void bias_grad_partial_kernel(const float* __restrict__ gy, float* __restrict__ part,
+                                         int64_t N, int64_t K, int64_t HW, int splits) {
+    const int64_t k = blockIdx.x;
+    const int split = blockIdx.y;
+    const int64_t total = N * HW;
+    const int64_t per = (total + splits - 1) / splits;
+    const int64_t lo = split * per, hi = lo + per < total ? lo + per : total;
+    float acc = 0.f;
+    // walk the images overlapping [lo, hi); consecutive threads read consecutive p
+    for (int64_t n = lo / HW; n * HW < hi; ++n) {
+        const int64_t p0 = lo > n * HW ? lo - n * HW : 0;
+        const int64_t p1 = hi - n * HW < HW ? hi - n * HW : HW;
+        const float* src = gy + (n * K + k) * HW;
+        for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) acc += __ldg(src + p);
+    }
+    __shared__ float red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) part[k * splits + split] = acc;
+    }
+}
+
+__global__ void bias_grad_final_kernel(const float* __restrict__ part, float* __restrict__ gb,
+                                       int64_t K, int splits, float scale, int accumulate) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    float s = 0.f;
+    for (int i = 0; i < splits; ++i) s += part[k * splits + i];
+    gb[k] = (accumulate ? gb[k] : 0.f) + scale * s;
+}
+
+int bias_splits(int64_t N, int64_t K, int64_t HW) {
+    const int64_t per_split = 1 << 16;  // >= 64K elements per block
+    int64_t s = (N * HW + per_split - 1) / per_split;
+    const int64_t want = (4 * (int64_t)sm_count() + K - 1) / K;
+    if (s > want) s = want;
+    if (s < 1) s = 1;
+    if (s > 1024) s = 1024;
+    return (int)s;
+}
+
+}  // namespace
+
+void nchw_to_nhwc(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
+                  bool round_tf32, cudaStream_t st) {
+    if (Cp <= 8) {
+        const int64_t total = N * HW;
+        const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * (int64_t)sm_count());
+        nchw_to_nhwc_small_kernel<<<blocks, 256, 0, st>>>(src, dst, N, C, HW, Cp, round_tf32);
+        after_launch("nchw_to_nhwc_small");
+        return;
+    }
+    PTB_REQUIRE(N <= 65535, "nchw_to_nhwc: batch too large");
+    dim3 grid((unsigned)ceil_div(HW, 32), (unsigned)ceil_div(Cp, 32), (unsigned)N);
+    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, dst, C, HW, Cp, round_tf32);
+    after_launch("nchw_to_nhwc");
+}
+
+void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW,
+                  bool flip, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
+                  bool round_tf32, cudaStream_t st) {
+    const int64_t total = layout == 32 ? n_pad * kH * kW * cin_p : slots_p * n_pad * 4;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * (int64_t)sm_count());
+    pack_weights_kernel<<<blocks, 256, 0, st>>>(w, dst, K, C, kH, kW, flip, layout, n_pad, cin_p,
+                                                slots_p, round_tf32);
+    after_launch("pack_weights");
+}
+
+size_t bias_grad_workspace(int64_t N, int64_t K, int64_t HW) {
+    return sizeof(float) * (size_t)K * (size_t)bias_splits(N, K, HW);
+}
+
+void bias_grad(const float* gy, float* gb, int64_t N, int64_t K, int64_t HW, float scale,
+               int accumulate, float* ws, size_t ws_bytes, cudaStream_t st) {
+    const int splits = bias_splits(N, K, HW);
+    PTB_REQUIRE(ws_bytes >= sizeof(float) * (size_t)K * splits, "bias_grad: workspace too small");
+    PTB_REQUIRE(K <= 2147483647, "bias_grad: K too large");
+    bias_grad_partial_kernel<<<dim3((unsigned)K, (unsigned)splits), 256, 0, st>>>(gy, ws, N, K, HW,
+                                                                                 splits);
+    after_launch("bias_grad_partial");
+    bias_grad_final_kernel<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(ws, gb, K, splits, scale,
+                                                                       accumulate);
+    after_launch("bias_grad_final");
+}
+
+}  // namespace ptb

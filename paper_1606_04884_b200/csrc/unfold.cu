@@ -1,0 +1,86 @@
+// unfold.cu — the standalone unfold / fold ops of the SPEC convolution module.
+//   im2col : proj/templates/im2col.kt.tmpl:9-21 (index maths, zero pad) — pure
+//            copies, so bit-exact with the reference kernel; one thread per
+//            column-matrix element so stores are coalesced along output pixels.
+//   col2im : SPEC.md:371-379 scatter-add, computed in gather form (one thread per
+//            image element, taps summed in (r, s) order from 0.0f) — no atomics,
+//            deterministic, and the same summation order as the oracle's scatter.
+#include "kernels.cuh"
+
+namespace ptb {
+
+namespace {
+
+__global__ void im2col_kernel(const float* __restrict__ x, float* __restrict__ col, int C, int H,
+                              int W, int kH, int kW, int pH, int pW, int sH, int sW, int oH,
+                              int oW, int64_t n0, int64_t count) {
+    const int64_t oHW = (int64_t)oH * oW;
+    const int64_t ld = count * oHW;
+    const int64_t rows = (int64_t)C * kH * kW;
+    const int64_t total = rows * ld;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e / ld, colpos = e - row * ld;
+        const int64_t t = colpos / oHW, pos = colpos - t * oHW;
+        const int c = (int)(row / (kH * kW));
+        const int rs = (int)(row - (int64_t)c * kH * kW);
+        const int r = rs / kW, s = rs - r * kW;
+        const int i = (int)(pos / oW), j = (int)(pos - (int64_t)i * oW);
+        const int h = i * sH - pH + r, w = j * sW - pW + s;
+        const bool inside = (h >= 0) && (h < H) && (w >= 0) && (w < W);
+        const float* img = x + (n0 + t) * (int64_t)C * H * W;
+        col[e] = inside ? img[((int64_t)c * H + h) * W + w] : 0.0f;
+    }
+}
+
+__global__ void col2im_kernel(const float* __restrict__ col, float* __restrict__ img, int C, int H,
+                              int W, int kH, int kW, int pH, int pW, int sH, int sW, int oH,
+                              int oW) {
+    const int64_t oHW = (int64_t)oH * oW;
+    const int64_t total = (int64_t)C * H * W;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e / ((int64_t)H * W));
+        const int hw = (int)(e - (int64_t)c * H * W);
+        const int h = hw / W, w = hw - h * W;
+        float acc = 0.0f;
+        for (int r = 0; r < kH; ++r) {
+            const int hn = h + pH - r;
+            if (hn < 0) break;
+            const int i = hn / sH;
+            if (i * sH != hn || i >= oH) continue;
+            for (int s = 0; s < kW; ++s) {
+                const int wn = w + pW - s;
+                if (wn < 0) break;
+                const int j = wn / sW;
+                if (j * sW != wn || j >= oW) continue;
+                acc += col[((int64_t)(c * kH + r) * kW + s) * oHW + (int64_t)i * oW + j];
+            }
+        }
+        img[e] = acc;
+    }
+}
+
+}  // namespace
+
+void im2col_launch(const Geo& g, const float* x, int64_t n0, int64_t count, float* col,
+                   cudaStream_t st) {
+    const int64_t total = g.CRS * count * g.oHW;
+    if (total == 0) return;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count());
+    im2col_kernel<<<blocks, 256, 0, st>>>(x, col, (int)g.C, (int)g.H, (int)g.W, (int)g.kH,
+                                          (int)g.kW, (int)g.pH, (int)g.pW, (int)g.sH, (int)g.sW,
+                                          (int)g.oH, (int)g.oW, n0, count);
+    after_launch("im2col");
+}
+
+void col2im_launch(const Geo& g, const float* col, float* img, cudaStream_t st) {
+    const int64_t total = g.C * g.HW;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count());
+    col2im_kernel<<<blocks, 256, 0, st>>>(col, img, (int)g.C, (int)g.H, (int)g.W, (int)g.kH,
+                                          (int)g.kW, (int)g.pH, (int)g.pW, (int)g.sH, (int)g.sW,
+                                          (int)g.oH, (int)g.oW);
+    after_launch("col2im");
+}
+
+}  // namespace ptb

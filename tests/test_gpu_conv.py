@@ -1,0 +1,117 @@
+"""GPU parity: the sm_100a conv passes through the C ABI vs the CPU oracle.
+
+Every device computation below runs in libpt_b200.so (called via ctypes on torch
+device memory). The oracle (oracle/liboracle.so) is only the checker.
+"""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from helpers import (CFG1, LAYERS, TC_GEOMS, check_fp32, check_tf32, conv_inputs, gstr,
+                     spec_random_geometries, with_batch)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _pt():
+    import paper_1606_04884_b200 as pt
+    return pt
+
+
+def _g(g):
+    pt = _pt()
+    return pt.ConvGeometry(g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH,
+                           g.strideW)
+
+
+def _d(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _h(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def run_all(g, math, seed=0x5EED):
+    pt = _pt()
+    x, w, b, gy = conv_inputs(g, seed)
+    G = _g(g)
+    y = pt.conv_forward(G, _d(x), _d(w), _d(b), math=math)
+    gx = pt.conv_backward_input(G, _d(gy), _d(w), math=math)
+    gw, gb = pt.conv_backward_weight(G, _d(x), _d(gy), math=math)
+    return (x, w, b, gy), (_h(y), _h(gx), _h(gw), _h(gb))
+
+
+def oracle_all(g, x, w, b, gy):
+    y = po.conv_direct(g, x, w, b, f64=True)
+    gx = po.conv_backward_input(g, gy, w)
+    gw, gb = po.conv_backward_weight(g, x, gy)
+    return y, gx, gw, gb
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("g", spec_random_geometries(50), ids=gstr)
+def test_spec_random_geometries(g, math):
+    """SPEC.md:436 oracle-equivalence sweep (50 random desk-scale geometries)."""
+    (x, w, b, gy), (y, gx, gw, gb) = run_all(g, math)
+    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
+    oh, ow = po.out_hw(g)
+    crs = g.C * g.kH * g.kW
+    if math == "fp32":
+        check_fp32(y, ry, crs, 1.0, np.abs(w).max(), "fwd")
+        check_fp32(gx, rgx, g.K * g.kH * g.kW, 1.0, np.abs(w).max(), "dgrad")
+        check_fp32(gw, rgw, g.N * oh * ow, 1.0, 1.0, "wgrad")
+    else:
+        check_tf32(y, ry, "fwd")
+        check_tf32(gx, rgx, "dgrad")
+        check_tf32(gw, rgw, "wgrad")
+    np.testing.assert_allclose(gb, rgb, rtol=1e-5, atol=1e-5 * g.N * oh * ow)
+
+
+@pytest.mark.parametrize("g", TC_GEOMS, ids=gstr)
+def test_tensor_core_tiles(g):
+    """tcgen05 tile variants (SW128 / small-C, bn 64..256, ragged tiles) in TF32 mode."""
+    (x, w, b, gy), (y, gx, gw, gb) = run_all(g, "tf32", seed=77)
+    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
+    check_tf32(y, ry, "fwd")
+    check_tf32(gx, rgx, "dgrad")
+    check_tf32(gw, rgw, "wgrad")
+
+
+@pytest.mark.parametrize("g", TC_GEOMS[:4], ids=gstr)
+def test_fp32_mode_tight(g):
+    (x, w, b, gy), (y, gx, gw, gb) = run_all(g, "fp32", seed=78)
+    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
+    oh, ow = po.out_hw(g)
+    check_fp32(y, ry, g.C * g.kH * g.kW, 1.0, np.abs(w).max(), "fwd")
+    check_fp32(gx, rgx, g.K * g.kH * g.kW, 1.0, np.abs(w).max(), "dgrad")
+    check_fp32(gw, rgw, g.N * oh * ow, 1.0, 1.0, "wgrad")
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_cfg1_full(math):
+    """BASELINE configs[0]: batch 16, 3->64, 3x3 pad 1, 32x32 — full size vs oracle."""
+    (x, w, b, gy), (y, gx, gw, gb) = run_all(CFG1, math)
+    ry, rgx, rgw, rgb = oracle_all(CFG1, x, w, b, gy)
+    if math == "tf32":
+        for o, r, n in ((y, ry, "fwd"), (gx, rgx, "dgrad"), (gw, rgw, "wgrad")):
+            check_tf32(o, r, n)
+    else:
+        check_fp32(y, ry, 27, 1.0, np.abs(w).max(), "fwd")
+        check_fp32(gx, rgx, 64 * 9, 1.0, np.abs(w).max(), "dgrad")
+        check_fp32(gw, rgw, 16 * 1024, 1.0, 1.0, "wgrad")
+    np.testing.assert_allclose(gb, rgb, rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("name", list(LAYERS))
+def test_convnet_layers_batch_slice(name):
+    """L1-L5 at the real per-image shape on a 2-image slice (fwd/dgrad are per-image
+    independent; the full-batch runs are covered by property tests)."""
+    g = with_batch(LAYERS[name], 2)
+    (x, w, b, gy), (y, gx, gw, gb) = run_all(g, "tf32", seed=99)
+    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
+    check_tf32(y, ry, f"{name} fwd")
+    check_tf32(gx, rgx, f"{name} dgrad")
+    check_tf32(gw, rgw, f"{name} wgrad")
