@@ -291,8 +291,7 @@ def main():
         for s in st:
             g = s["g"]
             pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math)
-            pt.conv_backward_input(g, s["gy"], s["w"], s["gx"], math=args.math)
-            pt.conv_backward_weight(g, s["x"], s["gy"], s["gw"], s["gb"], math=args.math)
+            pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math)
             if comm is not None:  # batch-sharded DP: allreduce(sum) gradW/gradB, overlapped
                 ev = torch.cuda.Event()
                 ev.record(cur)
@@ -417,8 +416,7 @@ def e2e(args, pt, torch, layers, dev, world, rank, dist):
             b = d["b"].to(dev, non_blocking=True)
             gy = d["gy"].to(dev, non_blocking=True)
             y = pt.conv_forward(g, x, w, b, math=args.math)
-            gx = pt.conv_backward_input(g, gy, w, math=args.math)
-            gw, gb = pt.conv_backward_weight(g, x, gy, math=args.math)
+            gx, gw, gb = pt.conv_backward(g, x, gy, w, math=args.math)
             if world > 1:
                 dist.all_reduce(gw)
                 dist.all_reduce(gb)

@@ -45,7 +45,7 @@ typedef struct pt_conv_geom {
 enum pt_math { PT_MATH_TF32 = 0, PT_MATH_FP32 = 1 };
 
 /* Which conv pass a workspace query is for. */
-enum pt_conv_op { PT_CONV_FWD = 0, PT_CONV_BWD_DATA = 1, PT_CONV_BWD_FILTER = 2 };
+enum pt_conv_op { PT_CONV_FWD = 0, PT_CONV_BWD_DATA = 1, PT_CONV_BWD_FILTER = 2, PT_CONV_BWD = 3 };
 
 /* Strided view (Tensor sizes/strides/storageOffset, proj/include/portten/tensor.hpp:56-120).
  * Rank 1..8 (kMaxDims, tensor.hpp:29); strides in elements, non-negative. */
@@ -113,6 +113,12 @@ int pt_b200_conv_bwd_data(const pt_conv_geom* g, const float* gy, const float* w
 int pt_b200_conv_bwd_filter(const pt_conv_geom* g, const float* x, const float* gy, float* gw,
                             float* gb, float scale, int accumulate, int math, void* ws,
                             size_t ws_bytes, void* stream);
+/* Torch backward() = updateGradInput + accGradParameters in one call: one NHWC
+ * transform of gy (with gradBias fused) feeds both tensor-core passes. gx may be NULL
+ * (first layer: no gradInput), gw may be NULL (gradInput only); gb may be NULL. */
+int pt_b200_conv_bwd(const pt_conv_geom* g, const float* x, const float* gy, const float* w,
+                     float* gx, float* gw, float* gb, float scale, int accumulate, int math,
+                     void* ws, size_t ws_bytes, void* stream);
 /* Standalone unfold of ONE image, bit-exact with proj/templates/im2col.kt.tmpl:9-21. */
 int pt_b200_im2col(const pt_conv_geom* g, const float* img, float* col, void* stream);
 /* Batched unfold: images [n0, n0+count) into (CRS) x (count*oHW). */

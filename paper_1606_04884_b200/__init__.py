@@ -4,7 +4,8 @@ include/pt_b200.h); this package is the Python host mirror used by tests and ben
 """
 from ._lib import (BackendError, LibraryMissing, ValidationError, PT_MATH_FP32,  # noqa: F401
                    PT_MATH_TF32, lib)
-from .conv import (ConvGeometry, conv_backward_input, conv_backward_weight,  # noqa: F401
+from .conv import (ConvGeometry, conv_backward, conv_backward_input,  # noqa: F401
+                   conv_backward_weight,
                    conv_forward, conv_im2col_batched, col2im, im2col, im2col_batched, gemm,
                    bias_add, fill_uniform, launch_count, device_count)
 from .nn import SpatialConvolutionMM  # noqa: F401

@@ -16,7 +16,7 @@ LIBPATH = os.path.join(LIBDIR, "libpt_b200.so")
 
 PT_OK, PT_EVALIDATION, PT_EBACKEND = 0, 2, 3
 PT_MATH_TF32, PT_MATH_FP32 = 0, 1
-PT_CONV_FWD, PT_CONV_BWD_DATA, PT_CONV_BWD_FILTER = 0, 1, 2
+PT_CONV_FWD, PT_CONV_BWD_DATA, PT_CONV_BWD_FILTER, PT_CONV_BWD = 0, 1, 2, 3
 PT_REDUCE_SUM, PT_REDUCE_MAX, PT_REDUCE_MIN = 0, 1, 2
 
 
@@ -74,6 +74,8 @@ _SIGS = {
                                         C.c_size_t, _P]),
     "pt_b200_conv_bwd_filter": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, C.c_float,
                                           C.c_int, C.c_int, _P, C.c_size_t, _P]),
+    "pt_b200_conv_bwd": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, _P, _P, C.c_float,
+                                   C.c_int, C.c_int, _P, C.c_size_t, _P]),
     "pt_b200_im2col": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P]),
     "pt_b200_im2col_batched": (C.c_int, [C.POINTER(PtConvGeom), _P, C.c_int64, C.c_int64, _P,
                                          _P]),

@@ -203,6 +203,31 @@ def conv_backward_weight(g: ConvGeometry, x, gy, gw=None, gb=None, scale: float 
     return gw, gb
 
 
+def conv_backward(g: ConvGeometry, x, gy, w, gx=None, gw=None, gb=None, scale: float = 1.0,
+                  accumulate: bool = False, need_input_grad: bool = True, with_bias: bool = True,
+                  math="tf32"):
+    """Torch backward() = updateGradInput + accGradParameters in one C-ABI call
+    (pt_b200_conv_bwd): one NHWC transform of gy, gradBias fused into it, feeds both
+    tensor-core passes. Returns (gx, gw, gb); gx is None when need_input_grad=False."""
+    gc, m = g.c(), _math(math)
+    check(lib().pt_b200_conv_validate(C.byref(gc)))
+    if gx is None and need_input_grad:
+        gx = torch.empty(g.input_shape(), dtype=torch.float32, device=gy.device)
+    if gw is None:
+        gw = torch.zeros(g.weight_shape(), dtype=torch.float32, device=gy.device)
+    if gb is None and with_bias:
+        gb = torch.zeros((g.outChannels,), dtype=torch.float32, device=gy.device)
+    ws, wsn = WORKSPACE.get(workspace_bytes(g, _lib.PT_CONV_BWD, m))
+    check(lib().pt_b200_conv_bwd(
+        C.byref(gc), _dev(x, g.input_shape(), "input"), _dev(gy, g.output_shape(), "gradOutput"),
+        _dev(w, g.weight_shape(), "weight"),
+        _dev(gx, g.input_shape(), "gradInput") if gx is not None else None,
+        _dev(gw, g.weight_shape(), "gradWeight"),
+        _dev(gb, (g.outChannels,), "gradBias") if gb is not None else None,
+        float(scale), int(bool(accumulate)), m, ws or None, wsn, _stream()))
+    return gx, gw, gb
+
+
 def im2col(g: ConvGeometry, img):
     """One image C x H x W -> (C*kH*kW) x (oH*oW), bit-exact with im2col.kt.tmpl:9-21."""
     gc = g.c()

@@ -69,8 +69,52 @@ size_t bwd_data_ws(const Geo& g, int math) {
     }
     return 0;
 }
-size_t bwd_filter_ws(const Geo& g, int) {
+bool wgrad_tc(const Geo& g, int math) { return math == PT_MATH_TF32 && umma_wgrad_ok(g); }
+size_t gyh_bytes(const Geo& g) { return align_up((size_t)(g.M * umma_wgrad_kp(g)) * 4, 256); }
+size_t bias_part_bytes(const Geo& g) { return align_up(nhwc_bias_partials_bytes(g.N, g.K, g.oHW), 256); }
+// TF32 wgrad workspace: [gy NHWC + fused gradBias partials][wgrad kernel scratch]
+// FP32 wgrad workspace: [split-K partials][gradBias partials]
+size_t bwd_filter_ws(const Geo& g, int math) {
+    if (wgrad_tc(g, math))
+        return gyh_bytes(g) + bias_part_bytes(g) + align_up(umma_wgrad_workspace(g), 256);
     return align_up(simt_wgrad_workspace(g), 256) + align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256);
+}
+// Combined backward shares the gy transform when dgrad's gy operand has wgrad's layout.
+bool bwd_shared(const Geo& g, int math, UmmaPlan* out = nullptr) {
+    if (!wgrad_tc(g, math)) return false;
+    const UmmaPlan pl = umma_plan(g, true);
+    if (out) *out = pl;
+    return pl.ok && pl.cb == 32 && pl.cin_p == umma_wgrad_kp(g);
+}
+size_t bwd_ws(const Geo& g, int math) {
+    UmmaPlan pl;
+    if (bwd_shared(g, math, &pl))
+        return gyh_bytes(g) + bias_part_bytes(g) + align_up(pl.ws_bytes, 256) +
+               align_up(umma_wgrad_workspace(g), 256);
+    return std::max(bwd_data_ws(g, math), bwd_filter_ws(g, math));
+}
+
+// accGradParameters body; ws laid out as bwd_filter_ws describes.
+void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, float* gb, float scale,
+                     int accumulate, int math, char* ws, cudaStream_t st) {
+    if (wgrad_tc(g, math)) {
+        float* gyh = reinterpret_cast<float*>(ws);
+        float* part = reinterpret_cast<float*>(ws + gyh_bytes(g));
+        {
+            ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
+            nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate,
+                              part, st);
+        }
+        umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, ws + gyh_bytes(g) + bias_part_bytes(g),
+                             st, gyh);
+        return;
+    }
+    simt_conv_bwd_filter(g, x, gy, gw, scale, accumulate, reinterpret_cast<float*>(ws), st);
+    if (gb) {
+        float* bws = reinterpret_cast<float*>(ws + align_up(simt_wgrad_workspace(g), 256));
+        bias_grad(gy, gb, g.N, g.K, g.oHW, scale, accumulate, bws,
+                  align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256), st);
+    }
 }
 
 void require_ws(size_t have, size_t need, const void* ws) {
@@ -197,6 +241,7 @@ size_t pt_b200_conv_workspace_bytes(const pt_conv_geom* gp, int op, int math) {
             case PT_CONV_FWD: r = fwd_ws(g, math); break;
             case PT_CONV_BWD_DATA: r = bwd_data_ws(g, math); break;
             case PT_CONV_BWD_FILTER: r = bwd_filter_ws(g, math); break;
+            case PT_CONV_BWD: r = bwd_ws(g, math); break;
             default: fail_validation("workspace: unknown conv op " + std::to_string(op));
         }
     });
@@ -260,14 +305,47 @@ int pt_b200_conv_bwd_filter(const pt_conv_geom* gp, const float* x, const float*
         cudaStream_t st = as_stream(stream);
         const size_t need = bwd_filter_ws(g, math);
         require_ws(ws_bytes, need, ws);
-        float* wsf = reinterpret_cast<float*>(ws);
-        simt_conv_bwd_filter(g, x, gy, gw, scale, accumulate, wsf, st);
-        if (gb) {
-            float* bws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
-                                                  align_up(simt_wgrad_workspace(g), 256));
-            bias_grad(gy, gb, g.N, g.K, g.oHW, scale, accumulate, bws,
-                      align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256), st);
+        bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st);
+    });
+}
+
+int pt_b200_conv_bwd(const pt_conv_geom* gp, const float* x, const float* gy, const float* w,
+                     float* gx, float* gw, float* gb, float scale, int accumulate, int math,
+                     void* ws, size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_math(math);
+        require_ptr(gy, "gradOutput");
+        PTB_REQUIRE(gx || gw, "conv bwd: nothing to compute (gradInput and gradWeight both null)");
+        if (gx) require_ptr(w, "weight");
+        if (gw) require_ptr(x, "input");
+        const Geo g(*gp);
+        cudaStream_t st = as_stream(stream);
+        require_ws(ws_bytes, bwd_ws(g, math), ws);
+        char* base = reinterpret_cast<char*>(ws);
+        UmmaPlan pl;
+        if (gx && gw && bwd_shared(g, math, &pl)) {
+            // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
+            float* gyh = reinterpret_cast<float*>(base);
+            float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
+            char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
+            char* wws = dws + align_up(pl.ws_bytes, 256);
+            {
+                ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
+                nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate,
+                                  part, st);
+            }
+            umma_conv_bwd_data(g, pl, gy, w, gx, dws, st, gyh);
+            umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, wws, st, gyh);
+            return;
         }
+        if (gx) {
+            if (math == PT_MATH_TF32 && (pl = umma_plan(g, true)).ok)
+                umma_conv_bwd_data(g, pl, gy, w, gx, ws, st);
+            else
+                simt_conv_bwd_data(g, gy, w, gx, st);
+        }
+        if (gw) bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st);
     });
 }
 

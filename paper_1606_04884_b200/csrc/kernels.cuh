@@ -23,14 +23,22 @@ void simt_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float al
 // rounded to TF32 (cvt.rna).
 void nchw_to_nhwc(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
                   bool round_tf32, cudaStream_t st);
+// Same transform (TF32-rounded) of gradOutput with gradBias fused: per-block channel
+// sums of the unrounded values land in `part` (nhwc_bias_partials_bytes) and a
+// fixed-order reduce writes gb (+)= scale * sum. gb may be null (no bias).
+size_t nhwc_bias_partials_bytes(int64_t N, int64_t C, int64_t HW);
+void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
+                       float* gb, float scale, int accumulate, float* part, cudaStream_t st);
 // Weight packing for the implicit GEMM B operand. W is KCRS [K][C][kH][kW].
-//  flip=false (fprop): row n = k, tap (r,s),            channel = c   (cin = C)
-//  flip=true  (dgrad): row n = c, tap (kH-1-r,kW-1-s),  channel = k   (cin = K)
+//  kPackFprop     : row n = k,         tap (r,s),           channel = c  (cin = C)
+//  kPackDgradFlip : row n = c,         tap (kH-1-r,kW-1-s), channel = k  (cin = K)
+//  kPackGcol      : row n = (c,r,s),   single tap,          channel = k  (cin = K)
 // layout 32: B[n_pad][taps][cin_p]           (Kdim-contiguous rows, SW128 tiles)
 // layout 4 : B[slots_p][n_pad][4], slot = tap*(cin_p/4) + chunk (core-matrix tiles)
+enum PackMode { kPackFprop = 0, kPackDgradFlip = 1, kPackGcol = 2 };
 void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW,
-                  bool flip, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
-                  bool round_tf32, cudaStream_t st);
+                  int mode, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
+                  int64_t total_elems, bool round_tf32, cudaStream_t st);
 // gb[k] = (acc ? gb[k] : 0) + scale * sum_{n,p} gy[n][k][p] (fixed-order, deterministic).
 void bias_grad(const float* gy, float* gb, int64_t N, int64_t K, int64_t HW, float scale,
                int accumulate, float* ws, size_t ws_bytes, cudaStream_t st);
@@ -38,8 +46,12 @@ size_t bias_grad_workspace(int64_t N, int64_t K, int64_t HW);
 
 // ---- umma_conv.cu: tcgen05 kind::tf32 implicit GEMM (fprop, stride-1 dgrad) ----
 struct UmmaPlan {
+    enum Mode { kFprop = 0, kDgradTconv = 1, kDgradGcol = 2 };
     bool ok = false;      // geometry supported by the tensor-core path
+    int mode = kFprop;
+    int64_t extra_elems = 0;  // gcol scratch (kDgradGcol)
     int cb = 32;          // channel chunk per TMA im2col box (32: SW128, 4: no swizzle)
+    int cg = 1;           // CTAs per MMA (2: cta_group::2 pair, M = 256)
     int64_t cin_p = 0;    // padded input channels of the NHWC operand
     int64_t taps = 0;     // kH*kW
     int64_t slots_p = 0;  // layout-4 slot count padded to 8
@@ -50,18 +62,31 @@ struct UmmaPlan {
     int64_t act_elems = 0, wt_elems = 0;  // workspace floats
     size_t ws_bytes = 0;
 };
-// fprop: act = x (C channels, HxW), n_rows = K.  dgrad: act = gy (K channels, oHxoW),
-// n_rows = C, flipped weights, pad' = k-1-pad (stride 1 only).
+// fprop: act = x (C channels, HxW), n_rows = K.
+// dgrad, kDgradTconv: act = gy (K channels, oHxoW), n_rows = C, flipped weights,
+//   pad' = k-1-pad (stride 1).  kDgradGcol (small C / strided): gcol = W^T gy as a
+//   1x1 conv over gy (n_rows = CRS) then a gather col2im.
 UmmaPlan umma_plan(const Geo& g, bool dgrad);
 void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float* w,
                    const float* b, float* y, void* ws, cudaStream_t st);
+// gyh_pre: gy already in NHWC [N][oHW][pl.cin_p] (TF32-rounded), or null to transform here.
 void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
-                        float* gx, void* ws, cudaStream_t st);
+                        float* gx, void* ws, cudaStream_t st, const float* gyh_pre = nullptr);
+
+// ---- umma_wgrad.cu: tcgen05 kind::tf32 weight gradient (MN-major operands, split-K) ----
+bool umma_wgrad_ok(const Geo& g);
+size_t umma_wgrad_workspace(const Geo& g);
+// gyh_pre: gy already in NHWC [M][round_up(K,32)] (TF32-rounded), or null.
+void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* gw, float scale,
+                          int accumulate, void* ws, cudaStream_t st, const float* gyh_pre = nullptr);
+int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 
 // ---- unfold.cu ----
 void im2col_launch(const Geo& g, const float* x, int64_t n0, int64_t count, float* col,
                    cudaStream_t st);
 void col2im_launch(const Geo& g, const float* col, float* img, cudaStream_t st);
+// gcol [N][CRS][oHW] -> gx [N][C][H][W]
+void col2im_batched_launch(const Geo& g, const float* col, float* img, cudaStream_t st);
 
 // ---- pointwise.cu ----
 void fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, cudaStream_t st);

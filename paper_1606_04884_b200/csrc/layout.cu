@@ -16,30 +16,73 @@ __device__ __forceinline__ float to_tf32(float v) {
     return __uint_as_float(r);
 }
 
-// 32x32 tile transpose through smem: reads coalesced along pixels, writes coalesced
-// along channels. grid = (ceil(HW/32), ceil(Cp/32), N), block = 32x8.
+// Tile transpose through smem: a block owns 32 channels x kStripPx pixels of one
+// image, moved as 32x32 tiles (reads coalesced along pixels, writes coalesced along
+// channels). With `part` set it also emits the block's per-channel sums of the
+// UNROUNDED source (the gradBias partials, fixed order -> deterministic):
+// part[(n * strips + strip) * C + c]. grid = (strips, ceil(Cp/32), N), block = 32x8.
+constexpr int kStripPx = 128;
+
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst,
-                                    int64_t C, int64_t HW, int64_t Cp, int round_tf32) {
+                                    int64_t C, int64_t HW, int64_t Cp, int round_tf32,
+                                    float* __restrict__ part) {
     __shared__ float tile[32][33];
     const int64_t n = blockIdx.z;
-    const int64_t p0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    const int64_t c0 = (int64_t)blockIdx.y * 32;
     const float* s = src + n * C * HW;
     float* d = dst + n * HW * Cp;
+    float rowsum[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int t = 0; t < kStripPx / 32; ++t) {
+        const int64_t p0 = (int64_t)blockIdx.x * kStripPx + t * 32;
+        if (p0 >= HW) break;
 #pragma unroll
-    for (int i = 0; i < 32; i += 8) {
-        const int64_t c = c0 + threadIdx.y + i, p = p0 + threadIdx.x;
-        float v = 0.f;
-        if (c < C && p < HW) v = __ldg(s + c * HW + p);
-        tile[threadIdx.y + i][threadIdx.x] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 32; i += 8) {
-        const int64_t p = p0 + threadIdx.y + i, c = c0 + threadIdx.x;
-        if (p < HW && c < Cp) {
-            float v = tile[threadIdx.x][threadIdx.y + i];
-            d[p * Cp + c] = round_tf32 ? to_tf32(v) : v;
+        for (int i = 0; i < 32; i += 8) {
+            const int64_t c = c0 + threadIdx.y + i, p = p0 + threadIdx.x;
+            float v = 0.f;
+            if (c < C && p < HW) v = __ldg(s + c * HW + p);
+            tile[threadIdx.y + i][threadIdx.x] = v;
+            rowsum[i / 8] += v;
         }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+            const int64_t p = p0 + threadIdx.y + i, c = c0 + threadIdx.x;
+            if (p < HW && c < Cp) {
+                float v = tile[threadIdx.x][threadIdx.y + i];
+                d[p * Cp + c] = round_tf32 ? to_tf32(v) : v;
+            }
+        }
+        __syncthreads();
+    }
+    if (part) {
+        // reduce each channel row's 32 lanes (warp = fixed threadIdx.y -> fixed channels)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float v = rowsum[i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            const int64_t c = c0 + threadIdx.y + 8 * i;
+            if (threadIdx.x == 0 && c < C) part[(n * gridDim.x + blockIdx.x) * C + c] = v;
+        }
+    }
+}
+
+// gb[k] = (acc ? gb[k] : 0) + scale * sum_r part[r * K + k], r over N*strips in order.
+__global__ void bias_from_partials_kernel(const float* __restrict__ part, int64_t rows, int64_t K,
+                                          float* __restrict__ gb, float scale, int accumulate) {
+    const int64_t k = blockIdx.x;
+    float acc = 0.f;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) acc += part[r * K + k];
+    __shared__ float red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) gb[k] = (accumulate ? gb[k] : 0.f) + scale * acc;
     }
 }
 
@@ -61,20 +104,22 @@ __global__ void nchw_to_nhwc_small_kernel(const float* __restrict__ src, float* 
 }
 
 __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restrict__ dst,
-                                    int64_t K, int64_t C, int64_t kH, int64_t kW, int flip,
+                                    int64_t K, int64_t C, int64_t kH, int64_t kW, int mode,
                                     int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
-                                    int round_tf32) {
-    const int64_t taps = kH * kW;
-    const int64_t total = layout == 32 ? n_pad * taps * cin_p : slots_p * n_pad * 4;
-    const int64_t n_real = flip ? C : K, cin_real = flip ? K : C;
+                                    int64_t total, int round_tf32) {
+    const int64_t taps = mode == kPackGcol ? 1 : kH * kW;
+    const int64_t n_real = mode == kPackFprop ? K : (mode == kPackDgradFlip ? C : C * kH * kW);
+    const int64_t cin_real = mode == kPackFprop ? C : K;
     const int64_t chunks = cin_p / 4;
+    const int64_t kdim_p = total / n_pad;  // layout 32: row stride (>= taps*cin_p)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t row, tap, ch;
         if (layout == 32) {
-            ch = i % cin_p;
-            tap = (i / cin_p) % taps;
-            row = i / (cin_p * taps);
+            row = i / kdim_p;
+            const int64_t kd = i - row * kdim_p;
+            tap = kd / cin_p;
+            ch = kd - tap * cin_p;
         } else {
             const int64_t e = i % 4;
             row = (i / 4) % n_pad;
@@ -85,10 +130,12 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restri
         float v = 0.f;
         if (row < n_real && ch < cin_real && tap < taps) {
             const int64_t r = tap / kW, s = tap % kW;
-            if (!flip) {
+            if (mode == kPackFprop) {
                 v = __ldg(w + ((row * C + ch) * kH + r) * kW + s);
-            } else {  // B[c][(r',s')][k] = W[k][c][kH-1-r'][kW-1-s']
+            } else if (mode == kPackDgradFlip) {  // B[c][(r',s')][k] = W[k][c][kH-1-r'][kW-1-s']
                 v = __ldg(w + ((ch * C + row) * kH + (kH - 1 - r)) * kW + (kW - 1 - s));
+            } else {  // B[(c,r,s)][k] = W[k][(c,r,s)]
+                v = __ldg(w + ch * C * kH * kW + row);
             }
         }
         dst[i] = round_tf32 ? to_tf32(v) : v;
@@ -155,18 +202,35 @@ void nchw_to_nhwc(const float* src, float* dst, int64_t N, int64_t C, int64_t HW
         return;
     }
     PTB_REQUIRE(N <= 65535, "nchw_to_nhwc: batch too large");
-    dim3 grid((unsigned)ceil_div(HW, 32), (unsigned)ceil_div(Cp, 32), (unsigned)N);
-    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, dst, C, HW, Cp, round_tf32);
+    dim3 grid((unsigned)ceil_div(HW, kStripPx), (unsigned)ceil_div(Cp, 32), (unsigned)N);
+    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, dst, C, HW, Cp, round_tf32, nullptr);
     after_launch("nchw_to_nhwc");
 }
 
+size_t nhwc_bias_partials_bytes(int64_t N, int64_t C, int64_t HW) {
+    return sizeof(float) * (size_t)(N * ceil_div(HW, kStripPx) * C);
+}
+
+void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
+                       float* gb, float scale, int accumulate, float* part, cudaStream_t st) {
+    PTB_REQUIRE(N <= 65535 && Cp >= C, "nchw_to_nhwc_bias: bad shape");
+    const int64_t strips = ceil_div(HW, kStripPx);
+    dim3 grid((unsigned)strips, (unsigned)ceil_div(Cp, 32), (unsigned)N);
+    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, dst, C, HW, Cp, 1, gb ? part : nullptr);
+    after_launch("nchw_to_nhwc_bias");
+    if (gb) {
+        bias_from_partials_kernel<<<(unsigned)C, 256, 0, st>>>(part, N * strips, C, gb, scale,
+                                                               accumulate);
+        after_launch("bias_from_partials");
+    }
+}
+
 void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW,
-                  bool flip, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
-                  bool round_tf32, cudaStream_t st) {
-    const int64_t total = layout == 32 ? n_pad * kH * kW * cin_p : slots_p * n_pad * 4;
+                  int mode, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
+                  int64_t total, bool round_tf32, cudaStream_t st) {
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * (int64_t)sm_count());
-    pack_weights_kernel<<<blocks, 256, 0, st>>>(w, dst, K, C, kH, kW, flip, layout, n_pad, cin_p,
-                                                slots_p, round_tf32);
+    pack_weights_kernel<<<blocks, 256, 0, st>>>(w, dst, K, C, kH, kW, mode, layout, n_pad, cin_p,
+                                                slots_p, total, round_tf32);
     after_launch("pack_weights");
 }
 

@@ -1,0 +1,372 @@
+// umma_wgrad.cu — tcgen05 (kind::tf32) weight gradient (accGradParameters).
+//
+//   gW^T[(r,s,c)][k] = sum_m im2col(x)[m][(r,s,c)] * gy[m][k]      m = output pixel (n,i,j)
+//
+// CTA-pair GEMM (cta_group::2): M = filter columns (tap, channel) — 256 per pair, 128
+// per CTA as four 32-channel im2col boxes; N = output channels k (BN per tile, each
+// CTA loads BN/2 of them); reduction over pixels, 64 per pipeline stage. In NHWC both
+// operands are MN-major: x by TMA im2col boxes (64 px x 32 ch at filter tap (r,s)),
+// gy by tiled TMA boxes (64 px x 32 ch), landing in the MN-major canonical layout
+// with 32-byte-atom 128B swizzle (SWIZZLE_128B_BASE32B / TMA SWIZZLE_128B_ATOM_32B).
+// The pixel reduction is split over CTA pairs (persistent, static schedule over
+// (column-tile, k-tile, split) units); each unit's FP32 tile is drained from TMEM to a
+// partial buffer and a fixed-order reduce kernel sums the splits (deterministic),
+// applies scale / accumulate and writes KCRS.
+#include <cuda.h>
+
+#include "kernels.cuh"
+#include "tmap.cuh"
+#include "umma.cuh"
+
+namespace ptb {
+
+namespace {
+
+using namespace umma;
+
+constexpr int kPix = 64;                     // pixels (reduction rows) per stage
+constexpr uint32_t kBox = kPix * 128;        // one 64-pixel x 32-channel box: 8 KB
+constexpr uint32_t kStageA = 4 * kBox;       // 128 filter columns per CTA
+constexpr int kThreadsW = 192;
+constexpr int kSmemLimit = 232448;
+
+struct UWgradParams {
+    CUtensorMap tmap_gy;  // tiled [M][Kp], box {32 ch, 64 px}
+    CUtensorMap tmap_x;   // im2col over x NHWC [N][H][W][Cp], box {32 ch, 64 px}
+    int oH, oW, sH, sW, pH, pW, kW;
+    int taps, Cp;
+    int m_tiles, n_tiles, splits;
+    int kb_per_split, total_kb;
+    int bn, stages;
+    uint32_t stage_b, tmem_cols;
+    float* part;          // [splits][m_tiles*256][n_tiles*bn]
+    int64_t part_ld, part_split;
+};
+
+__global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_constant__ UWgradParams p) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((((raw + 1023u) & ~1023u)) - raw);
+    const int S = p.stages;
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + (size_t)S * kStageA;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)S * p.stage_b);
+    uint64_t* empty = full + S;
+    uint64_t* tfull = empty + S;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.tmap_gy);
+        tma_prefetch(&p.tmap_x);
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full[i], 2);   // leader's expect_tx arrive + the peer's arrive
+            mbar_init(&empty[i], 1);  // one multicast commit
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc_cg2(tmem_holder, p.tmem_cols);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int units = p.m_tiles * p.n_tiles * p.splits;
+    const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+    // unit -> (m-tile, n-tile, split), m fastest: consecutive pairs share a pixel range
+    auto decode = [&](int u, int& mt, int& nt, int& sp) {
+        mt = u % p.m_tiles;
+        const int r = u / p.m_tiles;
+        nt = r % p.n_tiles;
+        sp = r / p.n_tiles;
+    };
+    auto kb_count = [&](int sp) {
+        const int lo = sp * p.kb_per_split;
+        const int hi = lo + p.kb_per_split < p.total_kb ? lo + p.kb_per_split : p.total_kb;
+        return hi - lo;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const int nbB = p.bn / 64;  // gy boxes per CTA
+            for (int u = cluster; u < units; u += nclusters) {
+                int mt, nt, sp;
+                decode(u, mt, nt, sp);
+                const int nkb = kb_count(sp);
+                // this CTA's four filter-column boxes: (tap, channel block) -> (r, s, c0)
+                int bc[4], br[4], bs[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int col = mt * 256 + (int)rank * 128 + b * 32;
+                    int tap = col / p.Cp;
+                    bc[b] = col - tap * p.Cp;
+                    if (tap >= p.taps) tap = 0;  // rows past the filter are never reduced
+                    br[b] = tap / p.kW;
+                    bs[b] = tap - br[b] * p.kW;
+                }
+                const int kbase = nt * p.bn + (int)rank * (p.bn / 2);
+                // pixel cursor (n, i, j) of the first pixel of this split
+                int m = sp * p.kb_per_split * kPix;
+                const int ohw = p.oH * p.oW;
+                int n = m / ohw;
+                int rem = m - n * ohw;
+                int i = rem / p.oW, j = rem - i * p.oW;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* a = sA + (size_t)stage * kStageA;
+                    uint8_t* b = sB + (size_t)stage * p.stage_b;
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kStageA + p.stage_b));
+                    else mbar_arrive_cluster(&full[stage], 0);
+                    const int wc = j * p.sW - p.pW, hc = i * p.sH - p.pH;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        tma_load_im2col_4d_cg2(a + t * kBox, &p.tmap_x, &full[stage], bc[t], wc, hc, n,
+                                               (uint16_t)bs[t], (uint16_t)br[t]);
+                    for (int t = 0; t < nbB; ++t)
+                        tma_load_2d_cg2(b + t * kBox, &p.tmap_gy, &full[stage], kbase + t * 32, m);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    m += kPix;
+                    j += kPix;
+                    while (j >= p.oW) {
+                        j -= p.oW;
+                        if (++i == p.oH) {
+                            i = 0;
+                            ++n;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            const uint32_t idesc = idesc_tf32(256, p.bn, 1, 1);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int u = cluster; u < units; u += nclusters, ++it) {
+                int mt, nt, sp;
+                decode(u, mt, nt, sp);
+                const int nkb = kb_count(sp);
+                const uint32_t acc = it & 1;
+                mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * p.bn;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a = smem_u32(sA + (size_t)stage * kStageA);
+                    const uint32_t b = smem_u32(sB + (size_t)stage * p.stage_b);
+#pragma unroll
+                    for (int k = 0; k < kPix / 8; ++k) {
+                        // MN-major: 32-element atoms along M/N at LBO = one box (8 KB),
+                        // 4-row swizzle groups along K at SBO = 512 B; K=8 rows = +1 KB.
+                        const uint64_t ad = smem_desc(a + k * 1024, kBox, 512, kSwizzle128B_Base32B);
+                        const uint64_t bd = smem_desc(b + k * 1024, kBox, 512, kSwizzle128B_Base32B);
+                        mma_tf32_cg2(d, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    mma_commit_cg2(&empty[stage]);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit_cg2(&tfull[acc]);
+            }
+        }
+    } else {
+        const uint32_t q = warp & 3;
+        int it = 0;
+        for (int u = cluster; u < units; u += nclusters, ++it) {
+            int mt, nt, sp;
+            decode(u, mt, nt, sp);
+            const uint32_t acc = it & 1;
+            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            tc_fence_after();
+            const int row = mt * 256 + (int)rank * 128 + (int)(q * 32 + lane);
+            float* dst = p.part + (int64_t)sp * p.part_split + (int64_t)row * p.part_ld +
+                         (int64_t)nt * p.bn;
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
+            for (int c0 = 0; c0 < p.bn; c0 += 16) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(taddr + c0, v);
+                tmem_ld_wait();
+                float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    d4[jj] = make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
+                                         __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3]));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(&tempty[acc], 0);
+            }
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc_cg2(tmem_base, p.tmem_cols);
+#endif
+}
+
+// gw[k][c][r][s] = (acc ? gw : 0) + scale * sum_sp part[sp][(r*kW+s)*Cp + c][k]
+__global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ gw,
+                                    int64_t K, int64_t C, int64_t kH, int64_t kW, int64_t Cp,
+                                    int splits, int64_t ld, int64_t split_stride, float scale,
+                                    int accumulate) {
+    const int64_t total = K * C * kH * kW;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i % kW, r = (i / kW) % kH, c = (i / (kW * kH)) % C, k = i / (kW * kH * C);
+        const float* src = part + ((r * kW + s) * Cp + c) * ld + k;
+        float acc = 0.f;
+        for (int sp = 0; sp < splits; ++sp) acc += src[(int64_t)sp * split_stride];
+        gw[i] = (accumulate ? gw[i] : 0.f) + scale * acc;
+    }
+}
+
+struct WPlan {
+    int64_t Cp, Kp, kdim;
+    int bn, m_tiles, n_tiles, splits, kb_per_split, total_kb, stages;
+    int64_t x_elems, gy_elems, part_elems;
+};
+
+WPlan wplan(const Geo& g) {
+    WPlan w;
+    w.Cp = (g.C + 31) / 32 * 32;
+    w.Kp = (g.K + 31) / 32 * 32;
+    w.kdim = g.kH * g.kW * w.Cp;
+    w.n_tiles = (int)ceil_div(w.Kp, 256);
+    w.bn = (int)(ceil_div(ceil_div(w.Kp, w.n_tiles), 64) * 64);
+    w.m_tiles = (int)ceil_div(w.kdim, 256);
+    w.total_kb = (int)ceil_div(g.M, kPix);
+    const int64_t tiles = (int64_t)w.m_tiles * w.n_tiles;
+    const int64_t target_units = 2 * (int64_t)sm_count();  // ~4 units per CTA pair
+    int64_t splits = ceil_div(target_units, tiles);
+    int64_t kbps = ceil_div(w.total_kb, splits);
+    if (kbps < 8) kbps = 8;  // >= 512 pixels per unit to amortise the epilogue
+    w.kb_per_split = (int)kbps;
+    w.splits = (int)ceil_div(w.total_kb, kbps);
+    w.stages = (kSmemLimit - 1024 - 256) / (int)(kStageA + (w.bn / 64) * kBox);
+    if (w.stages > 8) w.stages = 8;
+    w.x_elems = g.N * g.HW * w.Cp;
+    w.gy_elems = g.M * w.Kp;
+    w.part_elems = (int64_t)w.splits * w.m_tiles * 256 * w.n_tiles * w.bn;
+    return w;
+}
+
+}  // namespace
+
+bool umma_wgrad_ok(const Geo& g) {
+    if (g.M >= (1ll << 31) || g.N * g.HW >= (1ll << 31)) return false;
+    if (g.pH > 128 || g.pW > 128 || g.kH > 256 || g.kW > 256) return false;
+    if (g.pH - (g.kH - 1) < -128 || g.pW - (g.kW - 1) < -128) return false;
+    if (g.sH > 8 || g.sW > 8) return false;
+    return g.K <= 65536 && g.kH * g.kW * ((g.C + 31) / 32 * 32) < (1ll << 30) && sm_count() >= 2;
+}
+
+size_t umma_wgrad_workspace(const Geo& g) {
+    const WPlan w = wplan(g);
+    return align_up(w.x_elems * 4, 256) + align_up(w.gy_elems * 4, 256) +
+           align_up(w.part_elems * 4, 256);
+}
+
+int64_t umma_wgrad_kp(const Geo& g) { return (g.K + 31) / 32 * 32; }
+
+void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* gw, float scale,
+                          int accumulate, void* ws, cudaStream_t st, const float* gyh_pre) {
+    const WPlan w = wplan(g);
+    char* base = reinterpret_cast<char*>(ws);
+    float* xh = reinterpret_cast<float*>(base);
+    float* gyh = reinterpret_cast<float*>(base + align_up(w.x_elems * 4, 256));
+    float* part = reinterpret_cast<float*>(base + align_up(w.x_elems * 4, 256) +
+                                           align_up(w.gy_elems * 4, 256));
+    {
+        ProfScope prof("layout", st, 0.0,
+                       4.0 * (g.N * g.C * g.HW + w.x_elems +
+                              (gyh_pre ? 0 : g.M * g.K + w.gy_elems)));
+        nchw_to_nhwc(x, xh, g.N, g.C, g.HW, w.Cp, true, st);
+        if (gyh_pre) gyh = const_cast<float*>(gyh_pre);
+        else nchw_to_nhwc(gy, gyh, g.N, g.K, g.oHW, w.Kp, true, st);
+    }
+    UWgradParams p;
+    memset(&p, 0, sizeof p);
+    {
+        const uint64_t dims[2] = {(uint64_t)w.Kp, (uint64_t)g.M};
+        const uint64_t strides[1] = {(uint64_t)w.Kp * 4};
+        const uint32_t box[2] = {32, kPix};
+        tmap_tiled(&p.tmap_gy, gyh, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    }
+    tmap_im2col(&p.tmap_x, xh, g.N, g.H, g.W, w.Cp, (int)g.kH, (int)g.kW, (int)g.pH, (int)g.pW,
+                (int)g.sH, (int)g.sW, 32, kPix, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    p.oH = (int)g.oH;
+    p.oW = (int)g.oW;
+    p.sH = (int)g.sH;
+    p.sW = (int)g.sW;
+    p.pH = (int)g.pH;
+    p.pW = (int)g.pW;
+    p.kW = (int)g.kW;
+    p.taps = (int)(g.kH * g.kW);
+    p.Cp = (int)w.Cp;
+    p.m_tiles = w.m_tiles;
+    p.n_tiles = w.n_tiles;
+    p.splits = w.splits;
+    p.kb_per_split = w.kb_per_split;
+    p.total_kb = w.total_kb;
+    p.bn = w.bn;
+    p.stages = w.stages;
+    p.stage_b = (uint32_t)(w.bn / 64) * kBox;
+    p.tmem_cols = 2 * w.bn <= 256 ? 256 : 512;
+    p.part = part;
+    p.part_ld = (int64_t)w.n_tiles * w.bn;
+    p.part_split = (int64_t)w.m_tiles * 256 * p.part_ld;
+    const size_t smem = 1024 + (size_t)p.stages * (kStageA + p.stage_b) + (2 * p.stages + 4) * 8 + 16;
+    const int units = w.m_tiles * w.n_tiles * w.splits;
+    const int pairs = std::min(units, sm_count() / 2);
+    static bool attr = false;
+    if (!attr) {
+        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemLimit));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreadsW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    {
+        ProfScope prof("umma_wgrad", st, 2.0 * g.M * g.K * g.CRS, 0.0);
+        PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel, p));
+        after_launch("umma_wgrad");
+    }
+    const int64_t n = g.K * g.CRS;
+    wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256,
+                          0, st>>>(part, gw, g.K, g.C, g.kH, g.kW, w.Cp, w.splits, p.part_ld,
+                                   p.part_split, scale, accumulate);
+    after_launch("wgrad_reduce");
+}
+
+}  // namespace ptb

@@ -33,15 +33,21 @@ __global__ void im2col_kernel(const float* __restrict__ x, float* __restrict__ c
     }
 }
 
-__global__ void col2im_kernel(const float* __restrict__ col, float* __restrict__ img, int C, int H,
+// img[n] = col2im(col[n]) for n in [0, N): one thread per image element.
+__global__ void col2im_kernel(const float* __restrict__ colb, float* __restrict__ imgb, int C, int H,
                               int W, int kH, int kW, int pH, int pW, int sH, int sW, int oH,
-                              int oW) {
+                              int oW, int64_t N) {
     const int64_t oHW = (int64_t)oH * oW;
-    const int64_t total = (int64_t)C * H * W;
+    const int64_t per = (int64_t)C * H * W;
+    const int64_t total = per * N;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(e / ((int64_t)H * W));
-        const int hw = (int)(e - (int64_t)c * H * W);
+        const int64_t n = e / per;
+        const int64_t ei = e - n * per;
+        const float* col = colb + n * (int64_t)C * kH * kW * oHW;
+        float* img = imgb + n * per;
+        const int c = (int)(ei / ((int64_t)H * W));
+        const int hw = (int)(ei - (int64_t)c * H * W);
         const int h = hw / W, w = hw - h * W;
         float acc = 0.0f;
         for (int r = 0; r < kH; ++r) {
@@ -57,7 +63,7 @@ __global__ void col2im_kernel(const float* __restrict__ col, float* __restrict__
                 acc += col[((int64_t)(c * kH + r) * kW + s) * oHW + (int64_t)i * oW + j];
             }
         }
-        img[e] = acc;
+        img[ei] = acc;
     }
 }
 
@@ -74,13 +80,21 @@ void im2col_launch(const Geo& g, const float* x, int64_t n0, int64_t count, floa
     after_launch("im2col");
 }
 
-void col2im_launch(const Geo& g, const float* col, float* img, cudaStream_t st) {
-    const int64_t total = g.C * g.HW;
+static void col2im_n(const Geo& g, const float* col, float* img, int64_t n, cudaStream_t st) {
+    const int64_t total = g.C * g.HW * n;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count());
     col2im_kernel<<<blocks, 256, 0, st>>>(col, img, (int)g.C, (int)g.H, (int)g.W, (int)g.kH,
                                           (int)g.kW, (int)g.pH, (int)g.pW, (int)g.sH, (int)g.sW,
-                                          (int)g.oH, (int)g.oW);
+                                          (int)g.oH, (int)g.oW, n);
     after_launch("col2im");
+}
+
+void col2im_launch(const Geo& g, const float* col, float* img, cudaStream_t st) {
+    col2im_n(g, col, img, 1, st);
+}
+
+void col2im_batched_launch(const Geo& g, const float* col, float* img, cudaStream_t st) {
+    col2im_n(g, col, img, g.N, st);
 }
 
 }  // namespace ptb

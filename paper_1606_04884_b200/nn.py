@@ -88,8 +88,13 @@ class SpatialConvolutionMM:
         return self.updateOutput(input)
 
     def backward(self, input, gradOutput, scale=1.0):
-        self.updateGradInput(input, gradOutput)
-        self.accGradParameters(input, gradOutput, scale)
+        """updateGradInput + accGradParameters as one fused C-ABI call (pt_b200_conv_bwd)."""
+        x, host = self._on_device(input)
+        gy, _ = self._on_device(gradOutput)
+        g = self.geometry(x)
+        gx, _, _ = _conv.conv_backward(g, x, gy, self.weight, gw=self.gradWeight, gb=self.gradBias,
+                                       scale=scale, accumulate=True, math=self.math)
+        self.gradInput = gx.cpu() if host else gx
         return self.gradInput
 
     def parameters(self):

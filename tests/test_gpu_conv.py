@@ -105,6 +105,34 @@ def test_cfg1_full(math):
     np.testing.assert_allclose(gb, rgb, rtol=1e-5, atol=1e-3)
 
 
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("g", TC_GEOMS[:6] + [CFG1], ids=gstr)
+def test_fused_backward_matches_separate_passes(g, math):
+    """pt_b200_conv_bwd (shared gy transform, fused gradBias) == the separate ABI passes,
+    and Torch accumulate/scale semantics (gw += scale*dW) hold."""
+    pt = _pt()
+    x, w, b, gy = conv_inputs(g, 31)
+    G = _g(g)
+    gx, gw, gb = pt.conv_backward(G, _d(x), _d(gy), _d(w), math=math)
+    sgx = pt.conv_backward_input(G, _d(gy), _d(w), math=math)
+    sgw, sgb = pt.conv_backward_weight(G, _d(x), _d(gy), math=math)
+    np.testing.assert_array_equal(_h(gx), _h(sgx))
+    np.testing.assert_allclose(_h(gw), _h(sgw), rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(_h(gb), _h(sgb), rtol=1e-5, atol=1e-5)
+    # accumulate: start from gw0, add 0.5 * dW
+    gw0 = po.uniform((g.K, g.C, g.kH, g.kW), 5)
+    gb0 = po.uniform((g.K,), 6)
+    _, agw, agb = pt.conv_backward(G, _d(x), _d(gy), _d(w), gw=_d(gw0), gb=_d(gb0), scale=0.5,
+                                   accumulate=True, need_input_grad=False, math=math)
+    rgw, rgb = po.conv_backward_weight(g, x, gy)
+    oh, ow = po.out_hw(g)
+    if math == "fp32":
+        check_fp32(_h(agw), gw0 + 0.5 * rgw, g.N * oh * ow, 1.0, 1.0, "acc wgrad")
+    else:
+        check_tf32(_h(agw) - gw0, 0.5 * rgw, "acc wgrad")
+    np.testing.assert_allclose(_h(agb), gb0 + 0.5 * rgb, rtol=1e-5, atol=1e-4)
+
+
 @pytest.mark.parametrize("name", list(LAYERS))
 def test_convnet_layers_batch_slice(name):
     """L1-L5 at the real per-image shape on a 2-image slice (fwd/dgrad are per-image
