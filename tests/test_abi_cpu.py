@@ -1,0 +1,115 @@
+"""CPU: the C-ABI library loads and exports every symbol include/pt_b200.h declares;
+host-side validation, error mapping and planning work without a GPU; the host
+expression compiler matches the reference's grammar and error classes."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_1606_04884_b200 as pt
+from paper_1606_04884_b200 import _lib
+from paper_1606_04884_b200.backend import BackendDescriptor, choose_launch
+from paper_1606_04884_b200.expr import parse
+
+import pyoracle as po
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "pt_b200.h")).read()
+    return sorted(set(re.findall(r"\b(pt_b200_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = pt.lib()
+    syms = header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(lib, s), f"libpt_b200.so does not export {s}"
+    assert set(syms) <= set(_lib.EXPORTED)
+
+
+def test_abi_version_and_no_device_here():
+    assert pt.lib().pt_b200_abi_version() == 1
+    # no GPU in the CI container: count is 0, never an error
+    assert pt.lib().pt_b200_device_count() >= 0
+
+
+def test_validation_errors_map_to_reference_classes():
+    g = _lib.PtConvGeom(1, 1, 3, 3, 1, 5, 5, 0, 0, 1, 1)  # kernel exceeds padded input
+    st = pt.lib().pt_b200_conv_validate(C.byref(g))
+    assert st == _lib.PT_EVALIDATION
+    assert "kernel exceeds padded input" in pt.lib().pt_b200_last_error().decode()
+    with pytest.raises(pt.ValidationError):
+        _lib.check(st)
+    # null tensors are validation errors, reported before any device work
+    g = _lib.PtConvGeom(1, 1, 3, 3, 1, 3, 3, 1, 1, 1, 1)
+    assert pt.lib().pt_b200_conv_fwd(C.byref(g), None, None, None, None, 0, None, 0, None) == 2
+    assert pt.lib().pt_b200_conv_fwd(C.byref(g), 16, 16, None, 16, 7, None, 0, None) == 2
+
+
+@pytest.mark.parametrize("op", [0, 1, 2, 3])
+def test_workspace_query_is_host_only(op):
+    for name, g in [("L1", (128, 3, 128, 128, 96, 11, 11, 0, 0, 1, 1)),
+                    ("L5", (128, 384, 13, 13, 384, 3, 3, 0, 0, 1, 1)),
+                    ("alex1", (128, 3, 224, 224, 64, 11, 11, 2, 2, 4, 4))]:
+        gg = pt.ConvGeometry(*g)
+        for m in ("tf32", "fp32"):
+            n = pt.conv.workspace_bytes(gg, op, m)
+            assert 0 <= n < 64 << 30, (name, op, m, n)
+
+
+def test_geometry_mirror():
+    g = pt.ConvGeometry(16, 3, 32, 32, 64, 3, 3, 1, 1, 1, 1)
+    assert (g.outHeight(), g.outWidth(), g.patchSize(), g.outSpatial()) == (32, 32, 27, 1024)
+    assert g.toString() == "N16 C3 H32 W32 K64 k3x3 p1x1 s1x1"
+    g.validate()
+    with pytest.raises(pt.ValidationError):
+        pt.ConvGeometry(1, 1, 3, 3, 1, 3, 3, -1, 0).validate()
+
+
+@pytest.mark.parametrize("n,maxwg", [(1, 256), (1000, 256), (257, 1024), (5, 64), (1 << 30, 1)])
+def test_choose_launch_matches_reference(n, maxwg):
+    lc = choose_launch(n, BackendDescriptor("b200:0", maxwg, 0))
+    if po.ref_available():
+        st, glob, wg, _ = po.ref_choose_launch(n, maxwg)
+        assert st == 0 and (glob, wg) == (lc.globalSize, lc.workgroupSize)
+
+
+EXPRS_OK = ["x = x + s", "x = s", "x=x*2", "x = max(x, y) * 2.5 - z / 4", "x = -(-x)",
+            "x = tanh(exp(log(sqrt(abs(x)))))", "x = min(x, .5e1) + 1e-3", "x = ((x))",
+            "x = x - y - z", "x = 2 * -y"]
+EXPRS_BAD = [("y = x", 1), ("x + 1", 1), ("x = w", 1), ("x = y", 1), ("x = max(x)", 1),
+             ("x = (x", 1), ("x = x +", 1), ("x = x $ 2", 1), ("x = 1.2.3", 1), ("x = x x", 1),
+             ("x = foo(x)", 1), ("x = sqrt x", 1)]
+
+
+@pytest.mark.parametrize("text", EXPRS_OK)
+def test_expression_accepts_like_reference(text):
+    prog = parse(text, 3)
+    assert prog.code
+    if po.ref_available():
+        st, _ = po.ref_parse_expr(text, 3)
+        assert st == 0
+
+
+@pytest.mark.parametrize("text,arity", EXPRS_BAD)
+def test_expression_rejects_like_reference(text, arity):
+    with pytest.raises(pt.ValidationError) as ei:
+        parse(text, arity)
+    if po.ref_available():
+        st, msg = po.ref_parse_expr(text, arity)
+        assert st == 2
+        assert str(ei.value) == msg
+
+
+def test_expression_depth_limit():
+    deep = "x = " + "(" * 10 + "+".join(["x"] * 40) + ")" * 10
+    parse(deep, 1)  # left-assoc sums keep the stack shallow
+    nested = "x = " + "+".join(["(x*" * 1 + "x)"] * 2)
+    parse(nested, 1)
+    very = "x = " + "".join(f"x*(" for _ in range(33)) + "x" + ")" * 33
+    with pytest.raises(pt.ValidationError):
+        parse(very, 1)
