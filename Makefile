@@ -43,9 +43,10 @@ $(LIBDIR)/libportten.so: $(HOST_SRCS) $(HOST_HDRS) $(LIBDIR)/libpt_b200.so
 	@mkdir -p $(LIBDIR)
 	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIBDIR) -lpt_b200 -Wl,-rpath,'$$ORIGIN'
 
-tests/cpp/portten_tests: tests/cpp/portten_tests.cpp $(LIBDIR)/libportten.so oracle/oracle.h
+# test driver: links the product libraries and, as the checker only, the oracle
+tests/cpp/portten_tests: tests/cpp/portten_tests.cpp $(LIBDIR)/libportten.so oracle/oracle.h oracle
 	$(CXX) $(CXXFLAGS) -o $@ tests/cpp/portten_tests.cpp -L$(LIBDIR) -lportten -lpt_b200 \
-	    -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -ldl
+	    -Loracle -loracle -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' -Wl,-rpath,'$$ORIGIN/../../oracle' -ldl
 
 clean:
 	rm -rf build $(LIBDIR) tests/cpp/portten_tests
