@@ -267,6 +267,7 @@ def main():
 
     import paper_1606_04884_b200 as pt
     from paper_1606_04884_b200 import _lib as L
+    from paper_1606_04884_b200.dp import GradBucket, allreduce_async
 
     layers = WORKLOADS[args.workload]
     dev = torch.device("cuda", local)
@@ -280,27 +281,25 @@ def main():
         w = pt.fill_uniform(torch.empty(g.weight_shape(), device=dev), seed + 2, -s, s)
         b = pt.fill_uniform(torch.empty((K,), device=dev), seed + 3, -0.1, 0.1)
         gy = pt.fill_uniform(torch.empty(g.output_shape(), device=dev), seed + 4)
+        bucket = GradBucket([torch.Size(g.weight_shape()), torch.Size((K,))], dev)
         st.append(dict(g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
-                       gx=torch.empty(g.input_shape(), device=dev),
-                       gw=torch.empty(g.weight_shape(), device=dev),
-                       gb=torch.empty((K,), device=dev)))
+                       gx=torch.empty(g.input_shape(), device=dev), bucket=bucket,
+                       gw=bucket.views[0], gb=bucket.views[1]))
     comm = torch.cuda.Stream(device=dev) if world > 1 else None
 
     def step():
         cur = torch.cuda.current_stream()
+        done = []
         for s in st:
             g = s["g"]
             pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math)
             pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math)
-            if comm is not None:  # batch-sharded DP: allreduce(sum) gradW/gradB, overlapped
-                ev = torch.cuda.Event()
-                ev.record(cur)
-                comm.wait_event(ev)
-                with torch.cuda.stream(comm):
-                    dist.all_reduce(s["gw"])
-                    dist.all_reduce(s["gb"])
-        if comm is not None:
-            cur.wait_stream(comm)
+            # batch-sharded DP: one allreduce(sum) of this layer's gradW||gradB bucket on the
+            # comm stream, overlapping the next layer's kernels
+            done.append(allreduce_async(s["bucket"], comm))
+        for ev in done:
+            if ev is not None:
+                cur.wait_event(ev)
 
     for _ in range(max(3, args.warmup)):
         step()

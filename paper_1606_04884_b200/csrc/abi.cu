@@ -1,6 +1,7 @@
 // abi.cu — the extern "C" boundary of libpt_b200.so (include/pt_b200.h).
 // Validation mirrors the reference's checks (conv_geometry.hpp:53-63,
 // backend.cpp:115-161); every exception is converted to a status code here.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -55,7 +56,12 @@ void require_view(const pt_view& v, const char* what) {
     PTB_REQUIRE(v.offset >= 0, std::string(what) + ": negative storage offset");
 }
 
+bool fwd_rowconv(const Geo& g, int math) {
+    static const bool off = std::getenv("PT_B200_NO_ROWCONV") != nullptr;  // A/B switch for tests
+    return math == PT_MATH_TF32 && !off && rowconv_ok(g);
+}
 size_t fwd_ws(const Geo& g, int math) {
+    if (fwd_rowconv(g, math)) return rowconv_workspace(g);
     if (math == PT_MATH_TF32) {
         const UmmaPlan pl = umma_plan(g, false);
         if (pl.ok) return pl.ws_bytes;
@@ -258,6 +264,11 @@ int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, con
         require_ptr(y, "output");
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
+        if (fwd_rowconv(g, math)) {
+            require_ws(ws_bytes, rowconv_workspace(g), ws);
+            rowconv_fwd(g, x, w, b, y, ws, st);
+            return;
+        }
         if (math == PT_MATH_TF32) {
             const UmmaPlan pl = umma_plan(g, false);
             if (pl.ok) {

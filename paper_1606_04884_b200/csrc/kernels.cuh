@@ -73,6 +73,12 @@ void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float
 void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
                         float* gx, void* ws, cudaStream_t st, const float* gyh_pre = nullptr);
 
+// ---- umma_rowconv.cu: small-C (<=4), stride-1 forward via the Hankel row view ----
+bool rowconv_ok(const Geo& g);
+size_t rowconv_workspace(const Geo& g);
+void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, float* y, void* ws,
+                 cudaStream_t st);
+
 // ---- umma_wgrad.cu: tcgen05 kind::tf32 weight gradient (MN-major operands, split-K) ----
 bool umma_wgrad_ok(const Geo& g);
 size_t umma_wgrad_workspace(const Geo& g);
@@ -97,6 +103,6 @@ void reduce_all_launch(int op, const float* base, const pt_view& v, float* out, 
 void reduce_dim_launch(int op, const float* base, const pt_view& v, int dim, float* out,
                        cudaStream_t st);
 
-inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace ptb

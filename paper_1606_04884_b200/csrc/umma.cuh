@@ -230,6 +230,54 @@ __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
         : "memory");
 }
 
+// Epilogue helper: drain `ncols` accumulator columns of this thread's TMEM lane (one
+// output pixel) and store them to NCHW: out[ch * chan_stride] for ch = ch0 .. ch0+ncols-1
+// (`out` already points at the pixel of channel ch0), adding bias[ch] when given.
+// Channels >= n_valid are skipped. tcgen05.ld is warp-collective: every lane calls this.
+__device__ __forceinline__ void store_tmem_columns_nchw(uint32_t taddr, int ncols, float* out,
+                                                        int64_t chan_stride, const float* bias,
+                                                        int ch0, int n_valid, bool valid) {
+    for (int c0 = 0; c0 < ncols; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld_32x32b_x16(taddr + c0, v);
+        float bv[16];
+        const int chb = ch0 + c0;
+        const bool full16 = chb + 16 <= n_valid;
+        if (bias && full16) {
+            const float4* b4 = reinterpret_cast<const float4*>(bias + chb);
+            if ((reinterpret_cast<uintptr_t>(b4) & 15) == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 t = __ldg(b4 + q);
+                    bv[4 * q] = t.x; bv[4 * q + 1] = t.y; bv[4 * q + 2] = t.z; bv[4 * q + 3] = t.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) bv[q] = __ldg(bias + chb + q);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) bv[q] = (bias && chb + q < n_valid) ? __ldg(bias + chb + q) : 0.f;
+        }
+        tmem_ld_wait();
+        if (valid) {
+            float* o = out + (int64_t)c0 * chan_stride;
+            if (full16) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    __stcs(o, __uint_as_float(v[q]) + bv[q]);
+                    o += chan_stride;
+                }
+            } else {
+                for (int q = 0; q < 16 && chb + q < n_valid; ++q) {
+                    __stcs(o, __uint_as_float(v[q]) + bv[q]);
+                    o += chan_stride;
+                }
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x / 32; }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x % 32; }
 

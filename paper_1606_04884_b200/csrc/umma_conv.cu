@@ -259,22 +259,8 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
             }
             const int ch0 = nt * p.bn;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
-            for (int c0 = 0; c0 < p.bn; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(taddr + c0, v);
-                tmem_ld_wait();
-                if (valid) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int ch = ch0 + c0 + j;
-                        if (ch < p.n_rows) {
-                            float val = __uint_as_float(v[j]);
-                            if (p.bias) val += __ldg(p.bias + ch);
-                            p.out[base + (int64_t)ch * p.out_hw] = val;
-                        }
-                    }
-                }
-            }
+            store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base + (int64_t)ch0 * p.out_hw : 0),
+                                    p.out_hw, p.bias, ch0, p.n_rows, valid);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
