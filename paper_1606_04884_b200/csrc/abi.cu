@@ -68,35 +68,68 @@ size_t fwd_ws(const Geo& g, int math) {
     }
     return 0;
 }
+// small-C stride-1 dgrad: tconv of the row-expanded (kH x 1) layer + 1-D fold
+bool dgrad_row(const Geo& g, int math) {
+    static const bool off = std::getenv("PT_B200_NO_ROWCONV") != nullptr;
+    return math == PT_MATH_TF32 && !off && rowdgrad_ok(g);
+}
 size_t bwd_data_ws(const Geo& g, int math) {
+    if (dgrad_row(g, math)) return rowdgrad_workspace(g);
     if (math == PT_MATH_TF32) {
         const UmmaPlan pl = umma_plan(g, true);
         if (pl.ok) return pl.ws_bytes;
     }
     return 0;
 }
-bool wgrad_tc(const Geo& g, int math) { return math == PT_MATH_TF32 && umma_wgrad_ok(g); }
+// updateGradInput body. gyh_pre (gy NHWC, round_up(K,32) channels) is used when the
+// chosen engine reads that layout.
+void bwd_data_impl(const Geo& g, const float* gy, const float* w, float* gx, int math, void* ws,
+                   cudaStream_t st, const float* gyh_pre = nullptr) {
+    if (dgrad_row(g, math)) {
+        rowdgrad(g, gy, w, gx, ws, st, gyh_pre);
+        return;
+    }
+    if (math == PT_MATH_TF32) {
+        const UmmaPlan pl = umma_plan(g, true);
+        if (pl.ok) {
+            const bool same_layout = pl.cb == 32 && pl.cin_p == umma_wgrad_kp(g);
+            umma_conv_bwd_data(g, pl, gy, w, gx, ws, st, same_layout ? gyh_pre : nullptr);
+            return;
+        }
+    }
+    simt_conv_bwd_data(g, gy, w, gx, st);
+}
+// Tensor-core wgrad engines, both fed by gy in NHWC (round_up(K,32) channels):
+// the Hankel row kernel for small-C stride-1 layers, else the im2col-TMA kernel.
+bool wgrad_row(const Geo& g, int math) {
+    static const bool off = std::getenv("PT_B200_NO_ROWCONV") != nullptr;
+    return math == PT_MATH_TF32 && !off && rowwgrad_ok(g);
+}
+bool wgrad_tc(const Geo& g, int math) {
+    return math == PT_MATH_TF32 && (wgrad_row(g, math) || umma_wgrad_ok(g));
+}
+size_t wgrad_tc_ws(const Geo& g, int math) {
+    return align_up(wgrad_row(g, math) ? rowwgrad_workspace(g) : umma_wgrad_workspace(g), 256);
+}
+void wgrad_tc_run(const Geo& g, const float* x, const float* gy, const float* gyh, float* gw, float scale,
+                  int accumulate, int math, char* ws, cudaStream_t st) {
+    if (wgrad_row(g, math)) rowwgrad(g, x, gyh, gw, scale, accumulate, ws, st);
+    else umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, ws, st, gyh);
+}
 size_t gyh_bytes(const Geo& g) { return align_up((size_t)(g.M * umma_wgrad_kp(g)) * 4, 256); }
 size_t bias_part_bytes(const Geo& g) { return align_up(nhwc_bias_partials_bytes(g.N, g.K, g.oHW), 256); }
 // TF32 wgrad workspace: [gy NHWC + fused gradBias partials][wgrad kernel scratch]
 // FP32 wgrad workspace: [split-K partials][gradBias partials]
 size_t bwd_filter_ws(const Geo& g, int math) {
-    if (wgrad_tc(g, math))
-        return gyh_bytes(g) + bias_part_bytes(g) + align_up(umma_wgrad_workspace(g), 256);
+    if (wgrad_tc(g, math)) return gyh_bytes(g) + bias_part_bytes(g) + wgrad_tc_ws(g, math);
     return align_up(simt_wgrad_workspace(g), 256) + align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256);
 }
-// Combined backward shares the gy transform when dgrad's gy operand has wgrad's layout.
-bool bwd_shared(const Geo& g, int math, UmmaPlan* out = nullptr) {
-    if (!wgrad_tc(g, math)) return false;
-    const UmmaPlan pl = umma_plan(g, true);
-    if (out) *out = pl;
-    return pl.ok && pl.cb == 32 && pl.cin_p == umma_wgrad_kp(g);
-}
+// Combined backward: one gy NHWC transform (+ fused gradBias) feeds the tensor-core
+// wgrad and, when its engine reads the same layout, the dgrad.
+bool bwd_shared(const Geo& g, int math) { return wgrad_tc(g, math); }
 size_t bwd_ws(const Geo& g, int math) {
-    UmmaPlan pl;
-    if (bwd_shared(g, math, &pl))
-        return gyh_bytes(g) + bias_part_bytes(g) + align_up(pl.ws_bytes, 256) +
-               align_up(umma_wgrad_workspace(g), 256);
+    if (bwd_shared(g, math))
+        return gyh_bytes(g) + bias_part_bytes(g) + align_up(bwd_data_ws(g, math), 256) + wgrad_tc_ws(g, math);
     return std::max(bwd_data_ws(g, math), bwd_filter_ws(g, math));
 }
 
@@ -111,8 +144,8 @@ void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, f
             nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate,
                               part, st);
         }
-        umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, ws + gyh_bytes(g) + bias_part_bytes(g),
-                             st, gyh);
+        wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, ws + gyh_bytes(g) + bias_part_bytes(g),
+                     st);
         return;
     }
     simt_conv_bwd_filter(g, x, gy, gw, scale, accumulate, reinterpret_cast<float*>(ws), st);
@@ -290,16 +323,8 @@ int pt_b200_conv_bwd_data(const pt_conv_geom* gp, const float* gy, const float* 
         require_ptr(w, "weight");
         require_ptr(gx, "gradInput");
         const Geo g(*gp);
-        cudaStream_t st = as_stream(stream);
-        if (math == PT_MATH_TF32) {
-            const UmmaPlan pl = umma_plan(g, true);
-            if (pl.ok) {
-                require_ws(ws_bytes, pl.ws_bytes, ws);
-                umma_conv_bwd_data(g, pl, gy, w, gx, ws, st);
-                return;
-            }
-        }
-        simt_conv_bwd_data(g, gy, w, gx, st);
+        require_ws(ws_bytes, bwd_data_ws(g, math), ws);
+        bwd_data_impl(g, gy, w, gx, math, ws, as_stream(stream));
     });
 }
 
@@ -334,28 +359,22 @@ int pt_b200_conv_bwd(const pt_conv_geom* gp, const float* x, const float* gy, co
         cudaStream_t st = as_stream(stream);
         require_ws(ws_bytes, bwd_ws(g, math), ws);
         char* base = reinterpret_cast<char*>(ws);
-        UmmaPlan pl;
-        if (gx && gw && bwd_shared(g, math, &pl)) {
+        if (gx && gw && bwd_shared(g, math)) {
             // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
             float* gyh = reinterpret_cast<float*>(base);
             float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
             char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
-            char* wws = dws + align_up(pl.ws_bytes, 256);
+            char* wws = dws + align_up(bwd_data_ws(g, math), 256);
             {
                 ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
                 nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate,
                                   part, st);
             }
-            umma_conv_bwd_data(g, pl, gy, w, gx, dws, st, gyh);
-            umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, wws, st, gyh);
+            bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
+            wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st);
             return;
         }
-        if (gx) {
-            if (math == PT_MATH_TF32 && (pl = umma_plan(g, true)).ok)
-                umma_conv_bwd_data(g, pl, gy, w, gx, ws, st);
-            else
-                simt_conv_bwd_data(g, gy, w, gx, st);
-        }
+        if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
         if (gw) bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st);
     });
 }

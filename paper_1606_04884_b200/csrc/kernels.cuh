@@ -71,20 +71,39 @@ void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float
                    const float* b, float* y, void* ws, cudaStream_t st);
 // gyh_pre: gy already in NHWC [N][oHW][pl.cin_p] (TF32-rounded), or null to transform here.
 void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
-                        float* gx, void* ws, cudaStream_t st, const float* gyh_pre = nullptr);
+                        float* gx, void* ws, cudaStream_t st, const float* gyh_pre = nullptr,
+                        double alg_flops = -1.0);
+
+// ---- umma_rowwgrad.cu: small-C dgrad = tconv of the (kH x 1) row-expanded layer + 1-D fold ----
+bool rowdgrad_ok(const Geo& g, UmmaPlan* plan = nullptr);
+size_t rowdgrad_workspace(const Geo& g);
+void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st,
+              const float* gyh_pre = nullptr);
 
 // ---- umma_rowconv.cu: small-C (<=4), stride-1 forward via the Hankel row view ----
+// x NCHW -> zero-bordered NHWC4 xp[n][Hp][Wa][4] (TF32-rounded)
+void pad_nhwc4(const float* x, float* xp, const Geo& g, int Hp, int Wa, cudaStream_t st);
 bool rowconv_ok(const Geo& g);
 size_t rowconv_workspace(const Geo& g);
 void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, float* y, void* ws,
                  cudaStream_t st);
 
+// ---- umma_rowwgrad.cu: small-C (<=4), stride-1 weight gradient via the Hankel row view ----
+bool rowwgrad_ok(const Geo& g);
+size_t rowwgrad_workspace(const Geo& g);
+// gyh: gradOutput NHWC [N*oH*oW][round_up(K,32)], TF32-rounded
+void rowwgrad(const Geo& g, const float* x, const float* gyh, float* gw, float scale, int accumulate,
+              void* ws, cudaStream_t st);
+
 // ---- umma_wgrad.cu: tcgen05 kind::tf32 weight gradient (MN-major operands, split-K) ----
 bool umma_wgrad_ok(const Geo& g);
 size_t umma_wgrad_workspace(const Geo& g);
 // gyh_pre: gy already in NHWC [M][round_up(K,32)] (TF32-rounded), or null.
+// xh_pre: x already NHWC [N][HW][round_up(C,32)] (TF32-rounded), or null.
+// alg_flops: algorithmic FLOPs recorded for the live roofline (default 2*M*K*CRS of g).
 void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* gw, float scale,
-                          int accumulate, void* ws, cudaStream_t st, const float* gyh_pre = nullptr);
+                          int accumulate, void* ws, cudaStream_t st, const float* gyh_pre = nullptr,
+                          const float* xh_pre = nullptr, double alg_flops = -1.0);
 int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 
 // ---- unfold.cu ----

@@ -462,7 +462,8 @@ void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float
 }
 
 void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
-                        float* gx, void* ws, cudaStream_t st, const float* gyh_pre) {
+                        float* gx, void* ws, cudaStream_t st, const float* gyh_pre, double alg_flops) {
+    if (alg_flops < 0) alg_flops = 2.0 * g.M * g.K * g.CRS;
     float* act = reinterpret_cast<float*>(ws);
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
     if (gyh_pre) {
@@ -475,15 +476,14 @@ void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const
         pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackDgradFlip, pl.cb, pl.n_pad, pl.cin_p,
                      pl.slots_p, pl.wt_elems, true, st);
         run_umma(pl, act, wt, g.N, g.oH, g.oW, (int)g.kH, (int)g.kW, (int)(g.kH - 1 - g.pH),
-                 (int)(g.kW - 1 - g.pW), 1, 1, g.H, g.W, gx, nullptr, 2.0 * g.M * g.K * g.CRS, st);
+                 (int)(g.kW - 1 - g.pW), 1, 1, g.H, g.W, gx, nullptr, alg_flops, st);
         return;
     }
     // kDgradGcol: gcol = W^T * gy (tensor cores), then the deterministic gather col2im
     float* gcol = reinterpret_cast<float*>(reinterpret_cast<char*>(wt) + align_up(pl.wt_elems * 4, 256));
     pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackGcol, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
                  pl.wt_elems, true, st);
-    run_umma(pl, act, wt, g.N, g.oH, g.oW, 1, 1, 0, 0, 1, 1, g.oH, g.oW, gcol, nullptr,
-             2.0 * g.M * g.K * g.CRS, st);
+    run_umma(pl, act, wt, g.N, g.oH, g.oW, 1, 1, 0, 0, 1, 1, g.oH, g.oW, gcol, nullptr, alg_flops, st);
     {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.CRS * g.oHW + g.N * g.C * g.HW));
         col2im_batched_launch(g, gcol, gx, st);

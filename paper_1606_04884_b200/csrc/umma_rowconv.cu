@@ -247,6 +247,14 @@ RowPlan rplan(const Geo& g) {
 
 }  // namespace
 
+void pad_nhwc4(const float* x, float* xp, const Geo& g, int Hp, int Wa, cudaStream_t st) {
+    const int64_t total = g.N * Hp * Wa;
+    pad_nhwc4_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count()), 256, 0,
+                       st>>>(x, reinterpret_cast<float4*>(xp), g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.pH,
+                             (int)g.pW, Hp, Wa);
+    after_launch("pad_nhwc4");
+}
+
 bool rowconv_ok(const Geo& g) {
     if (!(g.C <= 4 && g.sH == 1 && g.sW == 1 && g.K <= 256 && g.kW <= 64 && g.kH <= 64 &&
           g.N * (g.H + 2 * g.pH) < (1ll << 31) && sm_count() >= 2))

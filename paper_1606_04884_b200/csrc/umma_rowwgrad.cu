@@ -1,0 +1,195 @@
+// umma_rowwgrad.cu — weight gradient for small-channel, stride-1 layers (C <= 4: the
+// first layer of L1 / VGG-A; accGradParameters).
+//
+// With C = 3 the im2col-TMA wgrad kernel would pad every 32-channel box from 3 real
+// channels (10.7x wasted MMA work). Instead the horizontal taps are folded into the
+// channel dimension once, in HBM:
+//   Xe[n][h][j][e],  e = s*C + c  (Ce = kW*C rounded up to 32),
+//   Xe[n][h][j][s*C + c] = x[n][c][h][j*sW + s - pW]   (0 outside the image)
+// so the layer becomes a (kH x 1) convolution over Xe with Ce channels, width oW and
+// the same output grid:  gW'[k][e][r] = sum_{n,i,j} gy[n][k][i][j] * Xe[n][i*sH+r-pH][j][e],
+// computed by the tcgen05 CTA-pair wgrad kernel (umma_wgrad.cu) with no channel waste
+// beyond Ce; a remap kernel writes gW[k][c][r][s] = gW'[k][s*C + c][r] with scale /
+// accumulate. (The tensor cores cannot take the un-expanded Hankel row as an MN-major
+// tf32 operand: that layout needs the 32-byte-atom swizzle.)
+#include <cuda.h>
+
+#include "kernels.cuh"
+
+namespace ptb {
+
+namespace {
+
+// One thread per output pixel (n, h, j): gathers its kW*C taps and writes the Ce-float
+// row with 16-byte stores (a warp writes 32 consecutive pixel rows: contiguous).
+__global__ void expand_rows_kernel(const float* __restrict__ x, float4* __restrict__ xe, int64_t rows,
+                                   int C, int H, int W, int oW, int kW, int pW, int sW, int Ce) {
+    const int64_t pix = rows * oW;  // rows = N*H
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pix;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = p / oW;
+        const int j = (int)(p - row * oW);
+        const int64_t n = row / H;
+        const int h = (int)(row - n * H);
+        const float* xr = x + (n * C * H + h) * (int64_t)W;  // channel 0 of image row (n, h)
+        const int64_t cstride = (int64_t)H * W;
+        float4* dst = xe + p * (Ce / 4);
+        for (int e0 = 0; e0 < Ce; e0 += 4) {
+            float v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = e0 + q, s = e / C, c = e - s * C;
+                const int w = j * sW + s - pW;
+                float f = 0.f;
+                if (s < kW && w >= 0 && w < W) f = __ldg(xr + c * cstride + w);
+                uint32_t r;
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+                v[q] = __uint_as_float(r);
+            }
+            dst[e0 / 4] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+    }
+}
+
+// gw[k][c][r][s] = (acc ? gw : 0) + scale * gwe[k][s*C + c][r]
+__global__ void remap_rows_kernel(const float* __restrict__ gwe, float* __restrict__ gw, int64_t K,
+                                  int C, int kH, int kW, int Ce, float scale, int accumulate) {
+    const int64_t total = K * C * kH * kW;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i % kW), r = (int)((i / kW) % kH), c = (int)((i / ((int64_t)kW * kH)) % C);
+        const int64_t k = i / ((int64_t)kW * kH * C);
+        const float v = gwe[(k * Ce + (s * C + c)) * kH + r];
+        gw[i] = (accumulate ? gw[i] : 0.f) + scale * v;
+    }
+}
+
+// W[k][c][r][s] -> W''[k][s*C + c][r][0]: the filter of the (kH x 1) row-expanded conv.
+__global__ void expand_filter_kernel(const float* __restrict__ w, float* __restrict__ we, int64_t K, int C,
+                                     int kH, int kW) {
+    const int64_t total = K * C * kH * kW;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i % kW), r = (int)((i / kW) % kH), c = (int)((i / ((int64_t)kW * kH)) % C);
+        const int64_t k = i / ((int64_t)kW * kH * C);
+        we[((k * kW * C) + s * C + c) * kH + r] = w[i];
+    }
+}
+
+// gx[n][c][h][w] = sum_{s=0..kW-1} gxe[n][s*C + c][h][(w + pW - s)/sW]  (taps in fixed order)
+__global__ void fold_rows_kernel(const float* __restrict__ gxe, float* __restrict__ gx, int64_t N, int C,
+                                 int H, int W, int oW, int kW, int pW, int sW) {
+    const int64_t total = N * C * (int64_t)H * W;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int w = (int)(i % W);
+        int64_t t = i / W;
+        const int h = (int)(t % H);
+        t /= H;
+        const int c = (int)(t % C);
+        const int64_t n = t / C;
+        const int64_t plane = (int64_t)H * oW;
+        const float* src = gxe + ((n * kW * C + c) * H + h) * (int64_t)oW;
+        float acc = 0.f;
+        for (int s = 0; s < kW; ++s) {
+            const int wn = w + pW - s;
+            if (wn < 0) break;
+            const int j = wn / sW;
+            if (j * sW != wn || j >= oW) continue;
+            acc += __ldg(src + (int64_t)s * C * plane + j);
+        }
+        gx[i] = acc;
+    }
+}
+
+// dgrad of the row-expanded (kH x 1) conv: its input has kW*C channels and width oW.
+Geo dgrad_rows_geo(const Geo& g) {
+    pt_conv_geom e{g.N, g.kW * g.C, g.H, g.oW, g.K, g.kH, 1, g.pH, 0, g.sH, 1};
+    return Geo(e);
+}
+
+Geo expanded_geo(const Geo& g, int64_t Ce) {
+    pt_conv_geom e{g.N, Ce, g.H, g.oW, g.K, g.kH, 1, g.pH, 0, g.sH, 1};
+    return Geo(e);
+}
+
+int64_t ce_of(const Geo& g) { return (g.kW * g.C + 31) / 32 * 32; }
+
+}  // namespace
+
+// ---- small-C dgrad: tensor-core tconv of the row-expanded layer + 1-D fold over s ----
+bool rowdgrad_ok(const Geo& g, UmmaPlan* plan) {
+    if (!(g.C <= 4 && g.sH == 1 && g.sW == 1 && g.kW * g.C <= 256)) return false;
+    const UmmaPlan pl = umma_plan(dgrad_rows_geo(g), true);
+    if (plan) *plan = pl;
+    return pl.ok && pl.mode == UmmaPlan::kDgradTconv;
+}
+
+size_t rowdgrad_workspace(const Geo& g) {
+    UmmaPlan pl;
+    if (!rowdgrad_ok(g, &pl)) return 0;
+    const Geo e = dgrad_rows_geo(g);
+    return align_up((size_t)(g.K * e.C * g.kH) * 4, 256) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256) +
+           align_up(pl.ws_bytes, 256);
+}
+
+void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st,
+              const float* gyh_pre) {
+    UmmaPlan pl;
+    PTB_REQUIRE(rowdgrad_ok(g, &pl), "rowdgrad: unsupported geometry");
+    const Geo e = dgrad_rows_geo(g);
+    char* base = reinterpret_cast<char*>(ws);
+    float* we = reinterpret_cast<float*>(base);
+    float* gxe = reinterpret_cast<float*>(base + align_up((size_t)(g.K * e.C * g.kH) * 4, 256));
+    char* dws = reinterpret_cast<char*>(gxe) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256);
+    const int64_t nw = g.K * g.CRS;
+    expand_filter_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nw, 256), 4 * (int64_t)sm_count()), 256, 0, st>>>(
+        w, we, g.K, (int)g.C, (int)g.kH, (int)g.kW);
+    after_launch("expand_filter");
+    umma_conv_bwd_data(e, pl, gy, we, gxe, dws, st, gyh_pre, 2.0 * g.M * g.K * g.CRS);
+    const int64_t total = g.N * g.C * g.HW;
+    ProfScope prof("layout", st, 0.0, 4.0 * (e.N * e.C * e.H * e.W + total));
+    fold_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count()), 256, 0, st>>>(
+        gxe, gx, g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.oW, (int)g.kW, (int)g.pW, (int)g.sW);
+    after_launch("fold_rows");
+}
+
+bool rowwgrad_ok(const Geo& g) {
+    // worthwhile when C is tiny; the expanded layer must fit the CTA-pair wgrad kernel
+    if (!(g.C <= 4 && g.sW <= 8 && g.kW * g.C <= 256)) return false;
+    return umma_wgrad_ok(expanded_geo(g, ce_of(g)));
+}
+
+size_t rowwgrad_workspace(const Geo& g) {
+    const int64_t Ce = ce_of(g);
+    const Geo e = expanded_geo(g, Ce);
+    return align_up((size_t)(g.N * g.H * g.oW * Ce) * 4, 256) + align_up((size_t)(g.K * Ce * g.kH) * 4, 256) +
+           align_up(umma_wgrad_workspace(e), 256);
+}
+
+void rowwgrad(const Geo& g, const float* x, const float* gyh, float* gw, float scale, int accumulate,
+              void* ws, cudaStream_t st) {
+    const int64_t Ce = ce_of(g);
+    const Geo e = expanded_geo(g, Ce);
+    char* base = reinterpret_cast<char*>(ws);
+    float* xe = reinterpret_cast<float*>(base);
+    float* gwe = reinterpret_cast<float*>(base + align_up((size_t)(g.N * g.H * g.oW * Ce) * 4, 256));
+    char* kws = reinterpret_cast<char*>(gwe) + align_up((size_t)(g.K * Ce * g.kH) * 4, 256);
+    {
+        const int64_t total = g.N * g.H * g.oW * Ce;
+        ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + total));
+        const int64_t pix = g.N * g.H * g.oW;
+        expand_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(pix, 128), 16 * (int64_t)sm_count()), 128, 0,
+                             st>>>(x, reinterpret_cast<float4*>(xe), g.N * g.H, (int)g.C, (int)g.H, (int)g.W,
+                                   (int)g.oW, (int)g.kW, (int)g.pW, (int)g.sW, (int)Ce);
+        after_launch("expand_rows");
+    }
+    // the expanded layer: Xe is already NHWC with Ce channels, gy NHWC is shared
+    umma_conv_bwd_filter(e, nullptr, nullptr, gwe, 1.0f, 0, kws, st, gyh, xe, 2.0 * g.M * g.K * g.CRS);
+    const int64_t n = g.K * g.CRS;
+    remap_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256, 0, st>>>(
+        gwe, gw, g.K, (int)g.C, (int)g.kH, (int)g.kW, (int)Ce, scale, accumulate);
+    after_launch("remap_rows");
+}
+
+}  // namespace ptb

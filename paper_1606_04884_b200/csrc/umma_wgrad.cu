@@ -290,21 +290,23 @@ size_t umma_wgrad_workspace(const Geo& g) {
 int64_t umma_wgrad_kp(const Geo& g) { return (g.K + 31) / 32 * 32; }
 
 void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* gw, float scale,
-                          int accumulate, void* ws, cudaStream_t st, const float* gyh_pre) {
+                          int accumulate, void* ws, cudaStream_t st, const float* gyh_pre,
+                          const float* xh_pre, double alg_flops) {
     const WPlan w = wplan(g);
     char* base = reinterpret_cast<char*>(ws);
     float* xh = reinterpret_cast<float*>(base);
     float* gyh = reinterpret_cast<float*>(base + align_up(w.x_elems * 4, 256));
     float* part = reinterpret_cast<float*>(base + align_up(w.x_elems * 4, 256) +
                                            align_up(w.gy_elems * 4, 256));
-    {
+    if (!(xh_pre && gyh_pre)) {
         ProfScope prof("layout", st, 0.0,
-                       4.0 * (g.N * g.C * g.HW + w.x_elems +
+                       4.0 * ((xh_pre ? 0 : g.N * g.C * g.HW + w.x_elems) +
                               (gyh_pre ? 0 : g.M * g.K + w.gy_elems)));
-        nchw_to_nhwc(x, xh, g.N, g.C, g.HW, w.Cp, true, st);
-        if (gyh_pre) gyh = const_cast<float*>(gyh_pre);
-        else nchw_to_nhwc(gy, gyh, g.N, g.K, g.oHW, w.Kp, true, st);
+        if (!xh_pre) nchw_to_nhwc(x, xh, g.N, g.C, g.HW, w.Cp, true, st);
+        if (!gyh_pre) nchw_to_nhwc(gy, gyh, g.N, g.K, g.oHW, w.Kp, true, st);
     }
+    if (xh_pre) xh = const_cast<float*>(xh_pre);
+    if (gyh_pre) gyh = const_cast<float*>(gyh_pre);
     UWgradParams p;
     memset(&p, 0, sizeof p);
     {
@@ -358,7 +360,7 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     {
-        ProfScope prof("umma_wgrad", st, 2.0 * g.M * g.K * g.CRS, 0.0);
+        ProfScope prof("umma_wgrad", st, alg_flops >= 0 ? alg_flops : 2.0 * g.M * g.K * g.CRS, 0.0);
         PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel, p));
         after_launch("umma_wgrad");
     }
