@@ -20,33 +20,37 @@ namespace ptb {
 
 namespace {
 
-// One thread per output pixel (n, h, j): gathers its kW*C taps and writes the Ce-float
-// row with 16-byte stores (a warp writes 32 consecutive pixel rows: contiguous).
+// One block per image row (n, h): the C input rows are staged (zero-padded, TF32-rounded)
+// in shared memory, then the oW x Ce expanded row is written with consecutive threads
+// storing consecutive float4s (fully coalesced).
 __global__ void expand_rows_kernel(const float* __restrict__ x, float4* __restrict__ xe, int64_t rows,
                                    int C, int H, int W, int oW, int kW, int pW, int sW, int Ce) {
-    const int64_t pix = rows * oW;  // rows = N*H
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < pix;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = p / oW;
-        const int j = (int)(p - row * oW);
+    extern __shared__ float srow[];  // [C][Wpad], Wpad = (oW-1)*sW + kW
+    const int Wpad = (oW - 1) * sW + kW;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
         const int64_t n = row / H;
         const int h = (int)(row - n * H);
-        const float* xr = x + (n * C * H + h) * (int64_t)W;  // channel 0 of image row (n, h)
-        const int64_t cstride = (int64_t)H * W;
-        float4* dst = xe + p * (Ce / 4);
-        for (int e0 = 0; e0 < Ce; e0 += 4) {
+        const float* xr = x + (n * C * H + h) * (int64_t)W;
+        __syncthreads();
+        for (int t = threadIdx.x; t < C * Wpad; t += blockDim.x) {
+            const int c = t / Wpad, u = t - c * Wpad, w = u - pW;
+            float f = (w >= 0 && w < W) ? __ldg(xr + (int64_t)c * H * W + w) : 0.f;
+            uint32_t r;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+            srow[t] = __uint_as_float(r);
+        }
+        __syncthreads();
+        float4* dst = xe + row * (int64_t)oW * (Ce / 4);
+        const int q4 = Ce / 4;
+        for (int t = threadIdx.x; t < oW * q4; t += blockDim.x) {
+            const int j = t / q4, e0 = (t - j * q4) * 4;
             float v[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int e = e0 + q, s = e / C, c = e - s * C;
-                const int w = j * sW + s - pW;
-                float f = 0.f;
-                if (s < kW && w >= 0 && w < W) f = __ldg(xr + c * cstride + w);
-                uint32_t r;
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
-                v[q] = __uint_as_float(r);
+                v[q] = s < kW ? srow[c * Wpad + j * sW + s] : 0.f;
             }
-            dst[e0 / 4] = make_float4(v[0], v[1], v[2], v[3]);
+            dst[t] = make_float4(v[0], v[1], v[2], v[3]);
         }
     }
 }
@@ -77,28 +81,29 @@ __global__ void expand_filter_kernel(const float* __restrict__ w, float* __restr
 }
 
 // gx[n][c][h][w] = sum_{s=0..kW-1} gxe[n][s*C + c][h][(w + pW - s)/sW]  (taps in fixed order)
+// One block-iteration per output row (n, c, h); threads sweep w (coalesced reads per tap).
 __global__ void fold_rows_kernel(const float* __restrict__ gxe, float* __restrict__ gx, int64_t N, int C,
                                  int H, int W, int oW, int kW, int pW, int sW) {
-    const int64_t total = N * C * (int64_t)H * W;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int w = (int)(i % W);
-        int64_t t = i / W;
-        const int h = (int)(t % H);
-        t /= H;
-        const int c = (int)(t % C);
-        const int64_t n = t / C;
-        const int64_t plane = (int64_t)H * oW;
+    const int64_t rows = N * C * (int64_t)H;
+    const int64_t plane = (int64_t)H * oW;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int h = (int)(row % H);
+        const int64_t nc = row / H;
+        const int c = (int)(nc % C);
+        const int64_t n = nc / C;
         const float* src = gxe + ((n * kW * C + c) * H + h) * (int64_t)oW;
-        float acc = 0.f;
-        for (int s = 0; s < kW; ++s) {
-            const int wn = w + pW - s;
-            if (wn < 0) break;
-            const int j = wn / sW;
-            if (j * sW != wn || j >= oW) continue;
-            acc += __ldg(src + (int64_t)s * C * plane + j);
+        float* dst = gx + row * W;
+        for (int w = threadIdx.x; w < W; w += blockDim.x) {
+            float acc = 0.f;
+            for (int s = 0; s < kW; ++s) {
+                const int wn = w + pW - s;
+                if (wn < 0) break;
+                const int j = wn / sW;
+                if (j * sW != wn || j >= oW) continue;
+                acc += __ldg(src + (int64_t)s * C * plane + j);
+            }
+            dst[w] = acc;
         }
-        gx[i] = acc;
     }
 }
 
@@ -149,7 +154,8 @@ void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws
     umma_conv_bwd_data(e, pl, gy, we, gxe, dws, st, gyh_pre, 2.0 * g.M * g.K * g.CRS);
     const int64_t total = g.N * g.C * g.HW;
     ProfScope prof("layout", st, 0.0, 4.0 * (e.N * e.C * e.H * e.W + total));
-    fold_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count()), 256, 0, st>>>(
+    const int64_t rows = g.N * g.C * g.H;
+    fold_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 32 * (int64_t)sm_count()), 128, 0, st>>>(
         gxe, gx, g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.oW, (int)g.kW, (int)g.pW, (int)g.sW);
     after_launch("fold_rows");
 }
@@ -157,6 +163,7 @@ void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws
 bool rowwgrad_ok(const Geo& g) {
     // worthwhile when C is tiny; the expanded layer must fit the CTA-pair wgrad kernel
     if (!(g.C <= 4 && g.sW <= 8 && g.kW * g.C <= 256)) return false;
+    if (g.C * ((g.oW - 1) * g.sW + g.kW) * 4 > 48 * 1024) return false;  // expand_rows staging
     return umma_wgrad_ok(expanded_geo(g, ce_of(g)));
 }
 
@@ -178,10 +185,12 @@ void rowwgrad(const Geo& g, const float* x, const float* gyh, float* gw, float s
     {
         const int64_t total = g.N * g.H * g.oW * Ce;
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + total));
-        const int64_t pix = g.N * g.H * g.oW;
-        expand_rows_kernel<<<(unsigned)std::min<int64_t>(ceil_div(pix, 128), 16 * (int64_t)sm_count()), 128, 0,
-                             st>>>(x, reinterpret_cast<float4*>(xe), g.N * g.H, (int)g.C, (int)g.H, (int)g.W,
-                                   (int)g.oW, (int)g.kW, (int)g.pW, (int)g.sW, (int)Ce);
+        const int64_t rows = g.N * g.H;
+        const size_t smem = sizeof(float) * (size_t)(g.C * ((g.oW - 1) * g.sW + g.kW));
+        PTB_REQUIRE(smem <= 48 * 1024, "expand_rows: input row too wide");
+        expand_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 16 * (int64_t)sm_count()), 256, smem, st>>>(
+            x, reinterpret_cast<float4*>(xe), rows, (int)g.C, (int)g.H, (int)g.W, (int)g.oW, (int)g.kW,
+            (int)g.pW, (int)g.sW, (int)Ce);
         after_launch("expand_rows");
     }
     // the expanded layer: Xe is already NHWC with Ce channels, gy NHWC is shared

@@ -230,14 +230,17 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
                                     int64_t K, int64_t C, int64_t kH, int64_t kW, int64_t Cp,
                                     int splits, int64_t ld, int64_t split_stride, float scale,
                                     int accumulate) {
+    // thread index: k fastest, so each split's partial row is read coalesced
     const int64_t total = K * C * kH * kW;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = i % kW, r = (i / kW) % kH, c = (i / (kW * kH)) % C, k = i / (kW * kH * C);
+        const int64_t k = i % K, crs = i / K;
+        const int64_t s = crs % kW, r = (crs / kW) % kH, c = crs / (kW * kH);
         const float* src = part + ((r * kW + s) * Cp + c) * ld + k;
         float acc = 0.f;
         for (int sp = 0; sp < splits; ++sp) acc += src[(int64_t)sp * split_stride];
-        gw[i] = (accumulate ? gw[i] : 0.f) + scale * acc;
+        const int64_t o = k * C * kH * kW + crs;
+        gw[o] = (accumulate ? gw[o] : 0.f) + scale * acc;
     }
 }
 
