@@ -180,6 +180,19 @@ def measure_cublas_tf32(torch):
         return None
 
 
+def ncu_traffic(workload, key):
+    """dram__bytes_read.sum + dram__bytes_write.sum of this launch from the committed
+    `ncu --set full` capture (profiles/ncu_traffic.json), or None when not captured."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        v = t.get(f"{workload}/{key}")
+        return None if v is None else {"bytes": v["bytes"], "source": v["source"]}
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------------- CPU legs
 def cpu_sample_run(layers, batch, threads):
     """One fwd+bwd of every layer at `batch` images through the oracle port (im2col +
@@ -282,7 +295,7 @@ def main():
         b = pt.fill_uniform(torch.empty((K,), device=dev), seed + 3, -0.1, 0.1)
         gy = pt.fill_uniform(torch.empty(g.output_shape(), device=dev), seed + 4)
         bucket = GradBucket([torch.Size(g.weight_shape()), torch.Size((K,))], dev)
-        st.append(dict(g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
+        st.append(dict(name=name, g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
                        gx=torch.empty(g.input_shape(), device=dev), bucket=bucket,
                        gw=bucket.views[0], gb=bucket.views[1]))
     comm = torch.cuda.Stream(device=dev) if world > 1 else None
@@ -292,6 +305,7 @@ def main():
         done = []
         for s in st:
             g = s["g"]
+            L.lib().pt_b200_profile_tag(s["name"].encode())
             pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math)
             pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math)
             # batch-sharded DP: one allreduce(sum) of this layer's gradW||gradB bucket on the
@@ -327,7 +341,6 @@ def main():
     launches = pt.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     prof = {c: L.profile_read(c) for c in ("umma_conv", "umma_wgrad", "simt_conv", "layout")}
-    L.lib().pt_b200_profile_enable(0)
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -336,26 +349,34 @@ def main():
     flops_step = sum(layer_flops(l) for l in layers)
     value = flops_step * world / (ms_step * 1e-3) / 1e9
 
-    # roofline of the dominant kernel class (by device time inside the timed region)
-    dom = max(prof, key=lambda c: prof[c][0])
-    dms, dn, dfl, dby = prof[dom]
+    # roofline of the dominant kernel: the (layer, pass) tensor-core launch with the
+    # largest device time inside the timed region (CUDA events on its own stream)
+    per = {}
+    for s_ in st:
+        for cls in ("umma_conv", "umma_wgrad", "simt_conv"):
+            for ps in ("fwd", "dgrad", "wgrad"):
+                v = L.profile_read(f"{cls}@{s_['name']}.{ps}")
+                if v[1] > 0:
+                    per[f"{cls}@{s_['name']}.{ps}"] = v
+    L.lib().pt_b200_profile_enable(0)
     tf32_cublas = measure_cublas_tf32(torch) if rank == 0 else None
     tf32_derived = peaks.get("bf16_tflops", 1590.0) / 2.0
-    if dom == "layout":
-        roof = {"bound": "hbm", "achieved": dby / (dms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s"}
-    else:
-        peak_tf = max(tf32_derived, tf32_cublas or 0.0)
-        roof = {"bound": "tensor", "achieved": dfl / (dms * 1e-3) / 1e12, "peak": peak_tf,
-                "unit": "TFLOP/s"}
+    peak_tf = max(tf32_derived, tf32_cublas or 0.0)
+    dom = max(per, key=lambda k: per[k][0])
+    dms, dn, dfl, _ = per[dom]
+    avg_ms = dms / dn
+    roof = {"bound": "tensor", "achieved": dfl / dn / (avg_ms * 1e-3) / 1e12, "peak": peak_tf,
+            "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    roof["traffic"] = ncu_traffic(args.workload, dom)
     roof["kernel"] = dom
-    roof["launches"] = dn
+    roof["avg_launch_ms"] = avg_ms
+    roof["flops_per_launch"] = dfl / dn
     roof["share_of_step"] = dms / ms if ms > 0 else None
     roof["peak_source"] = (f"max(cuBLAS TF32 8192^3 on this box = {tf32_cublas}, "
-                           f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})"
-                           if roof["bound"] == "tensor" else f"{peak_kind} hbm_gbs")
+                           f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})")
+    roof["per_launch"] = {k: {"ms": v[0] / v[1], "tflops": v[2] / v[0] * 1e-9}
+                          for k, v in sorted(per.items())}
 
     result = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,

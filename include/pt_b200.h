@@ -158,7 +158,11 @@ int64_t pt_b200_launch_count(void);
  * "umma_wgrad" (tcgen05 wgrad), "simt_conv" (FFMA passes), "layout" (NHWC/pack passes). */
 int pt_b200_profile_enable(int on);
 int pt_b200_profile_reset(void);
-/* total_ms = summed event durations, launches = count, flops = algorithmic FLOPs,
+/* Label for the launches the calling thread records next (e.g. the layer name); each
+ * launch is also accumulated under "<class>@<tag>.<pass>", pass = fwd | dgrad | wgrad. */
+int pt_b200_profile_tag(const char* tag);
+/* kernel_class: a class name or a "<class>@<tag>.<pass>" key.
+ * total_ms = summed event durations, launches = count, flops = algorithmic FLOPs,
  * bytes = algorithmic HBM bytes (for memory-bound classes). */
 int pt_b200_profile_read(const char* kernel_class, double* total_ms, int64_t* launches,
                          double* flops, double* bytes);

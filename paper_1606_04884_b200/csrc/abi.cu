@@ -84,15 +84,17 @@ size_t bwd_data_ws(const Geo& g, int math) {
 // updateGradInput body. gyh_pre (gy NHWC, round_up(K,32) channels) is used when the
 // chosen engine reads that layout.
 void bwd_data_impl(const Geo& g, const float* gy, const float* w, float* gx, int math, void* ws,
-                   cudaStream_t st, const float* gyh_pre = nullptr) {
+                   cudaStream_t st, const float* gyh_pre = nullptr, bool pre_padded = false) {
+    PassScope pass("dgrad");
     if (dgrad_row(g, math)) {
-        rowdgrad(g, gy, w, gx, ws, st, gyh_pre);
+        rowdgrad(g, gy, w, gx, ws, st, gyh_pre, pre_padded);
         return;
     }
     if (math == PT_MATH_TF32) {
         const UmmaPlan pl = umma_plan(g, true);
         if (pl.ok) {
-            const bool same_layout = pl.cb == 32 && pl.cin_p == umma_wgrad_kp(g);
+            const bool same_layout =
+                pl.cb == 32 && pl.cin_p == umma_wgrad_kp(g) && pl.hankel == pre_padded;
             umma_conv_bwd_data(g, pl, gy, w, gx, ws, st, same_layout ? gyh_pre : nullptr);
             return;
         }
@@ -113,6 +115,7 @@ size_t wgrad_tc_ws(const Geo& g, int math) {
 }
 void wgrad_tc_run(const Geo& g, const float* x, const float* gy, const float* gyh, float* gw, float scale,
                   int accumulate, int math, char* ws, cudaStream_t st) {
+    PassScope pass("wgrad");
     if (wgrad_row(g, math)) rowwgrad(g, x, gyh, gw, scale, accumulate, ws, st);
     else umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, ws, st, gyh);
 }
@@ -136,6 +139,7 @@ size_t bwd_ws(const Geo& g, int math) {
 // accGradParameters body; ws laid out as bwd_filter_ws describes.
 void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, float* gb, float scale,
                      int accumulate, int math, char* ws, cudaStream_t st) {
+    PassScope pass("wgrad");
     if (wgrad_tc(g, math)) {
         float* gyh = reinterpret_cast<float*>(ws);
         float* part = reinterpret_cast<float*>(ws + gyh_bytes(g));
@@ -297,6 +301,7 @@ int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, con
         require_ptr(y, "output");
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
+        PassScope pass("fwd");
         if (fwd_rowconv(g, math)) {
             require_ws(ws_bytes, rowconv_workspace(g), ws);
             rowconv_fwd(g, x, w, b, y, ws, st);
@@ -365,12 +370,32 @@ int pt_b200_conv_bwd(const pt_conv_geom* gp, const float* x, const float* gy, co
             float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
             char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
             char* wws = dws + align_up(bwd_data_ws(g, math), 256);
+            // a Hankel dgrad reads gy zero-bordered: the same pass writes that copy too
+            // (placed where that engine keeps its activation copy inside the dgrad workspace)
+            NhwcDst dpad{};
             {
-                ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
-                nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate,
-                                  part, st);
+                UmmaPlan dpl;
+                size_t off = 0;
+                if (dgrad_row(g, math)) {
+                    rowdgrad_ok(g, &dpl);
+                    off = rowdgrad_act_offset(g);
+                } else {
+                    dpl = umma_plan(g, true);
+                }
+                if (dpl.ok && dpl.hankel && dpl.cin_p == umma_wgrad_kp(g))
+                    dpad = NhwcDst::padded(reinterpret_cast<float*>(dws + off), g.oH, g.oW, dpl.aph,
+                                           dpl.apw);
             }
-            bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
+            {
+                PassScope pass("bwd");
+                ProfScope prof("layout", st, 0.0,
+                               4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g) +
+                                      (dpad.p ? g.N * dpad.img * umma_wgrad_kp(g) : 0)));
+                nchw_to_nhwc_padded(gy, NhwcDst::dense(gyh, g.oHW), dpad, g.N, g.K, g.oH, g.oW,
+                                    umma_wgrad_kp(g), gb, scale, accumulate, part, st);
+            }
+            if (dpad.p) bwd_data_impl(g, gy, w, gx, math, dws, st, dpad.p, true);
+            else bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
             wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st);
             return;
         }

@@ -84,4 +84,10 @@ struct ProfScope {
     ProfScope(const char* c, cudaStream_t s, double f, double b);
     ~ProfScope();
 };
+// Labels the launches recorded while alive with the conv pass ("fwd", "dgrad", "wgrad").
+struct PassScope {
+    const char* prev;
+    explicit PassScope(const char* pass);
+    ~PassScope();
+};
 }  // namespace ptb

@@ -27,6 +27,27 @@ void nchw_to_nhwc(const float* src, float* dst, int64_t N, int64_t C, int64_t HW
 // sums of the unrounded values land in `part` (nhwc_bias_partials_bytes) and a
 // fixed-order reduce writes gb (+)= scale * sum. gb may be null (no bias).
 size_t nhwc_bias_partials_bytes(int64_t N, int64_t C, int64_t HW);
+// Destination of an NCHW -> NHWC transform: pixel (h, w) of an H x W image lands at
+// (h + ph) * Wp + (w + pw) of an image of `img` pixels (dense: Wp = W, img = H*W).
+struct NhwcDst {
+    float* p = nullptr;
+    int64_t W = 1, Wp = 1, ph = 0, pw = 0, img = 0;
+    static NhwcDst dense(float* p, int64_t HW) { return NhwcDst{p, HW, HW, 0, 0, HW}; }
+    static NhwcDst padded(float* p, int64_t H, int64_t W, int64_t ph, int64_t pw) {
+        return NhwcDst{p, W, W + 2 * pw, ph, pw, (H + 2 * ph) * (W + 2 * pw)};
+    }
+    __host__ __device__ int64_t pixel(int64_t p_) const {
+        if (Wp == W) return p_ + ph * Wp;
+        const int64_t h = p_ / W;
+        return (h + ph) * Wp + (p_ - h * W) + pw;
+    }
+};
+// NCHW -> one or two NHWC copies (TF32-rounded, channels zero-padded to Cp), the
+// spatial border of padded destinations zeroed; gradBias fused as in nchw_to_nhwc_bias
+// when gb is set.
+void nchw_to_nhwc_padded(const float* src, const NhwcDst& d0, const NhwcDst& d1, int64_t N,
+                         int64_t C, int64_t H, int64_t W, int64_t Cp, float* gb, float scale,
+                         int accumulate, float* part, cudaStream_t st);
 void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
                        float* gb, float scale, int accumulate, float* part, cudaStream_t st);
 // Weight packing for the implicit GEMM B operand. W is KCRS [K][C][kH][kW].
@@ -61,7 +82,20 @@ struct UmmaPlan {
     int64_t n_pad = 0;    // n_tiles * bn
     int64_t act_elems = 0, wt_elems = 0;  // workspace floats
     size_t ws_bytes = 0;
+    // Hankel pixel-run engine (umma_hconv.cu): stride 1, 32-channel chunks, CTA pair.
+    // The activation is then stored zero-bordered: [N][aHp][aWp][cin_p], border (aph, apw).
+    bool hankel = false;
+    int64_t aH = 0, aW = 0, aph = 0, apw = 0, aHp = 0, aWp = 0;
 };
+struct HConvTiling {
+    int64_t P_img = 0;  // positions per image
+    int64_t tiles = 0;  // 256-position pair tiles
+};
+HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH);
+// act: zero-bordered NHWC [N][Hp][Wp][cin_p]; stride-1 kH x kW conv -> oH x oW NCHW.
+void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, int64_t Hp,
+               int64_t Wp, int kH, int kW, int64_t oH, int64_t oW, float* out, const float* bias,
+               double alg_flops, cudaStream_t st);
 // fprop: act = x (C channels, HxW), n_rows = K.
 // dgrad, kDgradTconv: act = gy (K channels, oHxoW), n_rows = C, flipped weights,
 //   pad' = k-1-pad (stride 1).  kDgradGcol (small C / strided): gcol = W^T gy as a
@@ -69,7 +103,8 @@ struct UmmaPlan {
 UmmaPlan umma_plan(const Geo& g, bool dgrad);
 void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float* w,
                    const float* b, float* y, void* ws, cudaStream_t st);
-// gyh_pre: gy already in NHWC [N][oHW][pl.cin_p] (TF32-rounded), or null to transform here.
+// gyh_pre: gy already in the plan's NHWC layout (TF32-rounded; zero-bordered when
+// pl.hankel), or null to transform here.
 void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
                         float* gx, void* ws, cudaStream_t st, const float* gyh_pre = nullptr,
                         double alg_flops = -1.0);
@@ -77,8 +112,11 @@ void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const
 // ---- umma_rowwgrad.cu: small-C dgrad = tconv of the (kH x 1) row-expanded layer + 1-D fold ----
 bool rowdgrad_ok(const Geo& g, UmmaPlan* plan = nullptr);
 size_t rowdgrad_workspace(const Geo& g);
+// gyh_pre: gy NHWC (round_up(K,32) channels), zero-bordered for the expanded layer's
+// Hankel plan when pre_padded; used only if it matches the plan's layout.
 void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st,
-              const float* gyh_pre = nullptr);
+              const float* gyh_pre = nullptr, bool pre_padded = false);
+size_t rowdgrad_act_offset(const Geo& g);  // byte offset of the engine's activation buffer in ws
 
 // ---- umma_rowconv.cu: small-C (<=4), stride-1 forward via the Hankel row view ----
 // x NCHW -> zero-bordered NHWC4 xp[n][Hp][Wa][4] (TF32-rounded)

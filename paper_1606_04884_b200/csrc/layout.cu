@@ -23,14 +23,15 @@ __device__ __forceinline__ float to_tf32(float v) {
 // part[(n * strips + strip) * C + c]. grid = (strips, ceil(Cp/32), N), block = 32x8.
 constexpr int kStripPx = 128;
 
-__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __restrict__ dst,
+__global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, NhwcDst d1,
                                     int64_t C, int64_t HW, int64_t Cp, int round_tf32,
                                     float* __restrict__ part) {
     __shared__ float tile[32][33];
     const int64_t n = blockIdx.z;
     const int64_t c0 = (int64_t)blockIdx.y * 32;
     const float* s = src + n * C * HW;
-    float* d = dst + n * HW * Cp;
+    float* o0 = d0.p + n * d0.img * Cp;
+    float* o1 = d1.p ? d1.p + n * d1.img * Cp : nullptr;
     float rowsum[4] = {0.f, 0.f, 0.f, 0.f};
     for (int t = 0; t < kStripPx / 32; ++t) {
         const int64_t p0 = (int64_t)blockIdx.x * kStripPx + t * 32;
@@ -49,7 +50,9 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __rest
             const int64_t p = p0 + threadIdx.y + i, c = c0 + threadIdx.x;
             if (p < HW && c < Cp) {
                 float v = tile[threadIdx.x][threadIdx.y + i];
-                d[p * Cp + c] = round_tf32 ? to_tf32(v) : v;
+                if (round_tf32) v = to_tf32(v);
+                o0[d0.pixel(p) * Cp + c] = v;
+                if (o1) o1[d1.pixel(p) * Cp + c] = v;
             }
         }
         __syncthreads();
@@ -64,6 +67,20 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, float* __rest
             const int64_t c = c0 + threadIdx.y + 8 * i;
             if (threadIdx.x == 0 && c < C) part[(n * gridDim.x + blockIdx.x) * C + c] = v;
         }
+    }
+}
+
+// Zero the spatial border of a padded NHWC image stack dst[n][Hp][Wp][Cp] (interior
+// pixels h in [ph, ph+H), w in [pw, pw+W) are left alone). float4 stores.
+__global__ void zero_border_kernel(float4* __restrict__ dst, int64_t N, int Hp, int Wp, int ph, int pw,
+                                   int H, int W, int cp4) {
+    const int64_t total = N * Hp * Wp * (int64_t)cp4;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pix = e / cp4;
+        const int hw = (int)(pix % ((int64_t)Hp * Wp));
+        const int h = hw / Wp - ph, w = hw % Wp - pw;
+        if (h < 0 || h >= H || w < 0 || w >= W) dst[e] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -203,8 +220,35 @@ void nchw_to_nhwc(const float* src, float* dst, int64_t N, int64_t C, int64_t HW
     }
     PTB_REQUIRE(N <= 65535, "nchw_to_nhwc: batch too large");
     dim3 grid((unsigned)ceil_div(HW, kStripPx), (unsigned)ceil_div(Cp, 32), (unsigned)N);
-    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, dst, C, HW, Cp, round_tf32, nullptr);
+    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, NhwcDst::dense(dst, HW), NhwcDst{}, C,
+                                                       HW, Cp, round_tf32, nullptr);
     after_launch("nchw_to_nhwc");
+}
+
+void nchw_to_nhwc_padded(const float* src, const NhwcDst& d0, const NhwcDst& d1, int64_t N,
+                         int64_t C, int64_t H, int64_t W, int64_t Cp, float* gb, float scale,
+                         int accumulate, float* part, cudaStream_t st) {
+    PTB_REQUIRE(N <= 65535 && Cp >= C && Cp % 4 == 0, "nchw_to_nhwc_padded: bad shape");
+    const int64_t HW = H * W;
+    for (const NhwcDst* d : {&d0, &d1}) {
+        if (!d->p || d->img == HW) continue;
+        const int Hp = (int)(d->img / d->Wp);
+        const int64_t total = N * d->img * (Cp / 4);
+        const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * (int64_t)sm_count());
+        zero_border_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<float4*>(d->p), N, Hp, (int)d->Wp,
+                                                   (int)d->ph, (int)d->pw, (int)H, (int)W,
+                                                   (int)(Cp / 4));
+        after_launch("zero_border");
+    }
+    const int64_t strips = ceil_div(HW, kStripPx);
+    dim3 grid((unsigned)strips, (unsigned)ceil_div(Cp, 32), (unsigned)N);
+    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, d0, d1, C, HW, Cp, 1, gb ? part : nullptr);
+    after_launch("nchw_to_nhwc_padded");
+    if (gb) {
+        bias_from_partials_kernel<<<(unsigned)C, 256, 0, st>>>(part, N * strips, C, gb, scale,
+                                                               accumulate);
+        after_launch("bias_from_partials");
+    }
 }
 
 size_t nhwc_bias_partials_bytes(int64_t N, int64_t C, int64_t HW) {
@@ -216,7 +260,8 @@ void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64
     PTB_REQUIRE(N <= 65535 && Cp >= C, "nchw_to_nhwc_bias: bad shape");
     const int64_t strips = ceil_div(HW, kStripPx);
     dim3 grid((unsigned)strips, (unsigned)ceil_div(Cp, 32), (unsigned)N);
-    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, dst, C, HW, Cp, 1, gb ? part : nullptr);
+    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, NhwcDst::dense(dst, HW), NhwcDst{}, C,
+                                                       HW, Cp, 1, gb ? part : nullptr);
     after_launch("nchw_to_nhwc_bias");
     if (gb) {
         bias_from_partials_kernel<<<(unsigned)C, 256, 0, st>>>(part, N * strips, C, gb, scale,

@@ -11,7 +11,7 @@ namespace ptb {
 
 namespace {
 struct Pending {
-    std::string cls;
+    std::string cls, key;
     cudaEvent_t e0, e1;
     double flops, bytes;
 };
@@ -23,17 +23,22 @@ std::atomic<bool> g_on{false};
 std::mutex g_mu;
 std::vector<Pending> g_pending;
 std::map<std::string, Totals> g_totals;
+thread_local std::string g_tag;        // caller label (bench: the layer name)
+thread_local const char* g_pass = "";  // set by the ABI entry point (fwd / dgrad / wgrad)
 
 void drain_locked() {
     for (auto& p : g_pending) {
         float ms = 0.f;
         cudaEventSynchronize(p.e1);
         cudaEventElapsedTime(&ms, p.e0, p.e1);
-        Totals& t = g_totals[p.cls];
-        t.ms += ms;
-        t.flops += p.flops;
-        t.bytes += p.bytes;
-        t.launches += 1;
+        for (const std::string* k : {&p.cls, &p.key}) {
+            if (k->empty()) continue;
+            Totals& t = g_totals[*k];
+            t.ms += ms;
+            t.flops += p.flops;
+            t.bytes += p.bytes;
+            t.launches += 1;
+        }
         cudaEventDestroy(p.e0);
         cudaEventDestroy(p.e1);
     }
@@ -42,6 +47,9 @@ void drain_locked() {
 }  // namespace
 
 bool prof_enabled() { return g_on.load(std::memory_order_relaxed); }
+
+PassScope::PassScope(const char* pass) : prev(g_pass) { g_pass = pass; }
+PassScope::~PassScope() { g_pass = prev; }
 
 ProfScope::ProfScope(const char* c, cudaStream_t s, double f, double b)
     : cls(c), st(s), flops(f), bytes(b) {
@@ -56,7 +64,9 @@ ProfScope::~ProfScope() {
     cudaEventCreate(&e1);
     cudaEventRecord(e1, st);
     std::lock_guard<std::mutex> lk(g_mu);
-    g_pending.push_back({cls, e0, e1, flops, bytes});
+    // per-launch key "class@tag.pass" (e.g. umma_conv@L2.dgrad) beside the class total
+    std::string key = g_tag.empty() && !*g_pass ? std::string() : std::string(cls) + "@" + g_tag + "." + g_pass;
+    g_pending.push_back({cls, std::move(key), e0, e1, flops, bytes});
 }
 
 }  // namespace ptb
@@ -64,6 +74,10 @@ ProfScope::~ProfScope() {
 extern "C" {
 int pt_b200_profile_enable(int on) {
     ptb::g_on.store(on != 0);
+    return PT_OK;
+}
+int pt_b200_profile_tag(const char* tag) {
+    ptb::g_tag = tag ? tag : "";
     return PT_OK;
 }
 int pt_b200_profile_reset(void) {

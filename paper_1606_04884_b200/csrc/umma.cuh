@@ -269,8 +269,11 @@ __device__ __forceinline__ void store_tmem_columns_nchw(uint32_t taddr, int ncol
                     o += chan_stride;
                 }
             } else {
-                for (int q = 0; q < 16 && chb + q < n_valid; ++q) {
-                    __stcs(o, __uint_as_float(v[q]) + bv[q]);
+                // fully unrolled + predicated: a data-dependent trip count would force
+                // v[] / bv[] into local memory
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    if (chb + q < n_valid) __stcs(o, __uint_as_float(v[q]) + bv[q]);
                     o += chan_stride;
                 }
             }

@@ -29,6 +29,8 @@
 //   warps 2..5  epilogue (warp w owns TMEM lanes 32*(w%4) .. +31)
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "tmap.cuh"
 #include "umma.cuh"
@@ -398,6 +400,34 @@ void plan_rows(UmmaPlan& pl) {
     pl.wt_elems = pl.cb == 32 ? pl.n_pad * kdim_p : pl.slots_p * pl.n_pad * 4;
 }
 
+// Hankel engine choice: the pixel-run kernel wastes the border columns it computes
+// (valid / computed positions); the im2col kernel wastes nothing but is L2->SM bound.
+int hconv_env() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_HCONV");
+        return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+
+void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, int64_t pw, int64_t kW,
+                 int64_t oH, int64_t oW) {
+    if (pl.cb != 32 || pl.cg != 2 || kW > 120 || hconv_env() != 1) return;  // opt-in for now
+    const int64_t Hp = aH + 2 * ph, Wp = aW + 2 * pw;
+    if (N * Hp * Wp >= (1ll << 31)) return;
+    const HConvTiling t = hconv_tiling(N, Hp, Wp, oH);
+    const double eff = (double)(N * oH * oW) / (double)(t.tiles * 256);
+    if (eff < 0.6) return;
+    pl.hankel = true;
+    pl.aH = aH;
+    pl.aW = aW;
+    pl.aph = ph;
+    pl.apw = pw;
+    pl.aHp = Hp;
+    pl.aWp = Wp;
+    pl.act_elems = N * Hp * Wp * pl.cin_p;
+}
+
 }  // namespace
 
 UmmaPlan umma_plan(const Geo& g, bool dgrad) {
@@ -415,6 +445,7 @@ UmmaPlan umma_plan(const Geo& g, bool dgrad) {
         plan_channels(pl, g.C);
         plan_rows(pl);
         pl.act_elems = g.N * g.HW * pl.cin_p;
+        if (g.sH == 1 && g.sW == 1) plan_hankel(pl, g.N, g.H, g.W, g.pH, g.pW, g.kW, g.oH, g.oW);
     } else {
         const bool tconv_ok = g.sH == 1 && g.sW == 1 && g.pH <= g.kH - 1 && g.pW <= g.kW - 1 &&
                               g.kH <= 129 && g.kW <= 129 && g.C <= 65536;
@@ -436,6 +467,7 @@ UmmaPlan umma_plan(const Geo& g, bool dgrad) {
             plan_channels(pl, g.K);
             plan_rows(pl);
             pl.act_elems = g.N * g.oHW * pl.cin_p;
+            plan_hankel(pl, g.N, g.oH, g.oW, g.kH - 1 - g.pH, g.kW - 1 - g.pW, g.kW, g.H, g.W);
         } else {
             return pl;
         }
@@ -451,6 +483,18 @@ void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float
                    const float* b, float* y, void* ws, cudaStream_t st) {
     float* act = reinterpret_cast<float*>(ws);
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
+    if (pl.hankel) {
+        {
+            ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + pl.act_elems));
+            nchw_to_nhwc_padded(x, NhwcDst::padded(act, g.H, g.W, g.pH, g.pW), NhwcDst{}, g.N, g.C,
+                                g.H, g.W, pl.cin_p, nullptr, 1.f, 0, nullptr, st);
+        }
+        pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackFprop, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
+                     pl.wt_elems, true, st);
+        run_hconv(pl, act, wt, g.N, pl.aHp, pl.aWp, (int)g.kH, (int)g.kW, g.oH, g.oW, y, b,
+                  2.0 * g.M * g.K * g.CRS, st);
+        return;
+    }
     {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + g.N * g.HW * pl.cin_p));
         nchw_to_nhwc(x, act, g.N, g.C, g.HW, pl.cin_p, true, st);
@@ -468,9 +512,20 @@ void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
     if (gyh_pre) {
         act = const_cast<float*>(gyh_pre);
+    } else if (pl.hankel) {
+        ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.K * g.oHW + pl.act_elems));
+        nchw_to_nhwc_padded(gy, NhwcDst::padded(act, g.oH, g.oW, pl.aph, pl.apw), NhwcDst{}, g.N, g.K,
+                            g.oH, g.oW, pl.cin_p, nullptr, 1.f, 0, nullptr, st);
     } else {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.K * g.oHW + g.N * g.oHW * pl.cin_p));
         nchw_to_nhwc(gy, act, g.N, g.K, g.oHW, pl.cin_p, true, st);
+    }
+    if (pl.hankel) {
+        pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackDgradFlip, pl.cb, pl.n_pad, pl.cin_p,
+                     pl.slots_p, pl.wt_elems, true, st);
+        run_hconv(pl, act, wt, g.N, pl.aHp, pl.aWp, (int)g.kH, (int)g.kW, g.H, g.W, gx, nullptr,
+                  alg_flops, st);
+        return;
     }
     if (pl.mode == UmmaPlan::kDgradTconv) {
         pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackDgradFlip, pl.cb, pl.n_pad, pl.cin_p,

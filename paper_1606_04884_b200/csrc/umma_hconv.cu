@@ -1,0 +1,341 @@
+// umma_hconv.cu — tcgen05 (kind::tf32) stride-1 convolution over a zero-bordered NHWC
+// activation with the im2col operand taken as a Hankel view of ONE pixel run per
+// (filter row, channel chunk): fprop (updateOutput) and the stride-1
+// input gradient as a transposed conv with the flipped filter.
+//
+// Position space. The activation is stored padded, xp[n][Hp][Wp][Cp] (Cp = C rounded up
+// to 32), flattened to pixels P = (n*Hp + h)*Wp + w. An output position q = i*Wp + j of
+// image n (j may run past oW into the right border: those columns are computed and
+// discarded) reads, for filter tap (r, s), the pixel n*Hp*Wp + q + r*Wp + s. So for a
+// run of 128 consecutive positions the im2col tile of tap (r, s) is the pixel run
+// starting at q0 + r*Wp, shifted by s: ONE TMA box of 128 + kW - 1 pixels x 32 channels
+// (128B-swizzled, K-major, a pixel = one 128-byte row) feeds all kW taps of filter row r
+// — the tcgen05 smem descriptor simply starts s rows (s*128 bytes) further in. The
+// im2col-mode kernel (umma_conv.cu) re-fetches the overlapping pixels once per tap, and
+// its L2->SM traffic, not the tensor pipe, bounds it (ncu: 13.2 TB/s of TMA reads on
+// convnet L2 dgrad at 28% tensor-pipe activity).
+//
+// Positions are tiled either per image (P_img = oH*Wp rounded up to the 256-position
+// pair tile; a tile never crosses images) or flat over the batch (P_img = Hp*Wp; a tile
+// may span two images, the pixel index is then just the global position). The host
+// picks whichever wastes fewer positions.
+//
+// CTA pair (cta_group::2): M = 256 positions (128 per CTA), N = BN output channels (each
+// CTA stages BN/2 weight rows). Two smem rings: A (pixel runs, one per (r, chunk)) and B
+// (weight tiles, one per (r, s, chunk)); the MMA issuer consumes kW B stages per A stage.
+// TMEM holds two BN-column accumulators so the epilogue of tile t overlaps tile t+1.
+//
+// Warp roles (192 threads, 1 CTA/SM, persistent): warp 0 TMA producer, warp 1 TMEM
+// allocator + MMA issuer (pair leader), warps 2..5 epilogue (TMEM -> +bias -> NCHW).
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "kernels.cuh"
+#include "tmap.cuh"
+#include "umma.cuh"
+
+namespace ptb {
+
+namespace {
+
+using namespace umma;
+
+constexpr int kThreadsH = 192;
+constexpr int kSmemLimitH = 232448;
+
+struct HConvParams {
+    CUtensorMap tmap_a;  // act, 2-D: {Cp, N*Hp*Wp}, box {32, rbox}, SW128
+    CUtensorMap tmap_b;  // packed weights, 2-D: {kdim, n_pad}, box {32, BN/2}, SW128
+    int N, Hp, Wp, kH, kW, chunks, cin_p;
+    int oH, oW;          // valid output extent
+    int64_t P_img;       // positions per image in the tiling
+    int64_t img_px;      // Hp*Wp
+    int tiles;           // 256-position pair tiles
+    int n_rows, bn, n_tiles;
+    int sa, sb;          // ring depths
+    uint32_t stage_a, stage_b;
+    uint32_t tmem_cols;
+    int desc_base_off;   // 1: encode the 128B-swizzle phase of shifted starts (bits 49-51)
+    float* out;
+    const float* bias;
+};
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr, int base_off) {
+    uint64_t d = smem_desc(addr, 16, 1024, kSwizzle128B);
+    if (base_off) d |= (uint64_t)((addr >> 7) & 7) << 49;
+    return d;
+}
+
+__global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_constant__ HConvParams p) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + ((((raw + 1023u) & ~1023u)) - raw);
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + (size_t)p.sa * p.stage_a;
+    uint64_t* afull = reinterpret_cast<uint64_t*>(sB + (size_t)p.sb * p.stage_b);
+    uint64_t* aempty = afull + p.sa;
+    uint64_t* bfull = aempty + p.sa;
+    uint64_t* bempty = bfull + p.sb;
+    uint64_t* tfull = bempty + p.sb;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.tmap_a);
+        tma_prefetch(&p.tmap_b);
+        for (int i = 0; i < p.sa; ++i) {
+            mbar_init(&afull[i], 2);
+            mbar_init(&aempty[i], 1);
+        }
+        for (int i = 0; i < p.sb; ++i) {
+            mbar_init(&bfull[i], 2);
+            mbar_init(&bempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc_cg2(tmem_holder, p.tmem_cols);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+    const int num_units = p.tiles * p.n_tiles;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer (both CTAs; bytes complete on the leader's barriers) =====
+            int as = 0, bs = 0;
+            uint32_t aph = 0, bph = 0;
+            const uint32_t atx = 2 * p.stage_a, btx = 2 * p.stage_b;
+            for (int u = cid; u < num_units; u += ncl) {
+                const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
+                const int64_t g0 = (int64_t)t * 256 + (int64_t)rank * 128;
+                const int64_t n = g0 / p.P_img;
+                const int64_t pix0 = n * p.img_px + (g0 - n * p.P_img);
+                const int brow = nt * p.bn + (int)rank * (p.bn / 2);
+                for (int r = 0; r < p.kH; ++r) {
+                    for (int cc = 0; cc < p.chunks; ++cc) {
+                        mbar_wait(&aempty[as], aph ^ 1);
+                        if (leader) mbar_arrive_expect_tx(&afull[as], atx);
+                        else mbar_arrive_cluster(&afull[as], 0);
+                        tma_load_2d_cg2(sA + (size_t)as * p.stage_a, &p.tmap_a, &afull[as], cc * 32,
+                                        (int)(pix0 + (int64_t)r * p.Wp));
+                        if (++as == p.sa) {
+                            as = 0;
+                            aph ^= 1;
+                        }
+                        for (int s = 0; s < p.kW; ++s) {
+                            mbar_wait(&bempty[bs], bph ^ 1);
+                            if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
+                            else mbar_arrive_cluster(&bfull[bs], 0);
+                            tma_load_2d_cg2(sB + (size_t)bs * p.stage_b, &p.tmap_b, &bfull[bs],
+                                            (r * p.kW + s) * p.cin_p + cc * 32, brow);
+                            if (++bs == p.sb) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ===== MMA issuer =====
+            const uint32_t idesc = idesc_tf32(256, p.bn, 0, 0);
+            int as = 0, bs = 0;
+            uint32_t aph = 0, bph = 0;
+            int it = 0;
+            for (int u = cid; u < num_units; u += ncl, ++it) {
+                const uint32_t acc = it & 1;
+                mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * p.bn;
+                bool first = true;
+                for (int r = 0; r < p.kH; ++r) {
+                    for (int cc = 0; cc < p.chunks; ++cc) {
+                        mbar_wait(&afull[as], aph);
+                        tc_fence_after();
+                        const uint32_t a = smem_u32(sA + (size_t)as * p.stage_a);
+                        for (int s = 0; s < p.kW; ++s) {
+                            mbar_wait(&bfull[bs], bph);
+                            tc_fence_after();
+                            const uint32_t b = smem_u32(sB + (size_t)bs * p.stage_b);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                mma_tf32_cg2(d, sw128_desc(a + (uint32_t)s * 128u + k * 32u, p.desc_base_off),
+                                             smem_desc(b + k * 32u, 16, 1024, kSwizzle128B), idesc,
+                                             first ? 0u : 1u);
+                                first = false;
+                            }
+                            mma_commit_cg2(&bempty[bs]);
+                            if (++bs == p.sb) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
+                        }
+                        mma_commit_cg2(&aempty[as]);
+                        if (++as == p.sa) {
+                            as = 0;
+                            aph ^= 1;
+                        }
+                    }
+                }
+                mma_commit_cg2(&tfull[acc]);
+            }
+        }
+    } else {
+        // ===== epilogue: TMEM -> registers -> (+bias) -> NCHW, border columns dropped =====
+        const uint32_t q = warp & 3;
+        const int64_t ohw = (int64_t)p.oH * p.oW;
+        int it = 0;
+        for (int u = cid; u < num_units; u += ncl, ++it) {
+            const uint32_t acc = it & 1;
+            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            tc_fence_after();
+            const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
+            const int64_t gpos = (int64_t)t * 256 + (int64_t)rank * 128 + q * 32 + lane;
+            const int64_t n = gpos / p.P_img;
+            const int64_t qq = gpos - n * p.P_img;
+            const int64_t i = qq / p.Wp, j = qq - i * p.Wp;
+            const bool valid = n < p.N && i < p.oH && j < p.oW;
+            const int ch0 = nt * p.bn;
+            const int64_t base = (n * p.n_rows + ch0) * ohw + i * p.oW + j;
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
+            store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base : 0), ohw, p.bias, ch0,
+                                    p.n_rows, valid);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(&tempty[acc], 0);
+            }
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc_cg2(tmem_base, p.tmem_cols);
+#endif
+}
+
+int hconv_desc_mode() {
+    static const int m = [] {
+        const char* e = std::getenv("PT_B200_HCONV_DESC");
+        return e ? std::atoi(e) : 0;
+    }();
+    return m;
+}
+
+}  // namespace
+
+// Tiling of the position space: per image vs flat, whichever computes fewer positions.
+HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH) {
+    HConvTiling t;
+    const int64_t per_img = ceil_div(oH * Wp, 256) * 256;
+    const int64_t tiles_img = N * per_img / 256;
+    const int64_t tiles_flat = ceil_div((N - 1) * Hp * Wp + oH * Wp, 256);
+    if (tiles_flat < tiles_img) {
+        t.P_img = Hp * Wp;
+        t.tiles = tiles_flat;
+    } else {
+        t.P_img = per_img;
+        t.tiles = tiles_img;
+    }
+    return t;
+}
+
+void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, int64_t Hp,
+               int64_t Wp, int kH, int kW, int64_t oH, int64_t oW, float* out, const float* bias,
+               double alg_flops, cudaStream_t st) {
+    PTB_REQUIRE(pl.cb == 32 && pl.cg == 2, "hconv: needs the 32-channel CTA-pair plan");
+    PTB_REQUIRE(kW <= 120, "hconv: filter too wide for one pixel-run box");
+    HConvParams p;
+    memset(&p, 0, sizeof p);
+    const int rbox = (int)align_up((size_t)(128 + kW - 1), 8);
+    const int64_t npx = N * Hp * Wp;
+    PTB_REQUIRE(npx < (1ll << 31), "hconv: activation too large");
+    {
+        const uint64_t dims[2] = {(uint64_t)pl.cin_p, (uint64_t)npx};
+        const uint64_t strides[1] = {(uint64_t)pl.cin_p * 4};
+        const uint32_t box[2] = {32, (uint32_t)rbox};
+        tmap_tiled(&p.tmap_a, act, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    {
+        const uint64_t kdim = (uint64_t)(ceil_div(pl.taps * pl.cin_p, 64) * 64);
+        const uint64_t dims[2] = {kdim, (uint64_t)pl.n_pad};
+        const uint64_t strides[1] = {kdim * 4};
+        const uint32_t box[2] = {32, (uint32_t)(pl.bn / 2)};
+        tmap_tiled(&p.tmap_b, wt, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+    const HConvTiling tl = hconv_tiling(N, Hp, Wp, oH);
+    PTB_REQUIRE(tl.tiles * (int64_t)pl.n_tiles < (1ll << 31), "hconv: too many tiles");
+    p.N = (int)N;
+    p.Hp = (int)Hp;
+    p.Wp = (int)Wp;
+    p.kH = kH;
+    p.kW = kW;
+    p.cin_p = (int)pl.cin_p;
+    p.chunks = (int)(pl.cin_p / 32);
+    p.oH = (int)oH;
+    p.oW = (int)oW;
+    p.P_img = tl.P_img;
+    p.img_px = Hp * Wp;
+    p.tiles = (int)tl.tiles;
+    p.n_rows = (int)pl.n_rows;
+    p.bn = pl.bn;
+    p.n_tiles = pl.n_tiles;
+    p.stage_a = (uint32_t)rbox * 128u;
+    p.stage_b = (uint32_t)align_up((size_t)(pl.bn / 2), 8) * 128u;
+    // B ring: enough stages to cover two filter rows' worth of taps; A ring: the rest
+    const int budget = kSmemLimitH - 1024 - 512;
+    int sb = std::min(16, std::max(4, 2 * kW));
+    while (sb > 4 && budget - sb * (int)p.stage_b < 3 * (int)p.stage_a) --sb;
+    int sa = (budget - sb * (int)p.stage_b) / (int)p.stage_a;
+    sa = std::min(sa, 8);
+    PTB_REQUIRE(sa >= 2, "hconv: shared memory too small for the rings");
+    p.sa = sa;
+    p.sb = sb;
+    p.tmem_cols = 32;
+    while ((int)p.tmem_cols < 2 * pl.bn) p.tmem_cols <<= 1;
+    p.desc_base_off = hconv_desc_mode();
+    p.out = out;
+    p.bias = bias;
+    const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
+                        (2 * sa + 2 * sb + 4) * 8 + 16;
+    const int units = p.tiles * p.n_tiles;
+    const int ncl = std::min(units, sm_count() / 2);
+    static bool attr = false;
+    if (!attr) {
+        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemLimitH));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * ncl);
+    cfg.blockDim = dim3(kThreadsH);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    ProfScope prof("umma_conv", st, alg_flops, 0.0);
+    PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel, p));
+    after_launch("umma_hconv");
+}
+
+}  // namespace ptb

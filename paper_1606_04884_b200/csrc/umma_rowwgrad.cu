@@ -138,10 +138,16 @@ size_t rowdgrad_workspace(const Geo& g) {
            align_up(pl.ws_bytes, 256);
 }
 
+size_t rowdgrad_act_offset(const Geo& g) {
+    const Geo e = dgrad_rows_geo(g);
+    return align_up((size_t)(g.K * e.C * g.kH) * 4, 256) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256);
+}
+
 void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st,
-              const float* gyh_pre) {
+              const float* gyh_pre, bool pre_padded) {
     UmmaPlan pl;
     PTB_REQUIRE(rowdgrad_ok(g, &pl), "rowdgrad: unsupported geometry");
+    if (pl.hankel != pre_padded) gyh_pre = nullptr;  // not the layout the engine reads
     const Geo e = dgrad_rows_geo(g);
     char* base = reinterpret_cast<char*>(ws);
     float* we = reinterpret_cast<float*>(base);

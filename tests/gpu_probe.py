@@ -50,6 +50,8 @@ if __name__ == "__main__":
         ("tf32 cb32 multi-tile", po.geom(2, 64, 20, 20, 96, 5, 5, 2, 2, 1, 1), "tf32"),
         ("tf32 L5-like", po.geom(2, 384, 13, 13, 384, 3, 3, 0, 0, 1, 1), "tf32"),
         ("tf32 L1-like", po.geom(1, 3, 40, 40, 96, 11, 11, 0, 0, 1, 1), "tf32"),
+        ("tf32 L2-like hconv", po.geom(2, 64, 20, 20, 128, 9, 9, 0, 0, 1, 1), "tf32"),
+        ("tf32 p2 C96", po.geom(2, 96, 17, 19, 80, 5, 5, 2, 2, 1, 1), "tf32"),
         ("tf32 stride4", po.geom(2, 3, 63, 63, 64, 11, 11, 2, 2, 4, 4), "tf32"),
     ]
     for name, g, math in cases:
