@@ -23,6 +23,8 @@ __device__ __forceinline__ float to_tf32(float v) {
 // part[(n * strips + strip) * C + c]. grid = (strips, ceil(Cp/32), N), block = 32x8.
 constexpr int kStripPx = 128;
 
+// PAD: destinations are zero-bordered (pixel index remapped); TWO: write d1 as well.
+template <bool PAD, bool TWO>
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, NhwcDst d1,
                                     int64_t C, int64_t HW, int64_t Cp, int round_tf32,
                                     float* __restrict__ part) {
@@ -31,7 +33,7 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, N
     const int64_t c0 = (int64_t)blockIdx.y * 32;
     const float* s = src + n * C * HW;
     float* o0 = d0.p + n * d0.img * Cp;
-    float* o1 = d1.p ? d1.p + n * d1.img * Cp : nullptr;
+    float* o1 = TWO ? d1.p + n * d1.img * Cp : nullptr;
     float rowsum[4] = {0.f, 0.f, 0.f, 0.f};
     for (int t = 0; t < kStripPx / 32; ++t) {
         const int64_t p0 = (int64_t)blockIdx.x * kStripPx + t * 32;
@@ -51,8 +53,13 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, N
             if (p < HW && c < Cp) {
                 float v = tile[threadIdx.x][threadIdx.y + i];
                 if (round_tf32) v = to_tf32(v);
-                o0[d0.pixel(p) * Cp + c] = v;
-                if (o1) o1[d1.pixel(p) * Cp + c] = v;
+                if constexpr (PAD) {
+                    o0[d0.pixel(p) * Cp + c] = v;
+                    if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
+                } else {
+                    o0[p * Cp + c] = v;
+                    if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
+                }
             }
         }
         __syncthreads();
@@ -70,17 +77,32 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, N
     }
 }
 
-// Zero the spatial border of a padded NHWC image stack dst[n][Hp][Wp][Cp] (interior
-// pixels h in [ph, ph+H), w in [pw, pw+W) are left alone). float4 stores.
+// Zero the spatial border of a padded NHWC image stack dst[n][Hp][Wp][Cp]: only the
+// border pixels are visited (top/bottom rows, then the left/right columns of the
+// interior rows), float4 stores.
 __global__ void zero_border_kernel(float4* __restrict__ dst, int64_t N, int Hp, int Wp, int ph, int pw,
-                                   int H, int W, int cp4) {
-    const int64_t total = N * Hp * Wp * (int64_t)cp4;
+                                   int H, int cp4) {
+    const int64_t per_img = 2ll * ph * Wp + 2ll * H * pw;  // border pixels per image
+    const int64_t total = N * per_img * cp4;
+    const int W = Wp - 2 * pw;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t pix = e / cp4;
-        const int hw = (int)(pix % ((int64_t)Hp * Wp));
-        const int h = hw / Wp - ph, w = hw % Wp - pw;
-        if (h < 0 || h >= H || w < 0 || w >= W) dst[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int64_t bp = e / cp4;
+        const int c4 = (int)(e - bp * cp4);
+        const int64_t n = bp / per_img;
+        int64_t b = bp - n * per_img;
+        int h, w;
+        if (b < 2ll * ph * Wp) {
+            const int r = (int)(b / Wp);
+            w = (int)(b - (int64_t)r * Wp);
+            h = r < ph ? r : H + r;  // rows [0, ph) and [ph + H, Hp)
+        } else {
+            b -= 2ll * ph * Wp;
+            const int r = (int)(b / (2 * pw)), k = (int)(b - (int64_t)r * 2 * pw);
+            h = ph + r;
+            w = k < pw ? k : W + k;
+        }
+        dst[((n * Hp + h) * Wp + w) * cp4 + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -220,8 +242,8 @@ void nchw_to_nhwc(const float* src, float* dst, int64_t N, int64_t C, int64_t HW
     }
     PTB_REQUIRE(N <= 65535, "nchw_to_nhwc: batch too large");
     dim3 grid((unsigned)ceil_div(HW, kStripPx), (unsigned)ceil_div(Cp, 32), (unsigned)N);
-    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, NhwcDst::dense(dst, HW), NhwcDst{}, C,
-                                                       HW, Cp, round_tf32, nullptr);
+    nchw_to_nhwc_kernel<false, false><<<grid, dim3(32, 8), 0, st>>>(src, NhwcDst::dense(dst, HW), NhwcDst{},
+                                                                     C, HW, Cp, round_tf32, nullptr);
     after_launch("nchw_to_nhwc");
 }
 
@@ -233,16 +255,24 @@ void nchw_to_nhwc_padded(const float* src, const NhwcDst& d0, const NhwcDst& d1,
     for (const NhwcDst* d : {&d0, &d1}) {
         if (!d->p || d->img == HW) continue;
         const int Hp = (int)(d->img / d->Wp);
-        const int64_t total = N * d->img * (Cp / 4);
+        const int64_t total = N * (2 * d->ph * d->Wp + 2 * H * d->pw) * (Cp / 4);
+        if (total == 0) continue;
         const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 8 * (int64_t)sm_count());
         zero_border_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<float4*>(d->p), N, Hp, (int)d->Wp,
-                                                   (int)d->ph, (int)d->pw, (int)H, (int)W,
-                                                   (int)(Cp / 4));
+                                                   (int)d->ph, (int)d->pw, (int)H, (int)(Cp / 4));
         after_launch("zero_border");
     }
     const int64_t strips = ceil_div(HW, kStripPx);
     dim3 grid((unsigned)strips, (unsigned)ceil_div(Cp, 32), (unsigned)N);
-    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, d0, d1, C, HW, Cp, 1, gb ? part : nullptr);
+    float* pp = gb ? part : nullptr;
+    const bool pad = d0.img != HW;
+    if (d1.p) {
+        if (pad) nchw_to_nhwc_kernel<true, true><<<grid, dim3(32, 8), 0, st>>>(src, d0, d1, C, HW, Cp, 1, pp);
+        else nchw_to_nhwc_kernel<false, true><<<grid, dim3(32, 8), 0, st>>>(src, d0, d1, C, HW, Cp, 1, pp);
+    } else {
+        if (pad) nchw_to_nhwc_kernel<true, false><<<grid, dim3(32, 8), 0, st>>>(src, d0, d1, C, HW, Cp, 1, pp);
+        else nchw_to_nhwc_kernel<false, false><<<grid, dim3(32, 8), 0, st>>>(src, d0, d1, C, HW, Cp, 1, pp);
+    }
     after_launch("nchw_to_nhwc_padded");
     if (gb) {
         bias_from_partials_kernel<<<(unsigned)C, 256, 0, st>>>(part, N * strips, C, gb, scale,
@@ -260,8 +290,8 @@ void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64
     PTB_REQUIRE(N <= 65535 && Cp >= C, "nchw_to_nhwc_bias: bad shape");
     const int64_t strips = ceil_div(HW, kStripPx);
     dim3 grid((unsigned)strips, (unsigned)ceil_div(Cp, 32), (unsigned)N);
-    nchw_to_nhwc_kernel<<<grid, dim3(32, 8), 0, st>>>(src, NhwcDst::dense(dst, HW), NhwcDst{}, C,
-                                                       HW, Cp, 1, gb ? part : nullptr);
+    nchw_to_nhwc_kernel<false, false><<<grid, dim3(32, 8), 0, st>>>(src, NhwcDst::dense(dst, HW), NhwcDst{},
+                                                                     C, HW, Cp, 1, gb ? part : nullptr);
     after_launch("nchw_to_nhwc_bias");
     if (gb) {
         bias_from_partials_kernel<<<(unsigned)C, 256, 0, st>>>(part, N * strips, C, gb, scale,

@@ -140,6 +140,22 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes
     return d;
 }
 
+// Split form for the MMA issue loops: the high word (SBO, version, layout) is constant
+// per operand layout and the low word (start >> 4 | LBO >> 4 << 16) moves by
+// (byte offset >> 4) — one integer add per descriptor instead of re-encoding. The
+// issuing thread is a single in-order thread; with full re-encoding per MMA it, not
+// the tensor pipe, sets the pace (tests/mma_bench.cu: 375 vs 64 cycles per M=256,
+// N=128, K=8 MMA).
+__device__ __forceinline__ uint32_t desc_lo(uint32_t saddr, uint32_t lbo_bytes) {
+    return ((saddr >> 4) & 0x3FFFu) | (((lbo_bytes >> 4) & 0x3FFFu) << 16);
+}
+__host__ __device__ constexpr uint32_t desc_hi(uint32_t sbo_bytes, uint32_t layout) {
+    return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14) | ((layout & 7u) << 29);
+}
+__device__ __forceinline__ uint64_t desc_make(uint32_t lo, uint32_t hi) {
+    return ((uint64_t)hi << 32) | (uint64_t)lo;
+}
+
 // Instruction descriptor for kind::tf32, fp32 accumulate.
 __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, uint32_t a_mn_major,
                                                   uint32_t b_mn_major) {
@@ -221,6 +237,52 @@ __device__ __forceinline__ void mma_tf32_cg2(uint32_t d_tmem, uint64_t a_desc, u
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-converged issue: the whole (converged) warp executes these and one elected lane
+// issues. Keeping the issuing loop warp-uniform lets ptxas hold descriptors in uniform
+// registers; a lane-0-only loop instead wraps every tcgen05.mma in an ELECT /
+// R2UR.BROADCAST sequence whose fixed latencies pace the tensor pipe (ncu: stall_wait on
+// the issuing warp at ~108 cycles per M=256 N=128 MMA).
+__device__ __forceinline__ void mma_tf32_cg2_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_cg2_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+__device__ __forceinline__ void mma_tf32_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ uint32_t warp_id_uniform() {
+    return __shfl_sync(0xffffffffu, threadIdx.x / 32, 0);
+}
+
 // Commit the leader's MMAs to the barrier at the same offset in both CTAs of the pair.
 __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
     asm volatile(

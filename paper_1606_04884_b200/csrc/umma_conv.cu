@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
     const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
@@ -193,9 +193,12 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
+        if (leader) {  // whole warp, converged; one elected lane issues
             // ===== MMA issuer =====
             const uint32_t idesc = idesc_tf32(kTileMC, p.bn, 0, 0);
+            constexpr uint32_t kHiSW128 = desc_hi(1024, kSwizzle128B), kHiNone = desc_hi(128, kSwizzleNone);
+            const uint32_t bhalf16 = (p.stage_b / 2) >> 4;      // CG=2: second box of B
+            const uint32_t bstep4 = (uint32_t)(2 * p.bn * 16) >> 4;  // CB=4: next K=8 slab of B
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -209,38 +212,40 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
                     tc_fence_after();
                     const uint32_t a = smem_u32(sA + (size_t)stage * p.stage_a);
                     const uint32_t b = smem_u32(sB + (size_t)stage * p.stage_b);
+                    const uint32_t acc0 = kb != 0;
                     if constexpr (CG == 2) {
+                        const uint32_t alo = desc_lo(a, 16), blo = desc_lo(b, 16);
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
-                            const uint32_t ao = (k >> 2) * kBoxA + (k & 3) * 32;
-                            const uint32_t bo = (k >> 2) * (p.stage_b / 2) + (k & 3) * 32;
-                            mma_tf32_cg2(d, smem_desc(a + ao, 16, 1024, kSwizzle128B),
-                                         smem_desc(b + bo, 16, 1024, kSwizzle128B), idesc,
-                                         (kb | k) != 0);
+                            const uint32_t ao = ((k >> 2) * kBoxA + (k & 3) * 32) >> 4;
+                            const uint32_t bo = (k >> 2) * bhalf16 + (uint32_t)(k & 3) * 2u;
+                            mma_tf32_cg2_warp(d, desc_make(alo + ao, kHiSW128), desc_make(blo + bo, kHiSW128),
+                                         idesc, k ? 1u : acc0);
                         }
-                        mma_commit_cg2(&empty[stage]);
+                        mma_commit_cg2_warp(&empty[stage]);
                     } else {
+                        if constexpr (CB == 32) {
+                            const uint32_t alo = desc_lo(a, 16), blo = desc_lo(b, 16);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            uint64_t ad, bd;
-                            if constexpr (CB == 32) {
-                                ad = smem_desc(a + k * 32, 16, 1024, kSwizzle128B);
-                                bd = smem_desc(b + k * 32, 16, 1024, kSwizzle128B);
-                            } else {
-                                ad = smem_desc(a + k * 4096, 2048, 128, kSwizzleNone);
-                                bd = smem_desc(b + k * 2 * p.bn * 16, p.bn * 16, 128, kSwizzleNone);
-                            }
-                            mma_tf32(d, ad, bd, idesc, (kb | k) != 0);
+                            for (int k = 0; k < 4; ++k)
+                                mma_tf32_warp(d, desc_make(alo + 2 * k, kHiSW128), desc_make(blo + 2 * k, kHiSW128),
+                                         idesc, k ? 1u : acc0);
+                        } else {
+                            const uint32_t alo = desc_lo(a, 2048), blo = desc_lo(b, p.bn * 16);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                mma_tf32_warp(d, desc_make(alo + k * 256, kHiNone), desc_make(blo + k * bstep4, kHiNone),
+                                         idesc, k ? 1u : acc0);
                         }
-                        mma_commit(&empty[stage]);
+                        mma_commit_warp(&empty[stage]);
                     }
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                if constexpr (CG == 2) mma_commit_cg2(&tfull[acc]);
-                else mma_commit(&tfull[acc]);
+                if constexpr (CG == 2) mma_commit_cg2_warp(&tfull[acc]);
+                else mma_commit_warp(&tfull[acc]);
             }
         }
     } else {
@@ -412,12 +417,17 @@ int hconv_env() {
 
 void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, int64_t pw, int64_t kW,
                  int64_t oH, int64_t oW) {
-    if (pl.cb != 32 || pl.cg != 2 || kW > 120 || hconv_env() != 1) return;  // opt-in for now
+    if (pl.cb != 32 || pl.cg != 2 || kW < 3 || kW > 120 || hconv_env() == 0) return;
     const int64_t Hp = aH + 2 * ph, Wp = aW + 2 * pw;
     if (N * Hp * Wp >= (1ll << 31)) return;
-    const HConvTiling t = hconv_tiling(N, Hp, Wp, oH);
-    const double eff = (double)(N * oH * oW) / (double)(t.tiles * 256);
-    if (eff < 0.6) return;
+    // efficiency from the geometry alone (not N) so a batch and its per-image slices
+    // always take the same engine (batched == per-image bitwise)
+    const double eff = (double)(oH * oW) /
+                       (double)std::min(Hp * Wp, ceil_div(oH * Wp, 256) * 256);
+    // measured (convnet L2/L3/L5): the pixel-run kernel wins at >= 0.85 of positions valid,
+    // ties near 0.8 and loses below, where the im2col kernel's zero waste pays for its
+    // L2->SM traffic
+    if (hconv_env() != 1 && eff < 0.84) return;
     pl.hankel = true;
     pl.aH = aH;
     pl.aW = aW;

@@ -54,19 +54,15 @@ struct HConvParams {
     int tiles;           // 256-position pair tiles
     int n_rows, bn, n_tiles;
     int sa, sb;          // ring depths
-    uint32_t stage_a, stage_b;
+    uint32_t stage_a, stage_b;  // bytes per stage (CPS boxes)
+    uint32_t box_a, box_b;      // bytes per 32-channel box
+    int exp;                    // timing experiments (PT_B200_HCONV_EXP; wrong results if != 0)
     uint32_t tmem_cols;
-    int desc_base_off;   // 1: encode the 128B-swizzle phase of shifted starts (bits 49-51)
     float* out;
     const float* bias;
 };
 
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr, int base_off) {
-    uint64_t d = smem_desc(addr, 16, 1024, kSwizzle128B);
-    if (base_off) d |= (uint64_t)((addr >> 7) & 7) << 49;
-    return d;
-}
-
+template <int CPS>  // 32-channel chunks per pipeline stage (1 or 2)
 __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_constant__ HConvParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ uint8_t smem_raw[];
@@ -82,7 +78,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
@@ -123,12 +119,14 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 const int64_t pix0 = n * p.img_px + (g0 - n * p.P_img);
                 const int brow = nt * p.bn + (int)rank * (p.bn / 2);
                 for (int r = 0; r < p.kH; ++r) {
-                    for (int cc = 0; cc < p.chunks; ++cc) {
+                    for (int cc = 0; cc < p.chunks; cc += CPS) {
                         mbar_wait(&aempty[as], aph ^ 1);
                         if (leader) mbar_arrive_expect_tx(&afull[as], atx);
                         else mbar_arrive_cluster(&afull[as], 0);
-                        tma_load_2d_cg2(sA + (size_t)as * p.stage_a, &p.tmap_a, &afull[as], cc * 32,
-                                        (int)(pix0 + (int64_t)r * p.Wp));
+#pragma unroll
+                        for (int c = 0; c < CPS; ++c)
+                            tma_load_2d_cg2(sA + (size_t)as * p.stage_a + c * p.box_a, &p.tmap_a, &afull[as],
+                                            (cc + c) * 32, (int)(pix0 + (int64_t)r * p.Wp));
                         if (++as == p.sa) {
                             as = 0;
                             aph ^= 1;
@@ -137,8 +135,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             mbar_wait(&bempty[bs], bph ^ 1);
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
                             else mbar_arrive_cluster(&bfull[bs], 0);
-                            tma_load_2d_cg2(sB + (size_t)bs * p.stage_b, &p.tmap_b, &bfull[bs],
-                                            (r * p.kW + s) * p.cin_p + cc * 32, brow);
+#pragma unroll
+                            for (int c = 0; c < CPS; ++c)
+                                tma_load_2d_cg2(sB + (size_t)bs * p.stage_b + c * p.box_b, &p.tmap_b, &bfull[bs],
+                                                (r * p.kW + s) * p.cin_p + (cc + c) * 32, brow);
                             if (++bs == p.sb) {
                                 bs = 0;
                                 bph ^= 1;
@@ -149,9 +149,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
-            // ===== MMA issuer =====
+        if (leader) {
+            // ===== MMA issuer (whole warp, converged; one elected lane issues) =====
             const uint32_t idesc = idesc_tf32(256, p.bn, 0, 0);
+            constexpr uint32_t kHi = desc_hi(1024, kSwizzle128B);
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
             int it = 0;
@@ -160,37 +161,41 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * p.bn;
-                bool first = true;
+                uint32_t accum = 0;
+                const uint32_t box_a16 = p.box_a >> 4, box_b16 = p.box_b >> 4;
                 for (int r = 0; r < p.kH; ++r) {
-                    for (int cc = 0; cc < p.chunks; ++cc) {
+                    for (int cc = 0; cc < p.chunks; cc += CPS) {
                         mbar_wait(&afull[as], aph);
                         tc_fence_after();
-                        const uint32_t a = smem_u32(sA + (size_t)as * p.stage_a);
+                        const uint32_t alo = desc_lo(smem_u32(sA + (size_t)as * p.stage_a), 16);
                         for (int s = 0; s < p.kW; ++s) {
                             mbar_wait(&bfull[bs], bph);
                             tc_fence_after();
-                            const uint32_t b = smem_u32(sB + (size_t)bs * p.stage_b);
+                            // tap s: the same pixel run, s rows (s*128 B) further in
+                            const uint32_t a_s = alo + (p.exp == 2 ? 0u : p.exp == 3 ? (uint32_t)(s & ~7) * 8u
+                                                                                   : (uint32_t)s * 8u);
+                            const uint32_t blo = desc_lo(smem_u32(sB + (size_t)bs * p.stage_b), 16);
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                mma_tf32_cg2(d, sw128_desc(a + (uint32_t)s * 128u + k * 32u, p.desc_base_off),
-                                             smem_desc(b + k * 32u, 16, 1024, kSwizzle128B), idesc,
-                                             first ? 0u : 1u);
-                                first = false;
+                            for (int k = 0; k < 4 * CPS; ++k) {
+                                mma_tf32_cg2_warp(d, desc_make(a_s + (k >> 2) * box_a16 + 2 * (k & 3), kHi),
+                                             desc_make(blo + (k >> 2) * box_b16 + 2 * (k & 3), kHi), idesc,
+                                             accum);
+                                accum = 1;
                             }
-                            mma_commit_cg2(&bempty[bs]);
+                            mma_commit_cg2_warp(&bempty[bs]);
                             if (++bs == p.sb) {
                                 bs = 0;
                                 bph ^= 1;
                             }
                         }
-                        mma_commit_cg2(&aempty[as]);
+                        mma_commit_cg2_warp(&aempty[as]);
                         if (++as == p.sa) {
                             as = 0;
                             aph ^= 1;
                         }
                     }
                 }
-                mma_commit_cg2(&tfull[acc]);
+                mma_commit_cg2_warp(&tfull[acc]);
             }
         }
     } else {
@@ -227,14 +232,6 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     tc_fence_after();
     if (warp == 1) tmem_dealloc_cg2(tmem_base, p.tmem_cols);
 #endif
-}
-
-int hconv_desc_mode() {
-    static const int m = [] {
-        const char* e = std::getenv("PT_B200_HCONV_DESC");
-        return e ? std::atoi(e) : 0;
-    }();
-    return m;
 }
 
 }  // namespace
@@ -295,12 +292,15 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.n_rows = (int)pl.n_rows;
     p.bn = pl.bn;
     p.n_tiles = pl.n_tiles;
-    p.stage_a = (uint32_t)rbox * 128u;
-    p.stage_b = (uint32_t)align_up((size_t)(pl.bn / 2), 8) * 128u;
+    const int cps = p.chunks % 2 == 0 ? 2 : 1;
+    p.box_a = (uint32_t)rbox * 128u;
+    p.box_b = (uint32_t)align_up((size_t)(pl.bn / 2), 8) * 128u;
+    p.stage_a = cps * p.box_a;
+    p.stage_b = cps * p.box_b;
     // B ring: enough stages to cover two filter rows' worth of taps; A ring: the rest
     const int budget = kSmemLimitH - 1024 - 512;
     int sb = std::min(16, std::max(4, 2 * kW));
-    while (sb > 4 && budget - sb * (int)p.stage_b < 3 * (int)p.stage_a) --sb;
+    while (sb > 3 && budget - sb * (int)p.stage_b < 2 * (int)p.stage_a) --sb;
     int sa = (budget - sb * (int)p.stage_b) / (int)p.stage_a;
     sa = std::min(sa, 8);
     PTB_REQUIRE(sa >= 2, "hconv: shared memory too small for the rings");
@@ -308,16 +308,21 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.sb = sb;
     p.tmem_cols = 32;
     while ((int)p.tmem_cols < 2 * pl.bn) p.tmem_cols <<= 1;
-    p.desc_base_off = hconv_desc_mode();
     p.out = out;
     p.bias = bias;
+    {
+        const char* e = std::getenv("PT_B200_HCONV_EXP");
+        p.exp = e ? std::atoi(e) : 0;
+    }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
                         (2 * sa + 2 * sb + 4) * 8 + 16;
     const int units = p.tiles * p.n_tiles;
     const int ncl = std::min(units, sm_count() / 2);
     static bool attr = false;
     if (!attr) {
-        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemLimitH));
+        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimitH));
         attr = true;
     }
@@ -334,7 +339,8 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ProfScope prof("umma_conv", st, alg_flops, 0.0);
-    PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel, p));
+    if (cps == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<2>, p));
+    else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<1>, p));
     after_launch("umma_hconv");
 }
 

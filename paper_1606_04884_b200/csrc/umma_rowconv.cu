@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
     uint64_t* wbar = tempty + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
 
-    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
+        if (leader) {  // whole warp, converged; one elected lane issues
             const uint32_t idesc = idesc_tf32(256, p.Np, 0, 0);
             const uint32_t lbo_b = (uint32_t)(p.Np / 2) * 16u;  // next tap s: next [Np/2][4] block
             const uint32_t wbase = smem_u32(sW);
@@ -127,22 +127,23 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
                 for (int r = 0; r < p.kH; ++r) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a = smem_u32(sA + (size_t)stage * p.stage_a);
-                    const uint32_t b = wbase + (uint32_t)(r * p.S2) * lbo_b;
-                    for (int k = 0; k < p.S2 / 2; ++k) {
-                        // A: Hankel view of the row segment — rows (pixels) 16 B apart inside a
-                        // core matrix, next 8 pixels at SBO=128, next tap s at LBO=16.
-                        const uint64_t ad = smem_desc(a + 32u * k, 16, 128, kSwizzleNone);
-                        const uint64_t bd = smem_desc(b + 2u * k * lbo_b, lbo_b, 128, kSwizzleNone);
-                        mma_tf32_cg2(d, ad, bd, idesc, (r | k) != 0);
-                    }
-                    mma_commit_cg2(&empty[stage]);
+                    // A: Hankel view of the row segment — rows (pixels) 16 B apart inside a
+                    // core matrix, next 8 pixels at SBO=128, next tap s at LBO=16.
+                    const uint32_t alo = desc_lo(smem_u32(sA + (size_t)stage * p.stage_a), 16);
+                    uint32_t blo = desc_lo(wbase + (uint32_t)(r * p.S2) * lbo_b, lbo_b);
+                    constexpr uint32_t kHi = desc_hi(128, kSwizzleNone);
+                    const uint32_t bstep = (2u * lbo_b) >> 4;
+                    const int npair = p.S2 / 2;
+                    for (int k = 0; k < npair; ++k, blo += bstep)
+                        mma_tf32_cg2_warp(d, desc_make(alo + 2u * k, kHi), desc_make(blo, kHi), idesc,
+                                     (r | k) != 0);
+                    mma_commit_cg2_warp(&empty[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                mma_commit_cg2(&tfull[acc]);
+                mma_commit_cg2_warp(&tfull[acc]);
             }
         }
     } else {

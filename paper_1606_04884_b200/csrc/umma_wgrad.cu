@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    const uint32_t warp = warp_id(), lane = lane_id();
+    const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
+        if (leader) {  // whole warp, converged; one elected lane issues
             const uint32_t idesc = idesc_tf32(256, p.bn, 1, 1);
             int stage = 0;
             uint32_t phase = 0;
@@ -167,23 +167,23 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a = smem_u32(sA + (size_t)stage * kStageA);
-                    const uint32_t b = smem_u32(sB + (size_t)stage * p.stage_b);
+                    // MN-major: 32-element atoms along M/N at LBO = one box (8 KB),
+                    // 4-row swizzle groups along K at SBO = 512 B; K=8 rows = +1 KB.
+                    const uint32_t alo = desc_lo(smem_u32(sA + (size_t)stage * kStageA), kBox);
+                    const uint32_t blo = desc_lo(smem_u32(sB + (size_t)stage * p.stage_b), kBox);
+                    constexpr uint32_t kHi = desc_hi(512, kSwizzle128B_Base32B);
+                    const uint32_t acc0 = kb != 0;
 #pragma unroll
-                    for (int k = 0; k < kPix / 8; ++k) {
-                        // MN-major: 32-element atoms along M/N at LBO = one box (8 KB),
-                        // 4-row swizzle groups along K at SBO = 512 B; K=8 rows = +1 KB.
-                        const uint64_t ad = smem_desc(a + k * 1024, kBox, 512, kSwizzle128B_Base32B);
-                        const uint64_t bd = smem_desc(b + k * 1024, kBox, 512, kSwizzle128B_Base32B);
-                        mma_tf32_cg2(d, ad, bd, idesc, (kb | k) != 0);
-                    }
-                    mma_commit_cg2(&empty[stage]);
+                    for (int k = 0; k < kPix / 8; ++k)
+                        mma_tf32_cg2_warp(d, desc_make(alo + k * 64, kHi), desc_make(blo + k * 64, kHi), idesc,
+                                     k ? 1u : acc0);
+                    mma_commit_cg2_warp(&empty[stage]);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                mma_commit_cg2(&tfull[acc]);
+                mma_commit_cg2_warp(&tfull[acc]);
             }
         }
     } else {

@@ -1,0 +1,7 @@
+#!/bin/bash
+OUT=gpurun_out/hc3; mkdir -p $OUT
+for m in 0 2 3; do
+  for pass in fwd dgrad; do
+    PT_B200_HCONV=1 PT_B200_HCONV_DESC=$m timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:umma_hconv --csv python tests/prof_one.py --layer L2 --pass $pass --iters 3 2>&1 | grep -E "gpu__time" | tail -1 | sed "s/^/mode $m $pass: /"
+  done
+done
