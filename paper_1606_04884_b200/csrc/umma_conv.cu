@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
         tma_prefetch(&p.tmap_a);
         tma_prefetch(&p.tmap_b);
         for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], CG);
+            mbar_init(&full[i], 1);  // armed by the leader only; the peer's bytes land on it
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -150,7 +150,6 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
                     uint8_t* b = sB + (size_t)stage * p.stage_b;
                     if constexpr (CG == 2) {
                         if (leader) mbar_arrive_expect_tx(&full[stage], tx);
-                        else mbar_arrive_cluster(&full[stage], 0);
 #pragma unroll
                         for (int t = 0; t < 2; ++t) {
                             // past the last k-slot: any valid tap (the weights there are 0)

@@ -85,11 +85,11 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         tma_prefetch(&p.tmap_a);
         tma_prefetch(&p.tmap_b);
         for (int i = 0; i < p.sa; ++i) {
-            mbar_init(&afull[i], 2);
+            mbar_init(&afull[i], 1);  // armed by the leader only
             mbar_init(&aempty[i], 1);
         }
         for (int i = 0; i < p.sb; ++i) {
-            mbar_init(&bfull[i], 2);
+            mbar_init(&bfull[i], 1);
             mbar_init(&bempty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -122,7 +122,6 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                     for (int cc = 0; cc < p.chunks; cc += CPS) {
                         mbar_wait(&aempty[as], aph ^ 1);
                         if (leader) mbar_arrive_expect_tx(&afull[as], atx);
-                        else mbar_arrive_cluster(&afull[as], 0);
 #pragma unroll
                         for (int c = 0; c < CPS; ++c)
                             tma_load_2d_cg2(sA + (size_t)as * p.stage_a + c * p.box_a, &p.tmap_a, &afull[as],
@@ -134,7 +133,6 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                         for (int s = 0; s < p.kW; ++s) {
                             mbar_wait(&bempty[bs], bph ^ 1);
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
-                            else mbar_arrive_cluster(&bfull[bs], 0);
 #pragma unroll
                             for (int c = 0; c < CPS; ++c)
                                 tma_load_2d_cg2(sB + (size_t)bs * p.stage_b + c * p.box_b, &p.tmap_b, &bfull[bs],

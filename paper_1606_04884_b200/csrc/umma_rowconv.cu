@@ -17,6 +17,7 @@
 // input row segment (one TMA box of 512-byte rows); K walks (r, s-pair): one stage
 // per filter row r, ceil(kW/2) MMAs (K = 8 = two taps x 4 channels) per stage.
 #include <cuda.h>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "tmap.cuh"
@@ -29,9 +30,19 @@ namespace {
 using namespace umma;
 
 constexpr int kThreadsR = 192;
+// A-ring depth: each stage is one ~2.5 KB row-segment TMA load feeding only kW/2 MMAs,
+// so many loads must be in flight to cover L2 latency
+static int kMaxStagesR = [] {
+    const char* e = std::getenv("PT_B200_ROWCONV_STAGES");
+    return e ? std::atoi(e) : 12;
+}();
 constexpr int kSmemLimit = 232448;
 
 struct RowConvParams {
+    int rps;              // padded input rows per pipeline stage
+    uint32_t stage_bytes; // bytes one CTA's stage TMA delivers
+    uint32_t row16;       // bytes between consecutive rows in a stage, >> 4
+    int exp;  // timing experiments (PT_B200_ROWCONV_EXP; wrong results if != 0)
     CUtensorMap tmap_x;  // xp viewed (128 floats, Wa*4/128 chunks, N*Hp rows), box {128, seg_chunks, 1}
     CUtensorMap tmap_w;  // packed weights viewed (128 floats, w_chunks, 2 halves), box {128, w_chunks, 1}
     int oH, oW, Hp, kH, S2;  // S2 = kW rounded up to even
@@ -65,7 +76,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
         tma_prefetch(&p.tmap_x);
         tma_prefetch(&p.tmap_w);
         for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 2);
+            mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -97,10 +108,11 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
                 const int row = t / p.segs, seg = t - row * p.segs;  // row = n*oH + i
                 const int n = row / p.oH, i = row - n * p.oH;
                 const int prow = n * p.Hp + i;  // padded input row of filter row r = 0
-                for (int r = 0; r < p.kH; ++r) {
+                // one stage = RPS consecutive padded input rows (a single 3-D TMA box); the
+                // peer's bytes complete on the leader's barrier, which only the leader arms
+                for (int r = 0; r < p.kH; r += p.rps) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2u * 512u * (uint32_t)p.seg_chunks);
-                    else mbar_arrive_cluster(&full[stage], 0);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2u * p.stage_bytes);
                     tma_load_3d_cg2(sA + (size_t)stage * p.stage_a, &p.tmap_x, &full[stage], 0,
                                     seg * 4, prow + r);
                     if (++stage == S) {
@@ -124,19 +136,25 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
                 mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * p.Np;
-                for (int r = 0; r < p.kH; ++r) {
-                    mbar_wait(&full[stage], phase);
+                const uint32_t bstep = (2u * lbo_b) >> 4;
+                const int npair = p.S2 / 2;
+                constexpr uint32_t kHi = desc_hi(128, kSwizzleNone);
+                for (int r0 = 0; r0 < p.kH; r0 += p.rps) {
+                    if ((p.exp & 2) == 0 || it == 0) mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    // A: Hankel view of the row segment — rows (pixels) 16 B apart inside a
-                    // core matrix, next 8 pixels at SBO=128, next tap s at LBO=16.
-                    const uint32_t alo = desc_lo(smem_u32(sA + (size_t)stage * p.stage_a), 16);
-                    uint32_t blo = desc_lo(wbase + (uint32_t)(r * p.S2) * lbo_b, lbo_b);
-                    constexpr uint32_t kHi = desc_hi(128, kSwizzleNone);
-                    const uint32_t bstep = (2u * lbo_b) >> 4;
-                    const int npair = p.S2 / 2;
-                    for (int k = 0; k < npair; ++k, blo += bstep)
-                        mma_tf32_cg2_warp(d, desc_make(alo + 2u * k, kHi), desc_make(blo, kHi), idesc,
-                                     (r | k) != 0);
+                    const uint32_t abase = desc_lo(smem_u32(sA + (size_t)stage * p.stage_a), 16);
+                    const int rn = p.kH - r0 < p.rps ? p.kH - r0 : p.rps;
+                    for (int rr = 0; rr < rn; ++rr) {
+                        const int r = r0 + rr;
+                        // A: Hankel view of the row segment — rows (pixels) 16 B apart inside a
+                        // core matrix, next 8 pixels at SBO=128, next tap s at LBO=16.
+                        const uint32_t alo = abase + (uint32_t)rr * p.row16;
+                        uint32_t blo = desc_lo(wbase + (uint32_t)(r * p.S2) * lbo_b, lbo_b);
+                        for (int k = 0; k < npair; ++k, blo += bstep)
+                            if ((p.exp & 4) == 0)
+                                mma_tf32_cg2_warp(d, desc_make(alo + 2u * k, kHi), desc_make(blo, kHi), idesc,
+                                                  (r | k) != 0);
+                    }
                     mma_commit_cg2_warp(&empty[stage]);
                     if (++stage == S) {
                         stage = 0;
@@ -161,7 +179,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
             const bool valid = t < p.tiles && j < p.oW;
             const int64_t base = (int64_t)n * p.n_rows * ohw + (int64_t)i * p.oW + j;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.Np;
-            store_tmem_columns_nchw(taddr, p.Np, p.out + (valid ? base : 0), ohw, p.bias, 0,
+            if ((p.exp & 1) == 0) store_tmem_columns_nchw(taddr, p.Np, p.out + (valid ? base : 0), ohw, p.bias, 0,
                                     p.n_rows, valid);
             tc_fence_before();
             __syncwarp();
@@ -291,14 +309,25 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     {
         const uint64_t dims[3] = {128, (uint64_t)rp.Wa * 4 / 128, (uint64_t)(g.N * rp.Hp)};
         const uint64_t strides[2] = {512, (uint64_t)rp.Wa * 16};
-        const uint32_t box[3] = {128, (uint32_t)rp.seg_chunks, 1};
+        // one stage = rps padded rows of seg_chunks x 512 B
+        p.rps = (int)g.kH;
+        while (p.rps > 1 && (size_t)p.rps * rp.seg_chunks * 512 * 3 >
+                                (size_t)(kSmemLimit - 2048 - (int)align_up(rp.w_half * 4, 1024)))
+            p.rps = (p.rps + 1) / 2;
+        const uint32_t box[3] = {128, (uint32_t)rp.seg_chunks, (uint32_t)p.rps};
         tmap_tiled(&p.tmap_x, xp, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+        p.stage_bytes = (uint32_t)(p.rps * rp.seg_chunks * 512);
+        p.row16 = (uint32_t)(rp.seg_chunks * 512) >> 4;
     }
     {
         const uint64_t dims[3] = {128, (uint64_t)rp.w_chunks, 2};
         const uint64_t strides[2] = {512, (uint64_t)rp.w_half * 4};
         const uint32_t box[3] = {128, (uint32_t)rp.w_chunks, 1};
         tmap_tiled(&p.tmap_w, bw, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
+    {
+        const char* e = std::getenv("PT_B200_ROWCONV_EXP");
+        p.exp = e ? std::atoi(e) : 0;
     }
     p.oH = (int)g.oH;
     p.oW = (int)g.oW;
@@ -310,11 +339,11 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     p.n_rows = (int)g.K;
     p.Np = rp.Np;
     p.tiles = (int)(g.N * g.oH * rp.segs);
-    p.stage_a = (uint32_t)align_up((size_t)rp.seg_chunks * 512, 1024);
+    p.stage_a = (uint32_t)align_up((size_t)p.stage_bytes, 1024);
     p.w_bytes = (uint32_t)(rp.w_half * 4);
     const int avail = kSmemLimit - 1024 - 512 - (int)align_up(p.w_bytes, 1024);
     int s = avail / (int)p.stage_a;
-    p.stages = s > 12 ? 12 : s;
+    p.stages = s > kMaxStagesR ? kMaxStagesR : s;
     uint32_t cols = 32;
     while ((int)cols < 2 * rp.Np) cols <<= 1;
     p.tmem_cols = cols;

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
         tma_prefetch(&p.tmap_gy);
         tma_prefetch(&p.tmap_x);
         for (int i = 0; i < S; ++i) {
-            mbar_init(&full[i], 2);   // leader's expect_tx arrive + the peer's arrive
+            mbar_init(&full[i], 1);   // the leader's expect_tx arrive (peer bytes land on it)
             mbar_init(&empty[i], 1);  // one multicast commit
         }
         for (int i = 0; i < 2; ++i) {
@@ -126,7 +126,6 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
                     uint8_t* a = sA + (size_t)stage * kStageA;
                     uint8_t* b = sB + (size_t)stage * p.stage_b;
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kStageA + p.stage_b));
-                    else mbar_arrive_cluster(&full[stage], 0);
                     const int wc = j * p.sW - p.pW, hc = i * p.sH - p.pH;
 #pragma unroll
                     for (int t = 0; t < 4; ++t)

@@ -1,3 +1,3 @@
 #!/bin/bash
 B=tests/mma_bench
-for cg in 2 1; do for n in 64 128 256; do for sh in 0 3 4; do timeout 20 $B $n $cg 1000000 $sh; done; done; done
+for n in 96 128; do for sh in 4 5 6; do timeout 20 $B $n 2 1000000 $sh 19998; done; done

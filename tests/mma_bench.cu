@@ -64,7 +64,25 @@ __global__ void __launch_bounds__(128, 1) bench(P p, unsigned long long* cyc) {
                 else mma_commit(&dummy);
             }
         }
-        for (int i = 0; i < (p.shift == 4 ? 0 : p.iters); ++i) {
+        if (p.shift == 5 || p.shift == 6) {
+            // rowconv pattern: A no-swizzle Hankel (LBO 16, SBO 128, K=8 per MMA = two 16-B
+            // taps, start +32 B per MMA); B no-swizzle [N/2][4] blocks (LBO = N/2*16).
+            // shift 6: the same with non-overlapping A (LBO 2048 = standard core-matrix layout)
+            const uint32_t lbo_b = (uint32_t)(p.n / CG) * 16u;
+            constexpr uint32_t kHi = desc_hi(128, kSwizzleNone);
+            const uint32_t alo = desc_lo(a, p.shift == 5 ? 16 : 2048), blo = desc_lo(b, lbo_b);
+            for (int i = 0; i < p.iters; i += 6) {
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    const uint32_t ao = p.shift == 5 ? 2u * k : 256u * k;
+                    if (CG == 2) mma_tf32_cg2(tmem, desc_make(alo + ao, kHi), desc_make(blo + k * ((2 * lbo_b) >> 4), kHi), idesc, 1);
+                    else mma_tf32(tmem, desc_make(alo + ao, kHi), desc_make(blo + k * ((2 * lbo_b) >> 4), kHi), idesc, 1);
+                }
+                if (CG == 2) mma_commit_cg2(&dummy);
+                else mma_commit(&dummy);
+            }
+        }
+        for (int i = 0; i < (p.shift >= 4 ? 0 : p.iters); ++i) {
             // shift 1: Hankel-style row shifts; shift 2: walk 4 distinct 16 KB A stages
             const uint32_t sh = p.shift == 1 ? (uint32_t)(i % 9) * 128u
                                 : p.shift == 2 ? (uint32_t)((i >> 2) & 3) * 16384u : 0u;
