@@ -86,12 +86,16 @@ struct UmmaPlan {
     // The activation is then stored zero-bordered: [N][aHp][aWp][cin_p], border (aph, apw).
     bool hankel = false;
     int64_t aH = 0, aW = 0, aph = 0, apw = 0, aHp = 0, aWp = 0;
+    // <= 64 output rows: pair taps (s, s+1) in one N = 2*bn MMA (umma_hconv.cu); the packed
+    // weights then carry one extra all-zero tap (index `taps`) for odd kW
+    bool tap_pair = false;
+    int64_t kdim = 0;  // packed weight row length (floats)
 };
 struct HConvTiling {
     int64_t P_img = 0;  // positions per image
     int64_t tiles = 0;  // 256-position pair tiles
 };
-HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH);
+HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH, int64_t span = 256);
 // act: zero-bordered NHWC [N][Hp][Wp][cin_p]; stride-1 kH x kW conv -> oH x oW NCHW.
 void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, int64_t Hp,
                int64_t Wp, int kH, int kW, int64_t oH, int64_t oW, float* out, const float* bias,

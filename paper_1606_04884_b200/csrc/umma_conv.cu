@@ -401,6 +401,7 @@ void plan_rows(UmmaPlan& pl) {
     pl.cg = (pl.cb == 32 && sm_count() >= 2) ? 2 : 1;
     // weights padded so the last (possibly half-empty) 2-slot stage reads zeros
     const int64_t kdim_p = ceil_div(pl.taps * pl.cin_p, 64) * 64;
+    pl.kdim = kdim_p;
     pl.wt_elems = pl.cb == 32 ? pl.n_pad * kdim_p : pl.slots_p * pl.n_pad * 4;
 }
 
@@ -410,6 +411,14 @@ int hconv_env() {
     static const int v = [] {
         const char* e = std::getenv("PT_B200_HCONV");
         return e ? std::atoi(e) : -1;
+    }();
+    return v;
+}
+
+int hconv_pair_env() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_HCONV_PAIR");
+        return e ? std::atoi(e) : 1;
     }();
     return v;
 }
@@ -428,6 +437,15 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
     // L2->SM traffic
     if (hconv_env() != 1 && eff < 0.84) return;
     pl.hankel = true;
+    if (pl.n_rows <= 64 && hconv_pair_env() != 0) {
+        // tap pairing: one N tile of all the rows, one extra zero tap in the packing
+        pl.tap_pair = true;
+        pl.bn = (int)((pl.n_rows + 7) / 8 * 8);
+        pl.n_tiles = 1;
+        pl.n_pad = pl.bn;
+        pl.kdim = ceil_div((pl.taps + 1) * pl.cin_p, 64) * 64;
+        pl.wt_elems = pl.n_pad * pl.kdim;
+    }
     pl.aH = aH;
     pl.aW = aW;
     pl.aph = ph;

@@ -51,7 +51,9 @@ struct HConvParams {
     int oH, oW;          // valid output extent
     int64_t P_img;       // positions per image in the tiling
     int64_t img_px;      // Hp*Wp
-    int tiles;           // 256-position pair tiles
+    int tiles;           // pair tiles of `span` positions
+    int span;            // positions per pair tile: 256, or 254 with tap pairing
+    int zero_tap;        // PAIR: packed-weight tap index holding zeros (odd kW)
     int n_rows, bn, n_tiles;
     int sa, sb;          // ring depths
     uint32_t stage_a, stage_b;  // bytes per stage (CPS boxes)
@@ -62,7 +64,14 @@ struct HConvParams {
     const float* bias;
 };
 
-template <int CPS>  // 32-channel chunks per pipeline stage (1 or 2)
+// CPS: 32-channel chunks per pipeline stage (1 or 2).
+// PAIR (output-shift tap pairing, for <= 64 output channels where an N=64 MMA costs as
+// much as N=128): one MMA computes taps s and s+1 from the SAME pixel run (shift s) —
+// CTA 0 stages tap s's weights, CTA 1 tap s+1's, N = 2*bn. Column half 1 then holds tap
+// s+1's contribution to the position one to the LEFT, so the epilogue forms
+// out[q] = D0[q] + D1[q+1]; each CTA's last lane lacks its right neighbour and is
+// dropped (tiles advance 127 positions per CTA).
+template <int CPS, bool PAIR>
 __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_constant__ HConvParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ uint8_t smem_raw[];
@@ -77,6 +86,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     uint64_t* tfull = bempty + p.sb;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // PAIR: [4 chunks][3 warps][16]
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
@@ -105,6 +115,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     const uint32_t tmem_base = *tmem_holder;
     const int num_units = p.tiles * p.n_tiles;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    constexpr int kCtaSpan = PAIR ? 127 : 128;  // positions a CTA advances per tile
 
     if (warp == 0) {
         if (lane == 0) {
@@ -114,10 +125,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             const uint32_t atx = 2 * p.stage_a, btx = 2 * p.stage_b;
             for (int u = cid; u < num_units; u += ncl) {
                 const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
-                const int64_t g0 = (int64_t)t * 256 + (int64_t)rank * 128;
+                const int64_t g0 = (int64_t)t * p.span + (int64_t)rank * kCtaSpan;
                 const int64_t n = g0 / p.P_img;
                 const int64_t pix0 = n * p.img_px + (g0 - n * p.P_img);
-                const int brow = nt * p.bn + (int)rank * (p.bn / 2);
+                const int brow = PAIR ? 0 : nt * p.bn + (int)rank * (p.bn / 2);
                 for (int r = 0; r < p.kH; ++r) {
                     for (int cc = 0; cc < p.chunks; cc += CPS) {
                         mbar_wait(&aempty[as], aph ^ 1);
@@ -130,13 +141,16 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             as = 0;
                             aph ^= 1;
                         }
-                        for (int s = 0; s < p.kW; ++s) {
+                        for (int s = 0; s < p.kW; s += PAIR ? 2 : 1) {
                             mbar_wait(&bempty[bs], bph ^ 1);
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
+                            // PAIR: this CTA's tap is s + rank (past the row: the zero tap)
+                            const int tap = PAIR ? (s + (int)rank < p.kW ? r * p.kW + s + (int)rank : p.zero_tap)
+                                                 : r * p.kW + s;
 #pragma unroll
                             for (int c = 0; c < CPS; ++c)
                                 tma_load_2d_cg2(sB + (size_t)bs * p.stage_b + c * p.box_b, &p.tmap_b, &bfull[bs],
-                                                (r * p.kW + s) * p.cin_p + (cc + c) * 32, brow);
+                                                tap * p.cin_p + (cc + c) * 32, brow);
                             if (++bs == p.sb) {
                                 bs = 0;
                                 bph ^= 1;
@@ -149,7 +163,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     } else if (warp == 1) {
         if (leader) {
             // ===== MMA issuer (whole warp, converged; one elected lane issues) =====
-            const uint32_t idesc = idesc_tf32(256, p.bn, 0, 0);
+            const uint32_t idesc = idesc_tf32(256, PAIR ? 2 * p.bn : p.bn, 0, 0);
             constexpr uint32_t kHi = desc_hi(1024, kSwizzle128B);
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
@@ -158,7 +172,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 const uint32_t acc = it & 1;
                 mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem_base + acc * p.bn;
+                const uint32_t d = tmem_base + acc * (PAIR ? 2 * p.bn : p.bn);
                 uint32_t accum = 0;
                 const uint32_t box_a16 = p.box_a >> 4, box_b16 = p.box_b >> 4;
                 for (int r = 0; r < p.kH; ++r) {
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                         mbar_wait(&afull[as], aph);
                         tc_fence_after();
                         const uint32_t alo = desc_lo(smem_u32(sA + (size_t)as * p.stage_a), 16);
-                        for (int s = 0; s < p.kW; ++s) {
+                        for (int s = 0; s < p.kW; s += PAIR ? 2 : 1) {
                             mbar_wait(&bfull[bs], bph);
                             tc_fence_after();
                             // tap s: the same pixel run, s rows (s*128 B) further in
@@ -206,16 +220,49 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             tc_fence_after();
             const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
-            const int64_t gpos = (int64_t)t * 256 + (int64_t)rank * 128 + q * 32 + lane;
+            const int64_t gpos = (int64_t)t * p.span + (int64_t)rank * kCtaSpan + q * 32 + lane;
             const int64_t n = gpos / p.P_img;
             const int64_t qq = gpos - n * p.P_img;
             const int64_t i = qq / p.Wp, j = qq - i * p.Wp;
-            const bool valid = n < p.N && i < p.oH && j < p.oW;
+            const bool valid = n < p.N && i < p.oH && j < p.oW && (!PAIR || q * 32 + lane < 127);
             const int ch0 = nt * p.bn;
             const int64_t base = (n * p.n_rows + ch0) * ohw + i * p.oW + j;
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
-            store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base : 0), ohw, p.bias, ch0,
-                                    p.n_rows, valid);
+            if constexpr (!PAIR) {
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
+                store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base : 0), ohw, p.bias, ch0,
+                                        p.n_rows, valid);
+            } else {
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * 2 * p.bn;
+                float* o = p.out + (valid ? base : 0);
+                for (int c0 = 0; c0 < p.bn; c0 += 16) {
+                    uint32_t v0[16], v1[16];
+                    tmem_ld_32x32b_x16(taddr + c0, v0);
+                    tmem_ld_32x32b_x16(taddr + p.bn + c0, v1);
+                    tmem_ld_wait();
+                    // right neighbour's tap-(s+1) half: next lane, or the next warp's lane 0
+                    float nb[16];
+                    float* slot = xch + (c0 >> 4) * 48;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        nb[e] = __shfl_down_sync(0xffffffffu, __uint_as_float(v1[e]), 1);
+                        if (lane == 0 && q > 0) slot[(q - 1) * 16 + e] = __uint_as_float(v1[e]);
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (lane == 31 && q < 3) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) nb[e] = slot[q * 16 + e];
+                    }
+                    if (valid) {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const int ch = ch0 + c0 + e;
+                            if (ch < p.n_rows)
+                                __stcs(o + (int64_t)(c0 + e) * ohw,
+                                       __uint_as_float(v0[e]) + nb[e] + (p.bias ? __ldg(p.bias + ch) : 0.f));
+                        }
+                    }
+                }
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -235,11 +282,11 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
 }  // namespace
 
 // Tiling of the position space: per image vs flat, whichever computes fewer positions.
-HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH) {
+HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH, int64_t span) {
     HConvTiling t;
-    const int64_t per_img = ceil_div(oH * Wp, 256) * 256;
-    const int64_t tiles_img = N * per_img / 256;
-    const int64_t tiles_flat = ceil_div((N - 1) * Hp * Wp + oH * Wp, 256);
+    const int64_t per_img = ceil_div(oH * Wp, span) * span;
+    const int64_t tiles_img = N * per_img / span;
+    const int64_t tiles_flat = ceil_div((N - 1) * Hp * Wp + oH * Wp, span);
     if (tiles_flat < tiles_img) {
         t.P_img = Hp * Wp;
         t.tiles = tiles_flat;
@@ -266,14 +313,18 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         const uint32_t box[2] = {32, (uint32_t)rbox};
         tmap_tiled(&p.tmap_a, act, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
+    const bool pair = pl.tap_pair;
     {
-        const uint64_t kdim = (uint64_t)(ceil_div(pl.taps * pl.cin_p, 64) * 64);
+        const uint64_t kdim = (uint64_t)pl.kdim;
         const uint64_t dims[2] = {kdim, (uint64_t)pl.n_pad};
         const uint64_t strides[1] = {kdim * 4};
-        const uint32_t box[2] = {32, (uint32_t)(pl.bn / 2)};
+        const uint32_t box[2] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2)};
         tmap_tiled(&p.tmap_b, wt, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
-    const HConvTiling tl = hconv_tiling(N, Hp, Wp, oH);
+    p.span = pair ? 254 : 256;
+    p.zero_tap = (int)pl.taps;
+    PTB_REQUIRE(!pair || ((int64_t)pl.taps + 1) * pl.cin_p <= pl.kdim, "hconv: no zero tap packed");
+    const HConvTiling tl = hconv_tiling(N, Hp, Wp, oH, p.span);
     PTB_REQUIRE(tl.tiles * (int64_t)pl.n_tiles < (1ll << 31), "hconv: too many tiles");
     p.N = (int)N;
     p.Hp = (int)Hp;
@@ -292,12 +343,12 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.n_tiles = pl.n_tiles;
     const int cps = p.chunks % 2 == 0 ? 2 : 1;
     p.box_a = (uint32_t)rbox * 128u;
-    p.box_b = (uint32_t)align_up((size_t)(pl.bn / 2), 8) * 128u;
+    p.box_b = (uint32_t)align_up((size_t)(pair ? pl.bn : pl.bn / 2), 8) * 128u;
     p.stage_a = cps * p.box_a;
     p.stage_b = cps * p.box_b;
     // B ring: enough stages to cover two filter rows' worth of taps; A ring: the rest
     const int budget = kSmemLimitH - 1024 - 512;
-    int sb = std::min(16, std::max(4, 2 * kW));
+    int sb = std::min(16, std::max(4, pair ? kW + 1 : 2 * kW));
     while (sb > 3 && budget - sb * (int)p.stage_b < 2 * (int)p.stage_a) --sb;
     int sa = (budget - sb * (int)p.stage_b) / (int)p.stage_a;
     sa = std::min(sa, 8);
@@ -305,7 +356,8 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.sa = sa;
     p.sb = sb;
     p.tmem_cols = 32;
-    while ((int)p.tmem_cols < 2 * pl.bn) p.tmem_cols <<= 1;
+    while ((int)p.tmem_cols < (pair ? 4 : 2) * pl.bn) p.tmem_cols <<= 1;
+    PTB_REQUIRE(p.tmem_cols <= 512, "hconv: accumulators exceed TMEM");
     p.out = out;
     p.bias = bias;
     {
@@ -313,15 +365,19 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         p.exp = e ? std::atoi(e) : 0;
     }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
-                        (2 * sa + 2 * sb + 4) * 8 + 16;
+                        (2 * sa + 2 * sb + 4) * 8 + 16 + 4 * 48 * 4;
     const int units = p.tiles * p.n_tiles;
     const int ncl = std::min(units, sm_count() / 2);
     static bool attr = false;
     if (!attr) {
-        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSmemLimitH));
-        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSmemLimitH));
+        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<1, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
+        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<2, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
+        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<1, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
+        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<2, true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -337,8 +393,14 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ProfScope prof("umma_conv", st, alg_flops, 0.0);
-    if (cps == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<2>, p));
-    else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<1>, p));
+    if (pair) {
+        PTB_REQUIRE(p.bn <= 64, "hconv: tap pairing needs <= 64 output channels");
+        if (cps == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<2, true>, p));
+        else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<1, true>, p));
+    } else {
+        if (cps == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<2, false>, p));
+        else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<1, false>, p));
+    }
     after_launch("umma_hconv");
 }
 
