@@ -28,41 +28,46 @@ template <bool PAD, bool TWO>
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, NhwcDst d1,
                                     int64_t C, int64_t HW, int64_t Cp, int round_tf32,
                                     float* __restrict__ part) {
-    __shared__ float tile[32][33];
+    // the whole 32-channel x 128-pixel strip is loaded before the first barrier: 16
+    // independent loads per thread keep enough bytes in flight to run at HBM rate
+    // (one 32x32 tile per barrier capped this pass at ~3.3 TB/s)
+    __shared__ float tile[32][kStripPx + 1];
     const int64_t n = blockIdx.z;
     const int64_t c0 = (int64_t)blockIdx.y * 32;
     const float* s = src + n * C * HW;
     float* o0 = d0.p + n * d0.img * Cp;
     float* o1 = TWO ? d1.p + n * d1.img * Cp : nullptr;
+    const int64_t p0 = (int64_t)blockIdx.x * kStripPx;
     float rowsum[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int t = 0; t < kStripPx / 32; ++t) {
-        const int64_t p0 = (int64_t)blockIdx.x * kStripPx + t * 32;
-        if (p0 >= HW) break;
 #pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-            const int64_t c = c0 + threadIdx.y + i, p = p0 + threadIdx.x;
-            float v = 0.f;
-            if (c < C && p < HW) v = __ldg(s + c * HW + p);
-            tile[threadIdx.y + i][threadIdx.x] = v;
-            rowsum[i / 8] += v;
+    for (int i = 0; i < 4; ++i) {
+        const int64_t c = c0 + threadIdx.y + 8 * i;
+        const float* sc = s + c * HW + p0;
+#pragma unroll
+        for (int t = 0; t < kStripPx / 32; ++t) {
+            const int64_t p = p0 + threadIdx.x + 32 * t;
+            const float v = (c < C && p < HW) ? __ldg(sc + threadIdx.x + 32 * t) : 0.f;
+            tile[threadIdx.y + 8 * i][threadIdx.x + 32 * t] = v;
+            rowsum[i] += v;
         }
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-            const int64_t p = p0 + threadIdx.y + i, c = c0 + threadIdx.x;
-            if (p < HW && c < Cp) {
-                float v = tile[threadIdx.x][threadIdx.y + i];
-                if (round_tf32) v = to_tf32(v);
-                if constexpr (PAD) {
-                    o0[d0.pixel(p) * Cp + c] = v;
-                    if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
-                } else {
-                    o0[p * Cp + c] = v;
-                    if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
-                }
+    }
+    __syncthreads();
+    const int64_t c = c0 + threadIdx.x;
+#pragma unroll 4
+    for (int k = 0; k < kStripPx / 8; ++k) {
+        const int pl = threadIdx.y + 8 * k;
+        const int64_t p = p0 + pl;
+        if (p < HW && c < Cp) {
+            float v = tile[threadIdx.x][pl];
+            if (round_tf32) v = to_tf32(v);
+            if constexpr (PAD) {
+                o0[d0.pixel(p) * Cp + c] = v;
+                if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
+            } else {
+                o0[p * Cp + c] = v;
+                if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
             }
         }
-        __syncthreads();
     }
     if (part) {
         // reduce each channel row's 32 lanes (warp = fixed threadIdx.y -> fixed channels)

@@ -95,12 +95,21 @@ __global__ void fold_rows_kernel(const float* __restrict__ gxe, float* __restric
         float* dst = gx + row * W;
         for (int w = threadIdx.x; w < W; w += blockDim.x) {
             float acc = 0.f;
-            for (int s = 0; s < kW; ++s) {
-                const int wn = w + pW - s;
-                if (wn < 0) break;
-                const int j = wn / sW;
-                if (j * sW != wn || j >= oW) continue;
-                acc += __ldg(src + (int64_t)s * C * plane + j);
+            if (sW == 1) {
+                // stride 1: tap s reads column w + pW - s; independent predicated loads
+#pragma unroll 4
+                for (int s = 0; s < kW; ++s) {
+                    const int j = w + pW - s;
+                    if (j >= 0 && j < oW) acc += __ldg(src + (int64_t)s * C * plane + j);
+                }
+            } else {
+                for (int s = 0; s < kW; ++s) {
+                    const int wn = w + pW - s;
+                    if (wn < 0) break;
+                    const int j = wn / sW;
+                    if (j * sW != wn || j >= oW) continue;
+                    acc += __ldg(src + (int64_t)s * C * plane + j);
+                }
             }
             dst[w] = acc;
         }
@@ -161,7 +170,7 @@ void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws
     const int64_t total = g.N * g.C * g.HW;
     ProfScope prof("layout", st, 0.0, 4.0 * (e.N * e.C * e.H * e.W + total));
     const int64_t rows = g.N * g.C * g.H;
-    fold_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 32 * (int64_t)sm_count()), 128, 0, st>>>(
+    fold_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 128 * (int64_t)sm_count()), 128, 0, st>>>(
         gxe, gx, g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.oW, (int)g.kW, (int)g.pW, (int)g.sW);
     after_launch("fold_rows");
 }
@@ -194,7 +203,7 @@ void rowwgrad(const Geo& g, const float* x, const float* gyh, float* gw, float s
         const int64_t rows = g.N * g.H;
         const size_t smem = sizeof(float) * (size_t)(g.C * ((g.oW - 1) * g.sW + g.kW));
         PTB_REQUIRE(smem <= 48 * 1024, "expand_rows: input row too wide");
-        expand_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 16 * (int64_t)sm_count()), 256, smem, st>>>(
+        expand_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 64 * (int64_t)sm_count()), 256, smem, st>>>(
             x, reinterpret_cast<float4*>(xe), rows, (int)g.C, (int)g.H, (int)g.W, (int)g.oW, (int)g.kW,
             (int)g.pW, (int)g.sW, (int)Ce);
         after_launch("expand_rows");
