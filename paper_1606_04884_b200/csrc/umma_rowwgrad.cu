@@ -42,6 +42,24 @@ __global__ void expand_rows_kernel(const float* __restrict__ x, float4* __restri
         __syncthreads();
         float4* dst = xe + row * (int64_t)oW * (Ce / 4);
         const int q4 = Ce / 4;
+        if (blockDim.x % q4 == 0) {
+            // each thread always writes the same 4 expanded channels: decode them once
+            const int e0 = (threadIdx.x % q4) * 4;
+            int off[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = e0 + q, s = e / C, c = e - s * C;
+                off[q] = s < kW ? c * Wpad + s : -1;
+            }
+            const int jstep = blockDim.x / q4;
+            for (int j = threadIdx.x / q4; j < oW; j += jstep) {
+                float v[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = off[q] >= 0 ? srow[off[q] + j * sW] : 0.f;
+                dst[(int64_t)j * q4 + (threadIdx.x % q4)] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+            continue;
+        }
         for (int t = threadIdx.x; t < oW * q4; t += blockDim.x) {
             const int j = t / q4, e0 = (t - j * q4) * 4;
             float v[4];
