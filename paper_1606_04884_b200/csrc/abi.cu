@@ -136,17 +136,18 @@ size_t bwd_ws(const Geo& g, int math) {
     return std::max(bwd_data_ws(g, math), bwd_filter_ws(g, math));
 }
 
-// accGradParameters body; ws laid out as bwd_filter_ws describes.
+// accGradParameters body; ws laid out as bwd_filter_ws describes. gw takes (scale,
+// accumulate), gb takes (bscale, bacc) — equal except under the s2d wrapper, whose remap
+// applies the caller's scale to gw.
 void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, float* gb, float scale,
-                     int accumulate, int math, char* ws, cudaStream_t st) {
+                     int accumulate, int math, char* ws, cudaStream_t st, float bscale, int bacc) {
     PassScope pass("wgrad");
     if (wgrad_tc(g, math)) {
         float* gyh = reinterpret_cast<float*>(ws);
         float* part = reinterpret_cast<float*>(ws + gyh_bytes(g));
         {
             ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
-            nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate,
-                              part, st);
+            nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, bscale, bacc, part, st);
         }
         wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, ws + gyh_bytes(g) + bias_part_bytes(g),
                      st);
@@ -155,9 +156,55 @@ void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, f
     simt_conv_bwd_filter(g, x, gy, gw, scale, accumulate, reinterpret_cast<float*>(ws), st);
     if (gb) {
         float* bws = reinterpret_cast<float*>(ws + align_up(simt_wgrad_workspace(g), 256));
-        bias_grad(gy, gb, g.N, g.K, g.oHW, scale, accumulate, bws,
+        bias_grad(gy, gb, g.N, g.K, g.oHW, bscale, bacc, bws,
                   align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256), st);
     }
+}
+
+void fwd_core(const Geo& g, const float* x, const float* w, const float* b, float* y, int math,
+              void* ws, cudaStream_t st) {
+    if (fwd_rowconv(g, math)) {
+        rowconv_fwd(g, x, w, b, y, ws, st);
+        return;
+    }
+    if (math == PT_MATH_TF32) {
+        const UmmaPlan pl = umma_plan(g, false);
+        if (pl.ok) {
+            umma_conv_fwd(g, pl, x, w, b, y, ws, st);
+            return;
+        }
+    }
+    simt_conv_fwd(g, x, w, b, y, st);
+}
+
+// ---- strided small-C layers: space-to-depth into a stride-1 conv (s2d.cu) ----
+bool s2d_on(const Geo& g, int math) {
+    static const bool off = std::getenv("PT_B200_NO_S2D") != nullptr;  // A/B switch
+    return math == PT_MATH_TF32 && !off && s2d_applies(g);
+}
+size_t s2d_x_bytes(const Geo& g) {
+    const Geo e = s2d_geo(g);
+    return align_up((size_t)(e.N * e.C * e.HW) * 4, 256);
+}
+size_t s2d_w_bytes(const Geo& g) {
+    const Geo e = s2d_geo(g);
+    return align_up((size_t)(e.K * e.CRS) * 4, 256);
+}
+size_t fwd_ws_top(const Geo& g, int math) {
+    if (s2d_on(g, math)) return s2d_x_bytes(g) + s2d_w_bytes(g) + fwd_ws(s2d_geo(g), math);
+    return fwd_ws(g, math);
+}
+size_t bwd_data_ws_top(const Geo& g, int math) {
+    if (s2d_on(g, math)) return s2d_w_bytes(g) + s2d_x_bytes(g) + bwd_data_ws(s2d_geo(g), math);
+    return bwd_data_ws(g, math);
+}
+size_t bwd_filter_ws_top(const Geo& g, int math) {
+    if (s2d_on(g, math)) return s2d_x_bytes(g) + s2d_w_bytes(g) + bwd_filter_ws(s2d_geo(g), math);
+    return bwd_filter_ws(g, math);
+}
+size_t bwd_ws_top(const Geo& g, int math) {
+    if (s2d_on(g, math)) return 2 * s2d_x_bytes(g) + 2 * s2d_w_bytes(g) + bwd_ws(s2d_geo(g), math);
+    return bwd_ws(g, math);
 }
 
 void require_ws(size_t have, size_t need, const void* ws) {
@@ -166,6 +213,57 @@ void require_ws(size_t have, size_t need, const void* ws) {
                     std::to_string(need) + " bytes)");
     PTB_REQUIRE((reinterpret_cast<uintptr_t>(ws) & 255) == 0, "conv: workspace must be 256-byte aligned");
 }
+
+// Combined backward body (pt_b200_conv_bwd). inner_gw_plain: write gw with unit scale and
+// overwrite (the s2d wrapper applies the caller's scale / accumulate in its remap) while
+// gradBias still takes the caller's scale / accumulate.
+void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, float* gx, float* gw,
+              float* gb, float scale, int accumulate, int math, char* ws, cudaStream_t st,
+              bool inner_gw_plain) {
+        char* base = ws;
+        if (gx && gw && bwd_shared(g, math)) {
+            // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
+            float* gyh = reinterpret_cast<float*>(base);
+            float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
+            char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
+            char* wws = dws + align_up(bwd_data_ws(g, math), 256);
+            // a Hankel dgrad reads gy zero-bordered: the same pass writes that copy too
+            // (placed where that engine keeps its activation copy inside the dgrad workspace)
+            NhwcDst dpad{};
+            {
+                UmmaPlan dpl;
+                size_t off = 0;
+                if (dgrad_row(g, math)) {
+                    rowdgrad_ok(g, &dpl);
+                    off = rowdgrad_act_offset(g);
+                } else {
+                    dpl = umma_plan(g, true);
+                }
+                if (dpl.ok && dpl.hankel && dpl.cin_p == umma_wgrad_kp(g))
+                    dpad = NhwcDst::padded(reinterpret_cast<float*>(dws + off), g.oH, g.oW, dpl.aph,
+                                           dpl.apw);
+            }
+            {
+                PassScope pass("bwd");
+                ProfScope prof("layout", st, 0.0,
+                               4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g) +
+                                      (dpad.p ? g.N * dpad.img * umma_wgrad_kp(g) : 0)));
+                nchw_to_nhwc_padded(gy, NhwcDst::dense(gyh, g.oHW), dpad, g.N, g.K, g.oH, g.oW,
+                                    umma_wgrad_kp(g), gb, scale, accumulate, part, st);
+            }
+            if (dpad.p) bwd_data_impl(g, gy, w, gx, math, dws, st, dpad.p, true);
+            else bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
+            if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, st);
+            else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st);
+            return;
+        }
+        if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
+        if (gw) {
+            if (inner_gw_plain) bwd_filter_impl(g, x, gy, gw, gb, 1.f, 0, math, base, st, scale, accumulate);
+            else bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st, scale, accumulate);
+        }
+}
+
 
 }  // namespace
 
@@ -281,10 +379,10 @@ size_t pt_b200_conv_workspace_bytes(const pt_conv_geom* gp, int op, int math) {
         require_math(math);
         const Geo g(*gp);
         switch (op) {
-            case PT_CONV_FWD: r = fwd_ws(g, math); break;
-            case PT_CONV_BWD_DATA: r = bwd_data_ws(g, math); break;
-            case PT_CONV_BWD_FILTER: r = bwd_filter_ws(g, math); break;
-            case PT_CONV_BWD: r = bwd_ws(g, math); break;
+            case PT_CONV_FWD: r = fwd_ws_top(g, math); break;
+            case PT_CONV_BWD_DATA: r = bwd_data_ws_top(g, math); break;
+            case PT_CONV_BWD_FILTER: r = bwd_filter_ws_top(g, math); break;
+            case PT_CONV_BWD: r = bwd_ws_top(g, math); break;
             default: fail_validation("workspace: unknown conv op " + std::to_string(op));
         }
     });
@@ -302,20 +400,18 @@ int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, con
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
         PassScope pass("fwd");
-        if (fwd_rowconv(g, math)) {
-            require_ws(ws_bytes, rowconv_workspace(g), ws);
-            rowconv_fwd(g, x, w, b, y, ws, st);
+        require_ws(ws_bytes, fwd_ws_top(g, math), ws);
+        if (s2d_on(g, math)) {
+            const Geo e = s2d_geo(g);
+            char* base = reinterpret_cast<char*>(ws);
+            float* xs = reinterpret_cast<float*>(base);
+            float* wsd = reinterpret_cast<float*>(base + s2d_x_bytes(g));
+            s2d_input(g, x, xs, st);
+            s2d_weight(g, w, wsd, st);
+            fwd_core(e, xs, wsd, b, y, math, base + s2d_x_bytes(g) + s2d_w_bytes(g), st);
             return;
         }
-        if (math == PT_MATH_TF32) {
-            const UmmaPlan pl = umma_plan(g, false);
-            if (pl.ok) {
-                require_ws(ws_bytes, pl.ws_bytes, ws);
-                umma_conv_fwd(g, pl, x, w, b, y, ws, st);
-                return;
-            }
-        }
-        simt_conv_fwd(g, x, w, b, y, st);
+        fwd_core(g, x, w, b, y, math, ws, st);
     });
 }
 
@@ -328,8 +424,19 @@ int pt_b200_conv_bwd_data(const pt_conv_geom* gp, const float* gy, const float* 
         require_ptr(w, "weight");
         require_ptr(gx, "gradInput");
         const Geo g(*gp);
-        require_ws(ws_bytes, bwd_data_ws(g, math), ws);
-        bwd_data_impl(g, gy, w, gx, math, ws, as_stream(stream));
+        cudaStream_t st = as_stream(stream);
+        require_ws(ws_bytes, bwd_data_ws_top(g, math), ws);
+        if (s2d_on(g, math)) {
+            const Geo e = s2d_geo(g);
+            char* base = reinterpret_cast<char*>(ws);
+            float* wsd = reinterpret_cast<float*>(base);
+            float* gxs = reinterpret_cast<float*>(base + s2d_w_bytes(g));
+            s2d_weight(g, w, wsd, st);
+            bwd_data_impl(e, gy, wsd, gxs, math, base + s2d_w_bytes(g) + s2d_x_bytes(g), st);
+            d2s_grad(g, gxs, gx, st);
+            return;
+        }
+        bwd_data_impl(g, gy, w, gx, math, ws, st);
     });
 }
 
@@ -344,9 +451,20 @@ int pt_b200_conv_bwd_filter(const pt_conv_geom* gp, const float* x, const float*
         require_ptr(gw, "gradWeight");
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
-        const size_t need = bwd_filter_ws(g, math);
-        require_ws(ws_bytes, need, ws);
-        bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st);
+        require_ws(ws_bytes, bwd_filter_ws_top(g, math), ws);
+        if (s2d_on(g, math)) {
+            const Geo e = s2d_geo(g);
+            char* base = reinterpret_cast<char*>(ws);
+            float* xs = reinterpret_cast<float*>(base);
+            float* gws = reinterpret_cast<float*>(base + s2d_x_bytes(g));
+            s2d_input(g, x, xs, st);
+            bwd_filter_impl(e, xs, gy, gws, gb, 1.f, 0, math, base + s2d_x_bytes(g) + s2d_w_bytes(g), st,
+                            scale, accumulate);
+            d2s_weight_grad(g, gws, gw, scale, accumulate, st);
+            return;
+        }
+        bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st, scale,
+                        accumulate);
     });
 }
 
@@ -362,45 +480,24 @@ int pt_b200_conv_bwd(const pt_conv_geom* gp, const float* x, const float* gy, co
         if (gw) require_ptr(x, "input");
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
-        require_ws(ws_bytes, bwd_ws(g, math), ws);
-        char* base = reinterpret_cast<char*>(ws);
-        if (gx && gw && bwd_shared(g, math)) {
-            // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
-            float* gyh = reinterpret_cast<float*>(base);
-            float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
-            char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
-            char* wws = dws + align_up(bwd_data_ws(g, math), 256);
-            // a Hankel dgrad reads gy zero-bordered: the same pass writes that copy too
-            // (placed where that engine keeps its activation copy inside the dgrad workspace)
-            NhwcDst dpad{};
-            {
-                UmmaPlan dpl;
-                size_t off = 0;
-                if (dgrad_row(g, math)) {
-                    rowdgrad_ok(g, &dpl);
-                    off = rowdgrad_act_offset(g);
-                } else {
-                    dpl = umma_plan(g, true);
-                }
-                if (dpl.ok && dpl.hankel && dpl.cin_p == umma_wgrad_kp(g))
-                    dpad = NhwcDst::padded(reinterpret_cast<float*>(dws + off), g.oH, g.oW, dpl.aph,
-                                           dpl.apw);
-            }
-            {
-                PassScope pass("bwd");
-                ProfScope prof("layout", st, 0.0,
-                               4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g) +
-                                      (dpad.p ? g.N * dpad.img * umma_wgrad_kp(g) : 0)));
-                nchw_to_nhwc_padded(gy, NhwcDst::dense(gyh, g.oHW), dpad, g.N, g.K, g.oH, g.oW,
-                                    umma_wgrad_kp(g), gb, scale, accumulate, part, st);
-            }
-            if (dpad.p) bwd_data_impl(g, gy, w, gx, math, dws, st, dpad.p, true);
-            else bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
-            wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st);
+        require_ws(ws_bytes, bwd_ws_top(g, math), ws);
+        if (s2d_on(g, math)) {
+            const Geo e = s2d_geo(g);
+            char* base = reinterpret_cast<char*>(ws);
+            float* xs = reinterpret_cast<float*>(base);
+            float* wsd = reinterpret_cast<float*>(base + s2d_x_bytes(g));
+            float* gxs = reinterpret_cast<float*>(base + s2d_x_bytes(g) + s2d_w_bytes(g));
+            float* gws = reinterpret_cast<float*>(base + 2 * s2d_x_bytes(g) + s2d_w_bytes(g));
+            char* inner = base + 2 * s2d_x_bytes(g) + 2 * s2d_w_bytes(g);
+            if (gw) s2d_input(g, x, xs, st);
+            if (gx) s2d_weight(g, w, wsd, st);
+            bwd_core(e, xs, gy, wsd, gx ? gxs : nullptr, gw ? gws : nullptr, gb, scale, accumulate, math,
+                     inner, st, /*inner_gw_plain=*/true);
+            if (gx) d2s_grad(g, gxs, gx, st);
+            if (gw) d2s_weight_grad(g, gws, gw, scale, accumulate, st);
             return;
         }
-        if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
-        if (gw) bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st);
+        bwd_core(g, x, gy, w, gx, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st, false);
     });
 }
 

@@ -148,6 +148,15 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
                           const float* xh_pre = nullptr, double alg_flops = -1.0);
 int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 
+// ---- s2d.cu: space-to-depth for strided small-C layers ----
+bool s2d_applies(const Geo& g);
+Geo s2d_geo(const Geo& g);  // the equivalent stride-1 conv over C*s*s channels
+void s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st);
+void s2d_weight(const Geo& g, const float* w, float* ws, cudaStream_t st);
+void d2s_grad(const Geo& g, const float* gxs, float* gx, cudaStream_t st);
+void d2s_weight_grad(const Geo& g, const float* gws, float* gw, float scale, int accumulate,
+                     cudaStream_t st);
+
 // ---- unfold.cu ----
 void im2col_launch(const Geo& g, const float* x, int64_t n0, int64_t count, float* col,
                    cudaStream_t st);

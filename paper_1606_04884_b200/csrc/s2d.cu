@@ -1,0 +1,150 @@
+// s2d.cu — space-to-depth re-indexing of a strided small-channel convolution.
+//
+// A stride-s convolution with few input channels (AlexNet / Overfeat conv1: C = 3,
+// 11x11, stride 4) maps badly onto the tensor cores: 3 useful channels per 32-channel
+// (or 4-channel) operand slot and one tiny gather per tap. Splitting the padded input
+// into s x s phases turns it into a STRIDE-1 convolution over C*s*s channels with a
+// ceil(k/s) x ceil(k/s) filter (taps beyond k are zero):
+//
+//   x'[n][(c,a,b)][I][J] = x[n][c][s*I + a - pH][s*J + b - pW]          (0 outside)
+//   W'[k][(c,a,b)][p][q] = W[k][c][s*p + a][s*q + b]                      (0 if >= k)
+//   y[n][k][i][j]        = sum_{(c,a,b),p,q} x'[n][(c,a,b)][i+p][j+q] W'[k][(c,a,b)][p][q]
+//
+// which is exactly SPEC.md:353-361's conv_direct sum regrouped (every (r, s) tap of the
+// original appears once as (p, a) / (q, b)). The backward passes follow: gx is the
+// depth-to-space gather of gx' (each input pixel is one x' element), gW the gather of
+// gW'. Output y and gradBias are untouched.
+#include "kernels.cuh"
+
+namespace ptb {
+
+namespace {
+
+__global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict__ xs, int64_t N, int C,
+                                 int H, int W, int s, int pH, int pW, int Hs, int Ws) {
+    const int Cs = C * s * s;
+    const int64_t total = N * Cs * (int64_t)Hs * Ws;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int J = (int)(e % Ws);
+        const int I = (int)((e / Ws) % Hs);
+        const int cs = (int)((e / ((int64_t)Ws * Hs)) % Cs);
+        const int64_t n = e / ((int64_t)Ws * Hs * Cs);
+        const int c = cs / (s * s), a = (cs / s) % s, b = cs % s;
+        const int h = s * I + a - pH, w = s * J + b - pW;
+        xs[e] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(x + ((n * C + c) * H + h) * (int64_t)W + w) : 0.f;
+    }
+}
+
+__global__ void s2d_weight_kernel(const float* __restrict__ w, float* __restrict__ ws, int64_t K, int C,
+                                  int kH, int kW, int s, int kHs, int kWs) {
+    const int Cs = C * s * s;
+    const int64_t total = K * Cs * (int64_t)kHs * kWs;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(e % kWs);
+        const int p = (int)((e / kWs) % kHs);
+        const int cs = (int)((e / ((int64_t)kWs * kHs)) % Cs);
+        const int64_t k = e / ((int64_t)kWs * kHs * Cs);
+        const int c = cs / (s * s), a = (cs / s) % s, b = cs % s;
+        const int r = s * p + a, t = s * q + b;
+        ws[e] = (r < kH && t < kW) ? __ldg(w + ((k * C + c) * kH + r) * (int64_t)kW + t) : 0.f;
+    }
+}
+
+// gx[n][c][h][w] = gx'[n][(c, (h+pH)%s, (w+pW)%s)][(h+pH)/s][(w+pW)/s]
+__global__ void d2s_grad_kernel(const float* __restrict__ gxs, float* __restrict__ gx, int64_t N, int C,
+                                int H, int W, int s, int pH, int pW, int Hs, int Ws) {
+    const int64_t total = N * C * (int64_t)H * W;
+    const int Cs = C * s * s;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int w = (int)(e % W);
+        const int h = (int)((e / W) % H);
+        const int c = (int)((e / ((int64_t)W * H)) % C);
+        const int64_t n = e / ((int64_t)W * H * C);
+        const int hh = h + pH, ww = w + pW;
+        const int I = hh / s, J = ww / s;
+        float v = 0.f;  // pixels past the last output's receptive field get no gradient
+        if (I < Hs && J < Ws) {
+            const int cs = (c * s + hh % s) * s + ww % s;
+            v = __ldg(gxs + ((n * Cs + cs) * Hs + I) * (int64_t)Ws + J);
+        }
+        gx[e] = v;
+    }
+}
+
+// gw[k][c][r][t] = (acc ? gw : 0) + scale * gW'[k][(c, r%s, t%s)][r/s][t/s]
+__global__ void d2s_weight_grad_kernel(const float* __restrict__ gws, float* __restrict__ gw, int64_t K,
+                                       int C, int kH, int kW, int s, int kHs, int kWs, float scale,
+                                       int accumulate) {
+    const int64_t total = K * C * (int64_t)kH * kW;
+    const int Cs = C * s * s;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(e % kW);
+        const int r = (int)((e / kW) % kH);
+        const int c = (int)((e / ((int64_t)kW * kH)) % C);
+        const int64_t k = e / ((int64_t)kW * kH * C);
+        const int cs = (c * s + r % s) * s + t % s;
+        const float v = __ldg(gws + ((k * Cs + cs) * kHs + r / s) * (int64_t)kWs + t / s);
+        gw[e] = (accumulate ? gw[e] : 0.f) + scale * v;
+    }
+}
+
+unsigned blocks_for(int64_t total) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count()));
+}
+
+}  // namespace
+
+bool s2d_applies(const Geo& g) {
+    const int64_t s = g.sH;
+    if (s < 2 || g.sW != s || g.C * s * s > 64 || g.kH < s || g.kW < s) return false;
+    const Geo e = s2d_geo(g);
+    // the regrouped filter may not inflate the contraction by more than 1.5x
+    return e.CRS * 2 <= g.CRS * 3 && e.N * e.C * e.H * e.W < (1ll << 31);
+}
+
+Geo s2d_geo(const Geo& g) {
+    const int64_t s = g.sH;
+    const int64_t kHs = (g.kH + s - 1) / s, kWs = (g.kW + s - 1) / s;
+    pt_conv_geom e{g.N, g.C * s * s, g.oH + kHs - 1, g.oW + kWs - 1, g.K, kHs, kWs, 0, 0, 1, 1};
+    return Geo(e);
+}
+
+void s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st) {
+    const Geo e = s2d_geo(g);
+    ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + e.N * e.C * e.HW));
+    s2d_input_kernel<<<blocks_for(e.N * e.C * e.HW), 256, 0, st>>>(x, xs, g.N, (int)g.C, (int)g.H, (int)g.W,
+                                                                   (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H,
+                                                                   (int)e.W);
+    after_launch("s2d_input");
+}
+
+void s2d_weight(const Geo& g, const float* w, float* ws, cudaStream_t st) {
+    const Geo e = s2d_geo(g);
+    s2d_weight_kernel<<<blocks_for(e.K * e.CRS), 256, 0, st>>>(w, ws, g.K, (int)g.C, (int)g.kH, (int)g.kW,
+                                                               (int)g.sH, (int)e.kH, (int)e.kW);
+    after_launch("s2d_weight");
+}
+
+void d2s_grad(const Geo& g, const float* gxs, float* gx, cudaStream_t st) {
+    const Geo e = s2d_geo(g);
+    ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW * 2));
+    d2s_grad_kernel<<<blocks_for(g.N * g.C * g.HW), 256, 0, st>>>(gxs, gx, g.N, (int)g.C, (int)g.H, (int)g.W,
+                                                                  (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H,
+                                                                  (int)e.W);
+    after_launch("d2s_grad");
+}
+
+void d2s_weight_grad(const Geo& g, const float* gws, float* gw, float scale, int accumulate,
+                     cudaStream_t st) {
+    const Geo e = s2d_geo(g);
+    d2s_weight_grad_kernel<<<blocks_for(g.K * g.CRS), 256, 0, st>>>(gws, gw, g.K, (int)g.C, (int)g.kH,
+                                                                    (int)g.kW, (int)g.sH, (int)e.kH,
+                                                                    (int)e.kW, scale, accumulate);
+    after_launch("d2s_weight_grad");
+}
+
+}  // namespace ptb
