@@ -295,7 +295,9 @@ def main():
         b = pt.fill_uniform(torch.empty((K,), device=dev), seed + 3, -0.1, 0.1)
         gy = pt.fill_uniform(torch.empty(g.output_shape(), device=dev), seed + 4)
         bucket = GradBucket([torch.Size(g.weight_shape()), torch.Size((K,))], dev)
-        st.append(dict(name=name, g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
+        fb = pt.finput_bytes(g, args.math)
+        finput = torch.empty(fb, dtype=torch.uint8, device=dev) if fb else None
+        st.append(dict(name=name, finput=finput, g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
                        gx=torch.empty(g.input_shape(), device=dev), bucket=bucket,
                        gw=bucket.views[0], gb=bucket.views[1]))
     comm = torch.cuda.Stream(device=dev) if world > 1 else None
@@ -306,8 +308,10 @@ def main():
         for s in st:
             g = s["g"]
             L.lib().pt_b200_profile_tag(s["name"].encode())
-            pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math)
-            pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math)
+            # Torch's finput: the forward's relaid input is reused by accGradParameters
+            pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math, finput=s["finput"])
+            pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math,
+                             finput=s["finput"])
             # batch-sharded DP: one allreduce(sum) of this layer's gradW||gradB bucket on the
             # comm stream, overlapping the next layer's kernels
             done.append(allreduce_async(s["bucket"], comm))
@@ -422,6 +426,8 @@ def e2e(args, pt, torch, layers, dev, world, rank, dist):
         for k in ("x", "w", "b", "gy"):
             d[k].uniform_(-1, 1)
         d["g"] = g
+        fb = pt.finput_bytes(g, args.math)
+        d["finput"] = torch.empty(fb, dtype=torch.uint8, device=dev) if fb else None
         host.append(d)
     h2d = sum(4 * (d["x"].numel() + d["w"].numel() + d["b"].numel() + d["gy"].numel())
               for d in host)
@@ -435,8 +441,8 @@ def e2e(args, pt, torch, layers, dev, world, rank, dist):
             w = d["w"].to(dev, non_blocking=True)
             b = d["b"].to(dev, non_blocking=True)
             gy = d["gy"].to(dev, non_blocking=True)
-            y = pt.conv_forward(g, x, w, b, math=args.math)
-            gx, gw, gb = pt.conv_backward(g, x, gy, w, math=args.math)
+            y = pt.conv_forward(g, x, w, b, math=args.math, finput=d["finput"])
+            gx, gw, gb = pt.conv_backward(g, x, gy, w, math=args.math, finput=d["finput"])
             if world > 1:
                 dist.all_reduce(gw)
                 dist.all_reduce(gb)

@@ -88,8 +88,14 @@ public:
     void zeroGradParameters();
 
     DeviceTensor weight, bias, gradWeight, gradBias, output, gradInput;
+    /// Torch's finput: updateOutput's relaid (channels-last) input, reused by backward()
+    /// while the same input tensor is passed (pt_b200_conv_finput_bytes may be 0).
+    DeviceTensor finput;
     int nInputPlane, nOutputPlane, kW, kH, dW, dH, padW, padH;
     Math math;
+
+private:
+    const float* finputFor_ = nullptr;
 };
 
 }  // namespace portten::conv

@@ -119,6 +119,18 @@ int pt_b200_conv_bwd_filter(const pt_conv_geom* g, const float* x, const float* 
 int pt_b200_conv_bwd(const pt_conv_geom* g, const float* x, const float* gy, const float* w,
                      float* gx, float* gw, float* gb, float scale, int accumulate, int math,
                      void* ws, size_t ws_bytes, void* stream);
+/* Torch's `finput` (nn.SpatialConvolutionMM keeps the input unfold of updateOutput for
+ * accGradParameters): the forward engine's channels-last copy of x, which the weight
+ * gradient can reuse instead of re-laying x out. finput_bytes is 0 when the engines do
+ * not share a layout for this geometry (the *_finput calls then ignore the buffer).
+ * Contract as in Torch: x must be unchanged between the two calls. */
+size_t pt_b200_conv_finput_bytes(const pt_conv_geom* g, int math);
+int pt_b200_conv_fwd_finput(const pt_conv_geom* g, const float* x, const float* w, const float* b,
+                            float* y, int math, void* ws, size_t ws_bytes, float* finput,
+                            void* stream);
+int pt_b200_conv_bwd_finput(const pt_conv_geom* g, const float* x, const float* gy, const float* w,
+                            float* gx, float* gw, float* gb, float scale, int accumulate, int math,
+                            void* ws, size_t ws_bytes, const float* finput, void* stream);
 /* Standalone unfold of ONE image, bit-exact with proj/templates/im2col.kt.tmpl:9-21. */
 int pt_b200_im2col(const pt_conv_geom* g, const float* img, float* col, void* stream);
 /* Batched unfold: images [n0, n0+count) into (CRS) x (count*oHW). */

@@ -76,6 +76,11 @@ _SIGS = {
                                           C.c_int, C.c_int, _P, C.c_size_t, _P]),
     "pt_b200_conv_bwd": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, _P, _P, C.c_float,
                                    C.c_int, C.c_int, _P, C.c_size_t, _P]),
+    "pt_b200_conv_finput_bytes": (C.c_size_t, [C.POINTER(PtConvGeom), C.c_int]),
+    "pt_b200_conv_fwd_finput": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, C.c_int, _P,
+                                          C.c_size_t, _P, _P]),
+    "pt_b200_conv_bwd_finput": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, _P, _P,
+                                          C.c_float, C.c_int, C.c_int, _P, C.c_size_t, _P, _P]),
     "pt_b200_im2col": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P]),
     "pt_b200_im2col_batched": (C.c_int, [C.POINTER(PtConvGeom), _P, C.c_int64, C.c_int64, _P,
                                          _P]),

@@ -146,8 +146,16 @@ def workspace_bytes(g: ConvGeometry, op: int, math="tf32") -> int:
     return n
 
 
-def conv_forward(g: ConvGeometry, x, w, b=None, y=None, math="tf32"):
-    """updateOutput == conv_im2col_forward (SPEC.md:389-397): y = W * im2col(x) + b."""
+def finput_bytes(g: ConvGeometry, math="tf32") -> int:
+    """Bytes of Torch's `finput` buffer for this geometry: the forward pass's channels-last
+    copy of x that accGradParameters reuses (0 = no shared layout, the buffer is ignored)."""
+    gc = g.c()
+    return int(lib().pt_b200_conv_finput_bytes(C.byref(gc), _math(math)))
+
+
+def conv_forward(g: ConvGeometry, x, w, b=None, y=None, math="tf32", finput=None):
+    """updateOutput == conv_im2col_forward (SPEC.md:389-397): y = W * im2col(x) + b.
+    finput (uint8 device tensor of finput_bytes(g)): keep the relaid input for backward."""
     gc, m = g.c(), _math(math)
     check(lib().pt_b200_conv_validate(C.byref(gc)))
     if y is None:
@@ -157,8 +165,21 @@ def conv_forward(g: ConvGeometry, x, w, b=None, y=None, math="tf32"):
     pb = _dev(b, (g.outChannels,), "bias") if b is not None else None
     py = _dev(y, g.output_shape(), "output")
     ws, wsn = WORKSPACE.get(workspace_bytes(g, _lib.PT_CONV_FWD, m))
-    check(lib().pt_b200_conv_fwd(C.byref(gc), px, pw, pb, py, m, ws or None, wsn, _stream()))
+    if finput is not None:
+        check(lib().pt_b200_conv_fwd_finput(C.byref(gc), px, pw, pb, py, m, ws or None, wsn,
+                                            _finput(g, finput, m), _stream()))
+    else:
+        check(lib().pt_b200_conv_fwd(C.byref(gc), px, pw, pb, py, m, ws or None, wsn, _stream()))
     return y
+
+
+def _finput(g: ConvGeometry, buf, m):
+    need = int(lib().pt_b200_conv_finput_bytes(C.byref(g.c()), m))
+    if need == 0:
+        return None
+    if not (buf.is_cuda and buf.is_contiguous() and buf.numel() * buf.element_size() >= need):
+        raise ValidationError(f"finput: need a contiguous device buffer of {need} bytes")
+    return buf.data_ptr()
 
 
 def conv_im2col_batched(g: ConvGeometry, x, w, b=None, batchChunk: int = 1, y=None, math="tf32"):
@@ -205,7 +226,7 @@ def conv_backward_weight(g: ConvGeometry, x, gy, gw=None, gb=None, scale: float 
 
 def conv_backward(g: ConvGeometry, x, gy, w, gx=None, gw=None, gb=None, scale: float = 1.0,
                   accumulate: bool = False, need_input_grad: bool = True, with_bias: bool = True,
-                  math="tf32"):
+                  math="tf32", finput=None):
     """Torch backward() = updateGradInput + accGradParameters in one C-ABI call
     (pt_b200_conv_bwd): one NHWC transform of gy, gradBias fused into it, feeds both
     tensor-core passes. Returns (gx, gw, gb); gx is None when need_input_grad=False."""
@@ -218,13 +239,16 @@ def conv_backward(g: ConvGeometry, x, gy, w, gx=None, gw=None, gb=None, scale: f
     if gb is None and with_bias:
         gb = torch.zeros((g.outChannels,), dtype=torch.float32, device=gy.device)
     ws, wsn = WORKSPACE.get(workspace_bytes(g, _lib.PT_CONV_BWD, m))
-    check(lib().pt_b200_conv_bwd(
-        C.byref(gc), _dev(x, g.input_shape(), "input"), _dev(gy, g.output_shape(), "gradOutput"),
-        _dev(w, g.weight_shape(), "weight"),
-        _dev(gx, g.input_shape(), "gradInput") if gx is not None else None,
-        _dev(gw, g.weight_shape(), "gradWeight"),
-        _dev(gb, (g.outChannels,), "gradBias") if gb is not None else None,
-        float(scale), int(bool(accumulate)), m, ws or None, wsn, _stream()))
+    args = (C.byref(gc), _dev(x, g.input_shape(), "input"), _dev(gy, g.output_shape(), "gradOutput"),
+            _dev(w, g.weight_shape(), "weight"),
+            _dev(gx, g.input_shape(), "gradInput") if gx is not None else None,
+            _dev(gw, g.weight_shape(), "gradWeight"),
+            _dev(gb, (g.outChannels,), "gradBias") if gb is not None else None,
+            float(scale), int(bool(accumulate)), m, ws or None, wsn)
+    if finput is not None:
+        check(lib().pt_b200_conv_bwd_finput(*args, _finput(g, finput, m), _stream()))
+    else:
+        check(lib().pt_b200_conv_bwd(*args, _stream()))
     return gx, gw, gb
 
 

@@ -114,10 +114,11 @@ size_t wgrad_tc_ws(const Geo& g, int math) {
     return align_up(wgrad_row(g, math) ? rowwgrad_workspace(g) : umma_wgrad_workspace(g), 256);
 }
 void wgrad_tc_run(const Geo& g, const float* x, const float* gy, const float* gyh, float* gw, float scale,
-                  int accumulate, int math, char* ws, cudaStream_t st) {
+                  int accumulate, int math, char* ws, cudaStream_t st, const float* xh_pre = nullptr,
+                  int64_t xph = 0, int64_t xpw = 0) {
     PassScope pass("wgrad");
     if (wgrad_row(g, math)) rowwgrad(g, x, gyh, gw, scale, accumulate, ws, st);
-    else umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, ws, st, gyh);
+    else umma_conv_bwd_filter(g, x, gy, gw, scale, accumulate, ws, st, gyh, xh_pre, -1.0, xph, xpw);
 }
 size_t gyh_bytes(const Geo& g) { return align_up((size_t)(g.M * umma_wgrad_kp(g)) * 4, 256); }
 size_t bias_part_bytes(const Geo& g) { return align_up(nhwc_bias_partials_bytes(g.N, g.K, g.oHW), 256); }
@@ -161,8 +162,25 @@ void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, f
     }
 }
 
+bool s2d_on(const Geo& g, int math);
+
+// Torch's `finput`: the relaid input updateOutput prepares and accGradParameters reuses.
+// Here it is the forward engine's NHWC copy of x, shareable when the weight-gradient
+// kernel reads the same layout (32-channel chunks; a Hankel forward's copy carries its
+// zero border, which the wgrad im2col descriptor absorbs). 0 = not shareable.
+size_t finput_layout(const Geo& g, int math, int64_t* ph = nullptr, int64_t* pw = nullptr) {
+    if (math != PT_MATH_TF32 || s2d_on(g, math) || fwd_rowconv(g, math) || wgrad_row(g, math) ||
+        !umma_wgrad_ok(g))
+        return 0;
+    const UmmaPlan pl = umma_plan(g, false);
+    if (!pl.ok || pl.cb != 32 || pl.cin_p != (g.C + 31) / 32 * 32) return 0;
+    if (ph) *ph = pl.hankel ? pl.aph : 0;
+    if (pw) *pw = pl.hankel ? pl.apw : 0;
+    return align_up((size_t)pl.act_elems * 4, 256);
+}
+
 void fwd_core(const Geo& g, const float* x, const float* w, const float* b, float* y, int math,
-              void* ws, cudaStream_t st) {
+              void* ws, cudaStream_t st, float* finput = nullptr) {
     if (fwd_rowconv(g, math)) {
         rowconv_fwd(g, x, w, b, y, ws, st);
         return;
@@ -170,7 +188,8 @@ void fwd_core(const Geo& g, const float* x, const float* w, const float* b, floa
     if (math == PT_MATH_TF32) {
         const UmmaPlan pl = umma_plan(g, false);
         if (pl.ok) {
-            umma_conv_fwd(g, pl, x, w, b, y, ws, st);
+            umma_conv_fwd(g, pl, x, w, b, y, ws, st,
+                          finput && finput_layout(g, math) ? finput : nullptr);
             return;
         }
     }
@@ -219,7 +238,9 @@ void require_ws(size_t have, size_t need, const void* ws) {
 // gradBias still takes the caller's scale / accumulate.
 void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, float* gx, float* gw,
               float* gb, float scale, int accumulate, int math, char* ws, cudaStream_t st,
-              bool inner_gw_plain) {
+              bool inner_gw_plain, const float* finput = nullptr) {
+    int64_t fph = 0, fpw = 0;
+    if (finput && !finput_layout(g, math, &fph, &fpw)) finput = nullptr;
         char* base = ws;
         if (gx && gw && bwd_shared(g, math)) {
             // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
@@ -253,8 +274,8 @@ void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, flo
             }
             if (dpad.p) bwd_data_impl(g, gy, w, gx, math, dws, st, dpad.p, true);
             else bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
-            if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, st);
-            else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st);
+            if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, st, finput, fph, fpw);
+            else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st, finput, fph, fpw);
             return;
         }
         if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
@@ -389,8 +410,8 @@ size_t pt_b200_conv_workspace_bytes(const pt_conv_geom* gp, int op, int math) {
     return st == PT_OK ? r : (size_t)-1;
 }
 
-int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, const float* b,
-                     float* y, int math, void* ws, size_t ws_bytes, void* stream) {
+static int conv_fwd_entry(const pt_conv_geom* gp, const float* x, const float* w, const float* b,
+                          float* y, int math, void* ws, size_t ws_bytes, float* finput, void* stream) {
     return guarded([&] {
         validate_geom(gp);
         require_math(math);
@@ -411,8 +432,28 @@ int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, con
             fwd_core(e, xs, wsd, b, y, math, base + s2d_x_bytes(g) + s2d_w_bytes(g), st);
             return;
         }
-        fwd_core(g, x, w, b, y, math, ws, st);
+        fwd_core(g, x, w, b, y, math, ws, st, finput);
     });
+}
+
+int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, const float* b,
+                     float* y, int math, void* ws, size_t ws_bytes, void* stream) {
+    return conv_fwd_entry(gp, x, w, b, y, math, ws, ws_bytes, nullptr, stream);
+}
+
+int pt_b200_conv_fwd_finput(const pt_conv_geom* gp, const float* x, const float* w, const float* b,
+                            float* y, int math, void* ws, size_t ws_bytes, float* finput, void* stream) {
+    return conv_fwd_entry(gp, x, w, b, y, math, ws, ws_bytes, finput, stream);
+}
+
+size_t pt_b200_conv_finput_bytes(const pt_conv_geom* gp, int math) {
+    size_t r = 0;
+    const int st = guarded([&] {
+        validate_geom(gp);
+        require_math(math);
+        r = finput_layout(Geo(*gp), math);
+    });
+    return st == PT_OK ? r : 0;
 }
 
 int pt_b200_conv_bwd_data(const pt_conv_geom* gp, const float* gy, const float* w, float* gx,
@@ -468,9 +509,9 @@ int pt_b200_conv_bwd_filter(const pt_conv_geom* gp, const float* x, const float*
     });
 }
 
-int pt_b200_conv_bwd(const pt_conv_geom* gp, const float* x, const float* gy, const float* w,
-                     float* gx, float* gw, float* gb, float scale, int accumulate, int math,
-                     void* ws, size_t ws_bytes, void* stream) {
+static int conv_bwd_entry(const pt_conv_geom* gp, const float* x, const float* gy, const float* w,
+                          float* gx, float* gw, float* gb, float scale, int accumulate, int math,
+                          void* ws, size_t ws_bytes, const float* finput, void* stream) {
     return guarded([&] {
         validate_geom(gp);
         require_math(math);
@@ -497,8 +538,23 @@ int pt_b200_conv_bwd(const pt_conv_geom* gp, const float* x, const float* gy, co
             if (gw) d2s_weight_grad(g, gws, gw, scale, accumulate, st);
             return;
         }
-        bwd_core(g, x, gy, w, gx, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st, false);
+        bwd_core(g, x, gy, w, gx, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st, false,
+                 finput);
     });
+}
+
+int pt_b200_conv_bwd(const pt_conv_geom* gp, const float* x, const float* gy, const float* w,
+                     float* gx, float* gw, float* gb, float scale, int accumulate, int math,
+                     void* ws, size_t ws_bytes, void* stream) {
+    return conv_bwd_entry(gp, x, gy, w, gx, gw, gb, scale, accumulate, math, ws, ws_bytes, nullptr,
+                          stream);
+}
+
+int pt_b200_conv_bwd_finput(const pt_conv_geom* gp, const float* x, const float* gy, const float* w,
+                            float* gx, float* gw, float* gb, float scale, int accumulate, int math,
+                            void* ws, size_t ws_bytes, const float* finput, void* stream) {
+    return conv_bwd_entry(gp, x, gy, w, gx, gw, gb, scale, accumulate, math, ws, ws_bytes, finput,
+                          stream);
 }
 
 int pt_b200_im2col(const pt_conv_geom* gp, const float* img, float* col, void* stream) {

@@ -105,8 +105,10 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
 //   pad' = k-1-pad (stride 1).  kDgradGcol (small C / strided): gcol = W^T gy as a
 //   1x1 conv over gy (n_rows = CRS) then a gather col2im.
 UmmaPlan umma_plan(const Geo& g, bool dgrad);
+// act_out: where the NHWC activation copy goes (Torch's finput, reused by the weight
+// gradient); null = the workspace.
 void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float* w,
-                   const float* b, float* y, void* ws, cudaStream_t st);
+                   const float* b, float* y, void* ws, cudaStream_t st, float* act_out = nullptr);
 // gyh_pre: gy already in the plan's NHWC layout (TF32-rounded; zero-bordered when
 // pl.hankel), or null to transform here.
 void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
@@ -141,11 +143,13 @@ void rowwgrad(const Geo& g, const float* x, const float* gyh, float* gw, float s
 bool umma_wgrad_ok(const Geo& g);
 size_t umma_wgrad_workspace(const Geo& g);
 // gyh_pre: gy already in NHWC [M][round_up(K,32)] (TF32-rounded), or null.
-// xh_pre: x already NHWC [N][HW][round_up(C,32)] (TF32-rounded), or null.
+// xh_pre: x already NHWC [N][H+2*xph][W+2*xpw][round_up(C,32)] (TF32-rounded, zero border
+// of (xph, xpw) — the forward pass's copy), or null.
 // alg_flops: algorithmic FLOPs recorded for the live roofline (default 2*M*K*CRS of g).
 void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* gw, float scale,
                           int accumulate, void* ws, cudaStream_t st, const float* gyh_pre = nullptr,
-                          const float* xh_pre = nullptr, double alg_flops = -1.0);
+                          const float* xh_pre = nullptr, double alg_flops = -1.0, int64_t xph = 0,
+                          int64_t xpw = 0);
 int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 
 // ---- s2d.cu: space-to-depth for strided small-C layers ----

@@ -423,6 +423,14 @@ int hconv_pair_env() {
     return v;
 }
 
+int hconv_pair_max() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_HCONV_PAIR_MAX");
+        return e ? std::atoi(e) : 64;  // measured: pairing at 128 rows (N=256) is slower
+    }();
+    return v;
+}
+
 void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, int64_t pw, int64_t kW,
                  int64_t oH, int64_t oW) {
     if (pl.cb != 32 || pl.cg != 2 || kW < 3 || kW > 120 || hconv_env() == 0) return;
@@ -437,7 +445,10 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
     // L2->SM traffic
     if (hconv_env() != 1 && eff < 0.84) return;
     pl.hankel = true;
-    if (pl.n_rows <= 64 && hconv_pair_env() != 0) {
+    // pairing doubles N: for <= 64 rows it beats the N=64 MMA floor (L2 dgrad 1.27 ->
+    // 0.92 ms). Allowed up to 128 rows (N=256) by PT_B200_HCONV_PAIR_MAX, but measured
+    // slower there (L2 fwd 0.65 -> 0.75 ms)
+    if (pl.n_rows <= hconv_pair_max() && hconv_pair_env() != 0) {
         // tap pairing: one N tile of all the rows, one extra zero tap in the packing
         pl.tap_pair = true;
         pl.bn = (int)((pl.n_rows + 7) / 8 * 8);
@@ -507,8 +518,8 @@ UmmaPlan umma_plan(const Geo& g, bool dgrad) {
 }
 
 void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float* w,
-                   const float* b, float* y, void* ws, cudaStream_t st) {
-    float* act = reinterpret_cast<float*>(ws);
+                   const float* b, float* y, void* ws, cudaStream_t st, float* act_out) {
+    float* act = act_out ? act_out : reinterpret_cast<float*>(ws);
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
     if (pl.hankel) {
         {

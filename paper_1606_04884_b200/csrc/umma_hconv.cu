@@ -65,8 +65,8 @@ struct HConvParams {
 };
 
 // CPS: 32-channel chunks per pipeline stage (1 or 2).
-// PAIR (output-shift tap pairing, for <= 64 output channels where an N=64 MMA costs as
-// much as N=128): one MMA computes taps s and s+1 from the SAME pixel run (shift s) —
+// PAIR (output-shift tap pairing, for <= 128 output channels: an N=64 MMA costs as much
+// as N=128, and an N=256 MMA reads the A tile once for two taps): one MMA computes taps s and s+1 from the SAME pixel run (shift s) —
 // CTA 0 stages tap s's weights, CTA 1 tap s+1's, N = 2*bn. Column half 1 then holds tap
 // s+1's contribution to the position one to the LEFT, so the epilogue forms
 // out[q] = D0[q] + D1[q+1]; each CTA's last lane lacks its right neighbour and is
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     uint64_t* tfull = bempty + p.sb;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // PAIR: [4 chunks][3 warps][16]
+    float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // PAIR: [8 chunks][3 warps][16]
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                         tc_fence_after();
                         const uint32_t alo = desc_lo(smem_u32(sA + (size_t)as * p.stage_a), 16);
                         for (int s = 0; s < p.kW; s += PAIR ? 2 : 1) {
-                            mbar_wait(&bfull[bs], bph);
+                            if (p.exp != 4 || s == 0) mbar_wait(&bfull[bs], bph);
                             tc_fence_after();
                             // tap s: the same pixel run, s rows (s*128 B) further in
                             const uint32_t a_s = alo + (p.exp == 2 ? 0u : p.exp == 3 ? (uint32_t)(s & ~7) * 8u
@@ -365,7 +365,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         p.exp = e ? std::atoi(e) : 0;
     }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
-                        (2 * sa + 2 * sb + 4) * 8 + 16 + 4 * 48 * 4;
+                        (2 * sa + 2 * sb + 4) * 8 + 16 + 8 * 48 * 4;
     const int units = p.tiles * p.n_tiles;
     const int ncl = std::min(units, sm_count() / 2);
     static bool attr = false;
@@ -394,7 +394,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     cfg.numAttrs = 1;
     ProfScope prof("umma_conv", st, alg_flops, 0.0);
     if (pair) {
-        PTB_REQUIRE(p.bn <= 64, "hconv: tap pairing needs <= 64 output channels");
+        PTB_REQUIRE(p.bn <= 128, "hconv: tap pairing needs <= 128 output channels");
         if (cps == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<2, true>, p));
         else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<1, true>, p));
     } else {

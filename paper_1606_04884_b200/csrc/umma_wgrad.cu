@@ -293,7 +293,8 @@ int64_t umma_wgrad_kp(const Geo& g) { return (g.K + 31) / 32 * 32; }
 
 void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* gw, float scale,
                           int accumulate, void* ws, cudaStream_t st, const float* gyh_pre,
-                          const float* xh_pre, double alg_flops) {
+                          const float* xh_pre, double alg_flops, int64_t xph, int64_t xpw) {
+    if (!xh_pre) xph = xpw = 0;
     const WPlan w = wplan(g);
     char* base = reinterpret_cast<char*>(ws);
     float* xh = reinterpret_cast<float*>(base);
@@ -317,14 +318,16 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
         const uint32_t box[2] = {32, kPix};
         tmap_tiled(&p.tmap_gy, gyh, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
-    tmap_im2col(&p.tmap_x, xh, g.N, g.H, g.W, w.Cp, (int)g.kH, (int)g.kW, (int)g.pH, (int)g.pW,
+    // a zero-bordered copy carries (part of) the padding itself
+    const int64_t xH = g.H + 2 * xph, xW = g.W + 2 * xpw, epH = g.pH - xph, epW = g.pW - xpw;
+    tmap_im2col(&p.tmap_x, xh, g.N, xH, xW, w.Cp, (int)g.kH, (int)g.kW, (int)epH, (int)epW,
                 (int)g.sH, (int)g.sW, 32, kPix, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     p.oH = (int)g.oH;
     p.oW = (int)g.oW;
     p.sH = (int)g.sH;
     p.sW = (int)g.sW;
-    p.pH = (int)g.pH;
-    p.pW = (int)g.pW;
+    p.pH = (int)epH;
+    p.pW = (int)epW;
     p.kW = (int)g.kW;
     p.taps = (int)(g.kH * g.kW);
     p.Cp = (int)w.Cp;

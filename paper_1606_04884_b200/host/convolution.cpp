@@ -255,7 +255,24 @@ ConvGeometry SpatialConvolutionMM::geometry(const DeviceTensor& x) const {
 }
 
 const DeviceTensor& SpatialConvolutionMM::updateOutput(const DeviceTensor& input) {
-    output = conv_forward(geometry(input), input, weight, &bias, math);
+    const ConvGeometry g = geometry(input);
+    const pt_conv_geom a = g.abi();
+    const std::size_t fb = pt_b200_conv_finput_bytes(&a, static_cast<int>(math));
+    finputFor_ = nullptr;
+    if (fb == 0) {
+        output = conv_forward(g, input, weight, &bias, math);
+        return output;
+    }
+    // Torch's finput: keep the forward's relaid input for accGradParameters
+    const std::int64_t fe = static_cast<std::int64_t>((fb + 3) / 4);
+    if (finput.numel() < fe) finput = DeviceTensor::empty({fe});
+    PORTTEN_CHECK(input.isContiguous() && weight.isContiguous(), "conv operands must be contiguous");
+    output = DeviceTensor::empty({g.batch, g.outChannels, g.outHeight(), g.outWidth()});
+    const std::size_t n = ws_bytes(g, PT_CONV_FWD, math);
+    throw_if_error(pt_b200_conv_fwd_finput(&a, input.data(), weight.data(), bias.data(), output.data(),
+                                           static_cast<int>(math), t_scratch.get(n), n, finput.data(),
+                                           nullptr));
+    finputFor_ = input.data();
     return output;
 }
 
@@ -276,9 +293,11 @@ const DeviceTensor& SpatialConvolutionMM::backward(const DeviceTensor& input, co
     gradInput = DeviceTensor::empty({g.batch, g.inChannels, g.inHeight, g.inWidth});
     const pt_conv_geom a = g.abi();
     const std::size_t n = ws_bytes(g, PT_CONV_BWD, math);
-    throw_if_error(pt_b200_conv_bwd(&a, input.data(), gradOutput.data(), weight.data(), gradInput.data(),
-                                    gradWeight.data(), gradBias.data(), scale, 1, static_cast<int>(math),
-                                    t_scratch.get(n), n, nullptr));
+    // the saved finput stands for `input` only if it is the tensor updateOutput saw
+    const float* fin = finputFor_ == input.data() ? finput.data() : nullptr;
+    throw_if_error(pt_b200_conv_bwd_finput(&a, input.data(), gradOutput.data(), weight.data(),
+                                           gradInput.data(), gradWeight.data(), gradBias.data(), scale, 1,
+                                           static_cast<int>(math), t_scratch.get(n), n, fin, nullptr));
     return gradInput;
 }
 

@@ -34,6 +34,10 @@ class SpatialConvolutionMM:
         self.gradBias = torch.zeros_like(self.bias)
         self.output = None
         self.gradInput = None
+        # Torch's finput: updateOutput's relaid input, reused by accGradParameters while the
+        # input is unchanged (same storage, same version counter)
+        self.finput = None
+        self._finput_key = None
         self.reset()
 
     def reset(self, stdv=None, seed=0x5EED):
@@ -61,9 +65,21 @@ class SpatialConvolutionMM:
     def updateOutput(self, input):
         x, host = self._on_device(input)
         g = self.geometry(x)
-        y = _conv.conv_forward(g, x, self.weight, self.bias, math=self.math)
+        need = _conv.finput_bytes(g, self.math)
+        if need:
+            if self.finput is None or self.finput.numel() < need:
+                self.finput = torch.empty(need, dtype=torch.uint8, device=self.device)
+            y = _conv.conv_forward(g, x, self.weight, self.bias, math=self.math, finput=self.finput)
+            self._finput_key = (x.data_ptr(), x._version, tuple(x.shape))
+        else:
+            y = _conv.conv_forward(g, x, self.weight, self.bias, math=self.math)
+            self._finput_key = None
         self.output = y.cpu() if host else y
         return self.output
+
+    def _saved_finput(self, x):
+        key = (x.data_ptr(), x._version, tuple(x.shape))
+        return self.finput if self._finput_key is not None and key == self._finput_key else None
 
     def updateGradInput(self, input, gradOutput):
         x, host = self._on_device(input)
@@ -93,7 +109,8 @@ class SpatialConvolutionMM:
         gy, _ = self._on_device(gradOutput)
         g = self.geometry(x)
         gx, _, _ = _conv.conv_backward(g, x, gy, self.weight, gw=self.gradWeight, gb=self.gradBias,
-                                       scale=scale, accumulate=True, math=self.math)
+                                       scale=scale, accumulate=True, math=self.math,
+                                       finput=self._saved_finput(x))
         self.gradInput = gx.cpu() if host else gx
         return self.gradInput
 

@@ -143,3 +143,27 @@ def test_convnet_layers_batch_slice(name):
     check_tf32(y, ry, f"{name} fwd")
     check_tf32(gx, rgx, f"{name} dgrad")
     check_tf32(gw, rgw, f"{name} wgrad")
+
+
+FINPUT_GEOMS = [g for g in TC_GEOMS] + [
+    po.geom(2, 64, 20, 20, 128, 9, 9, 0, 0, 1, 1),   # Hankel fwd, pad 0
+    po.geom(2, 96, 17, 19, 80, 5, 5, 2, 2, 1, 1),    # Hankel fwd copy carries a 2-pixel border
+    po.geom(2, 32, 30, 30, 64, 3, 3, 1, 1, 1, 1),    # tap-paired Hankel (<= 64 out channels)
+]
+
+
+@pytest.mark.parametrize("g", FINPUT_GEOMS, ids=gstr)
+def test_finput_reuse_bitwise(g):
+    """Torch's finput: the forward's channels-last copy of x reused by accGradParameters
+    gives bitwise the same y / gradInput / gradWeight / gradBias as re-laying x out."""
+    pt = _pt()
+    x, w, b, gy = conv_inputs(g, 77)
+    G = _g(g)
+    nb = pt.finput_bytes(G)
+    fin = torch.empty(max(nb, 1), dtype=torch.uint8, device="cuda")
+    y0 = pt.conv_forward(G, _d(x), _d(w), _d(b))
+    y1 = pt.conv_forward(G, _d(x), _d(w), _d(b), finput=fin)
+    gx0, gw0, gb0 = pt.conv_backward(G, _d(x), _d(gy), _d(w))
+    gx1, gw1, gb1 = pt.conv_backward(G, _d(x), _d(gy), _d(w), finput=fin)
+    for a, c, what in ((y0, y1, "y"), (gx0, gx1, "gx"), (gw0, gw1, "gw"), (gb0, gb1, "gb")):
+        np.testing.assert_array_equal(_h(a), _h(c), err_msg=f"{gstr(g)} {what} (finput {nb} B)")
