@@ -83,6 +83,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-finput", action="store_true", help="re-lay x out in the weight gradient")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -295,7 +296,7 @@ def main():
         b = pt.fill_uniform(torch.empty((K,), device=dev), seed + 3, -0.1, 0.1)
         gy = pt.fill_uniform(torch.empty(g.output_shape(), device=dev), seed + 4)
         bucket = GradBucket([torch.Size(g.weight_shape()), torch.Size((K,))], dev)
-        fb = pt.finput_bytes(g, args.math)
+        fb = 0 if args.no_finput else pt.finput_bytes(g, args.math)
         finput = torch.empty(fb, dtype=torch.uint8, device=dev) if fb else None
         st.append(dict(name=name, finput=finput, g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
                        gx=torch.empty(g.input_shape(), device=dev), bucket=bucket,

@@ -53,6 +53,10 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, N
     }
     __syncthreads();
     const int64_t c = c0 + threadIdx.x;
+    // zero-bordered destinations: (h, w) of this thread's pixel advanced incrementally
+    // (a division per element made the padded pass ALU-bound)
+    const int Wd = (int)(PAD ? d0.W : d1.W);
+    int ph_ = (int)((p0 + threadIdx.y) / Wd), pw_ = (int)((p0 + threadIdx.y) - (int64_t)ph_ * Wd);
 #pragma unroll 4
     for (int k = 0; k < kStripPx / 8; ++k) {
         const int pl = threadIdx.y + 8 * k;
@@ -61,11 +65,18 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, N
             float v = tile[threadIdx.x][pl];
             if (round_tf32) v = to_tf32(v);
             if constexpr (PAD) {
-                o0[d0.pixel(p) * Cp + c] = v;
-                if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
+                o0[((ph_ + d0.ph) * d0.Wp + pw_ + d0.pw) * Cp + c] = v;
+                if constexpr (TWO) o1[((ph_ + d1.ph) * d1.Wp + pw_ + d1.pw) * Cp + c] = v;
             } else {
                 o0[p * Cp + c] = v;
-                if constexpr (TWO) o1[d1.pixel(p) * Cp + c] = v;
+                if constexpr (TWO) o1[((ph_ + d1.ph) * d1.Wp + pw_ + d1.pw) * Cp + c] = v;
+            }
+        }
+        if constexpr (PAD || TWO) {
+            pw_ += 8;
+            while (pw_ >= Wd) {
+                pw_ -= Wd;
+                ++ph_;
             }
         }
     }

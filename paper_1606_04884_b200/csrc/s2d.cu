@@ -20,19 +20,25 @@ namespace ptb {
 
 namespace {
 
-__global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict__ xs, int64_t N, int C,
+// One output row (n, (c,a,b), I) per (blockIdx.x, threadIdx.y); threads sweep J. 32-bit
+// index maths only once per row: the per-element 64-bit div/mod chain made this pass
+// ALU-bound (0.45 TB/s).
+__global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict__ xs, int rows, int C,
                                  int H, int W, int s, int pH, int pW, int Hs, int Ws) {
     const int Cs = C * s * s;
-    const int64_t total = N * Cs * (int64_t)Hs * Ws;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int J = (int)(e % Ws);
-        const int I = (int)((e / Ws) % Hs);
-        const int cs = (int)((e / ((int64_t)Ws * Hs)) % Cs);
-        const int64_t n = e / ((int64_t)Ws * Hs * Cs);
-        const int c = cs / (s * s), a = (cs / s) % s, b = cs % s;
-        const int h = s * I + a - pH, w = s * J + b - pW;
-        xs[e] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(x + ((n * C + c) * H + h) * (int64_t)W + w) : 0.f;
+    const int row = blockIdx.x * blockDim.y + threadIdx.y;
+    if (row >= rows) return;
+    const int I = row % Hs;
+    const int cs = (row / Hs) % Cs;
+    const int n = row / (Hs * Cs);
+    const int c = cs / (s * s), a = (cs / s) % s, b = cs % s;
+    const int h = s * I + a - pH;
+    float* dst = xs + (int64_t)row * Ws;
+    const bool hin = h >= 0 && h < H;
+    const float* src = x + (((int64_t)n * C + c) * H + (hin ? h : 0)) * W;
+    for (int J = threadIdx.x; J < Ws; J += blockDim.x) {
+        const int w = s * J + b - pW;
+        dst[J] = (hin && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
     }
 }
 
@@ -52,25 +58,24 @@ __global__ void s2d_weight_kernel(const float* __restrict__ w, float* __restrict
     }
 }
 
-// gx[n][c][h][w] = gx'[n][(c, (h+pH)%s, (w+pW)%s)][(h+pH)/s][(w+pW)/s]
-__global__ void d2s_grad_kernel(const float* __restrict__ gxs, float* __restrict__ gx, int64_t N, int C,
+// gx[n][c][h][w] = gx'[n][(c, (h+pH)%s, (w+pW)%s)][(h+pH)/s][(w+pW)/s]; one gx row per
+// (blockIdx.x, threadIdx.y), threads sweep w.
+__global__ void d2s_grad_kernel(const float* __restrict__ gxs, float* __restrict__ gx, int rows, int C,
                                 int H, int W, int s, int pH, int pW, int Hs, int Ws) {
-    const int64_t total = N * C * (int64_t)H * W;
+    const int row = blockIdx.x * blockDim.y + threadIdx.y;  // (n, c, h)
+    if (row >= rows) return;
+    const int h = row % H;
+    const int c = (row / H) % C;
+    const int n = row / (H * C);
     const int Cs = C * s * s;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int w = (int)(e % W);
-        const int h = (int)((e / W) % H);
-        const int c = (int)((e / ((int64_t)W * H)) % C);
-        const int64_t n = e / ((int64_t)W * H * C);
-        const int hh = h + pH, ww = w + pW;
-        const int I = hh / s, J = ww / s;
-        float v = 0.f;  // pixels past the last output's receptive field get no gradient
-        if (I < Hs && J < Ws) {
-            const int cs = (c * s + hh % s) * s + ww % s;
-            v = __ldg(gxs + ((n * Cs + cs) * Hs + I) * (int64_t)Ws + J);
-        }
-        gx[e] = v;
+    const int hh = h + pH, I = hh / s;
+    float* dst = gx + (int64_t)row * W;
+    // pixels past the last output's receptive field get no gradient
+    const float* src = gxs + (((int64_t)n * Cs + (c * s + hh % s) * s) * Hs + I) * (int64_t)Ws;
+    const int64_t plane = (int64_t)Hs * Ws;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        const int ww = w + pW, J = ww / s;
+        dst[w] = (I < Hs && J < Ws) ? __ldg(src + (ww % s) * plane + J) : 0.f;
     }
 }
 
@@ -101,6 +106,7 @@ unsigned blocks_for(int64_t total) {
 bool s2d_applies(const Geo& g) {
     const int64_t s = g.sH;
     if (s < 2 || g.sW != s || g.C * s * s > 64 || g.kH < s || g.kW < s) return false;
+    if (g.N * g.C * g.H >= (1ll << 31)) return false;  // 32-bit row indices
     const Geo e = s2d_geo(g);
     // the regrouped filter may not inflate the contraction by more than 1.5x
     return e.CRS * 2 <= g.CRS * 3 && e.N * e.C * e.H * e.W < (1ll << 31);
@@ -116,9 +122,9 @@ Geo s2d_geo(const Geo& g) {
 void s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st) {
     const Geo e = s2d_geo(g);
     ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + e.N * e.C * e.HW));
-    s2d_input_kernel<<<blocks_for(e.N * e.C * e.HW), 256, 0, st>>>(x, xs, g.N, (int)g.C, (int)g.H, (int)g.W,
-                                                                   (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H,
-                                                                   (int)e.W);
+    const int rows = (int)(e.N * e.C * e.H);
+    s2d_input_kernel<<<(unsigned)ceil_div(rows, 4), dim3(64, 4), 0, st>>>(
+        x, xs, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H, (int)e.W);
     after_launch("s2d_input");
 }
 
@@ -132,9 +138,9 @@ void s2d_weight(const Geo& g, const float* w, float* ws, cudaStream_t st) {
 void d2s_grad(const Geo& g, const float* gxs, float* gx, cudaStream_t st) {
     const Geo e = s2d_geo(g);
     ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW * 2));
-    d2s_grad_kernel<<<blocks_for(g.N * g.C * g.HW), 256, 0, st>>>(gxs, gx, g.N, (int)g.C, (int)g.H, (int)g.W,
-                                                                  (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H,
-                                                                  (int)e.W);
+    const int rows = (int)(g.N * g.C * g.H);
+    d2s_grad_kernel<<<(unsigned)ceil_div(rows, 2), dim3(128, 2), 0, st>>>(
+        gxs, gx, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H, (int)e.W);
     after_launch("d2s_grad");
 }
 

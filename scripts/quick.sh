@@ -5,7 +5,7 @@ timeout 300 python tests/gpu_probe.py > $OUT/probe.log 2>&1; echo "probe rc=$?" 
 grep -E "ERROR|rc=|': [0-9.]+e-0[12]|': [0-9]\.[0-9]" $OUT/probe.log | head
 for envs in "$@"; do
   for wl in ${WLS:-convnet}; do
-    env $envs timeout 300 python bench.py --workload $wl --no-cpu-baseline --no-e2e > $OUT/b.json 2>$OUT/b.err
+    env $envs timeout 300 python bench.py --workload $wl --no-cpu-baseline --no-e2e $BARGS > $OUT/b.json 2>$OUT/b.err
     python -c "
 import json
 d=json.load(open('$OUT/b.json'))
