@@ -14,6 +14,8 @@
 // applies scale / accumulate and writes KCRS.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "tmap.cuh"
 #include "umma.cuh"
@@ -25,8 +27,6 @@ namespace {
 using namespace umma;
 
 constexpr int kPix = 64;                     // pixels (reduction rows) per stage
-constexpr uint32_t kBox = kPix * 128;        // one 64-pixel x 32-channel box: 8 KB
-constexpr uint32_t kStageA = 4 * kBox;       // 128 filter columns per CTA
 constexpr int kThreadsW = 192;
 constexpr int kSmemLimit = 232448;
 
@@ -35,7 +35,7 @@ struct UWgradParams {
     CUtensorMap tmap_x;   // im2col over x NHWC [N][H][W][Cp], box {32 ch, 64 px}
     int oH, oW, sH, sW, pH, pW, kW;
     int taps, Cp;
-    int m_tiles, n_tiles, splits;
+    int m_tiles, m_groups, n_tiles, splits;  // a unit covers MT consecutive m-tiles
     int kb_per_split, total_kb;
     int bn, stages;
     uint32_t stage_b, tmem_cols;
@@ -43,14 +43,21 @@ struct UWgradParams {
     int64_t part_ld, part_split;
 };
 
+// MT = 2: one unit computes two 256-column m-tiles into two accumulators from the same
+// gradOutput (B) stage — B is fetched once for both, and each stage covers 32 pixels so
+// the smem ring keeps its depth (opt-in; see wplan).
+template <int MT>
 __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_constant__ UWgradParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+    constexpr int KP = kPix / MT;             // pixels (reduction rows) per stage
+    constexpr uint32_t BOX = KP * 128;        // one KP-pixel x 32-channel box
+    constexpr uint32_t STAGE_A = MT * 4 * BOX;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + ((((raw + 1023u) & ~1023u)) - raw);
     const int S = p.stages;
     uint8_t* sA = smem;
-    uint8_t* sB = smem + (size_t)S * kStageA;
+    uint8_t* sB = smem + (size_t)S * STAGE_A;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)S * p.stage_b);
     uint64_t* empty = full + S;
     uint64_t* tfull = empty + S;
@@ -78,13 +85,13 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    const int units = p.m_tiles * p.n_tiles * p.splits;
+    const int units = p.m_groups * p.n_tiles * p.splits;
     const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
 
     // unit -> (m-tile, n-tile, split), m fastest: consecutive pairs share a pixel range
     auto decode = [&](int u, int& mt, int& nt, int& sp) {
-        mt = u % p.m_tiles;
-        const int r = u / p.m_tiles;
+        mt = (u % p.m_groups) * MT;  // first m-tile of the unit
+        const int r = u / p.m_groups;
         nt = r % p.n_tiles;
         sp = r / p.n_tiles;
     };
@@ -103,42 +110,45 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
                 int mt, nt, sp;
                 decode(u, mt, nt, sp);
                 const int nkb = kb_count(sp);
-                // this CTA's four filter-column boxes: (tap, channel block) -> (r, s, c0)
-                int bc[4], br[4], bs[4];
+                // this CTA's filter-column boxes: (tap, channel block) -> (r, s, c0), four per m-tile
+                int bc[4 * MT], br[4 * MT], bs[4 * MT];
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int col = mt * 256 + (int)rank * 128 + b * 32;
+                for (int b = 0; b < 4 * MT; ++b) {
+                    const int col = (mt + b / 4) * 256 + (int)rank * 128 + (b % 4) * 32;
                     int tap = col / p.Cp;
                     bc[b] = col - tap * p.Cp;
-                    if (tap >= p.taps) tap = 0;  // rows past the filter are never reduced
+                    if (tap >= p.taps) {  // columns past the filter are never reduced
+                        tap = 0;
+                        bc[b] = 0;
+                    }
                     br[b] = tap / p.kW;
                     bs[b] = tap - br[b] * p.kW;
                 }
                 const int kbase = nt * p.bn + (int)rank * (p.bn / 2);
                 // pixel cursor (n, i, j) of the first pixel of this split
-                int m = sp * p.kb_per_split * kPix;
+                int m = sp * p.kb_per_split * KP;
                 const int ohw = p.oH * p.oW;
                 int n = m / ohw;
                 int rem = m - n * ohw;
                 int i = rem / p.oW, j = rem - i * p.oW;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* a = sA + (size_t)stage * kStageA;
+                    uint8_t* a = sA + (size_t)stage * STAGE_A;
                     uint8_t* b = sB + (size_t)stage * p.stage_b;
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kStageA + p.stage_b));
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (STAGE_A + p.stage_b));
                     const int wc = j * p.sW - p.pW, hc = i * p.sH - p.pH;
 #pragma unroll
-                    for (int t = 0; t < 4; ++t)
-                        tma_load_im2col_4d_cg2(a + t * kBox, &p.tmap_x, &full[stage], bc[t], wc, hc, n,
+                    for (int t = 0; t < 4 * MT; ++t)
+                        tma_load_im2col_4d_cg2(a + t * BOX, &p.tmap_x, &full[stage], bc[t], wc, hc, n,
                                                (uint16_t)bs[t], (uint16_t)br[t]);
                     for (int t = 0; t < nbB; ++t)
-                        tma_load_2d_cg2(b + t * kBox, &p.tmap_gy, &full[stage], kbase + t * 32, m);
+                        tma_load_2d_cg2(b + t * BOX, &p.tmap_gy, &full[stage], kbase + t * 32, m);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
                     }
-                    m += kPix;
-                    j += kPix;
+                    m += KP;
+                    j += KP;
                     while (j >= p.oW) {
                         j -= p.oW;
                         if (++i == p.oH) {
@@ -162,20 +172,22 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
                 const uint32_t acc = it & 1;
                 mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem_base + acc * p.bn;
+                const uint32_t d = tmem_base + acc * MT * p.bn;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    // MN-major: 32-element atoms along M/N at LBO = one box (8 KB),
+                    // MN-major: 32-element atoms along M/N at LBO = one box,
                     // 4-row swizzle groups along K at SBO = 512 B; K=8 rows = +1 KB.
-                    const uint32_t alo = desc_lo(smem_u32(sA + (size_t)stage * kStageA), kBox);
-                    const uint32_t blo = desc_lo(smem_u32(sB + (size_t)stage * p.stage_b), kBox);
+                    const uint32_t alo = desc_lo(smem_u32(sA + (size_t)stage * STAGE_A), BOX);
+                    const uint32_t blo = desc_lo(smem_u32(sB + (size_t)stage * p.stage_b), BOX);
                     constexpr uint32_t kHi = desc_hi(512, kSwizzle128B_Base32B);
                     const uint32_t acc0 = kb != 0;
 #pragma unroll
-                    for (int k = 0; k < kPix / 8; ++k)
-                        mma_tf32_cg2_warp(d, desc_make(alo + k * 64, kHi), desc_make(blo + k * 64, kHi), idesc,
-                                     k ? 1u : acc0);
+                    for (int t = 0; t < MT; ++t)
+#pragma unroll
+                        for (int k = 0; k < KP / 8; ++k)
+                            mma_tf32_cg2_warp(d + t * p.bn, desc_make(alo + t * (4 * BOX >> 4) + k * 64, kHi),
+                                              desc_make(blo + k * 64, kHi), idesc, k ? 1u : acc0);
                     mma_commit_cg2_warp(&empty[stage]);
                     if (++stage == S) {
                         stage = 0;
@@ -194,19 +206,22 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
             const uint32_t acc = it & 1;
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             tc_fence_after();
-            const int row = mt * 256 + (int)rank * 128 + (int)(q * 32 + lane);
-            float* dst = p.part + (int64_t)sp * p.part_split + (int64_t)row * p.part_ld +
-                         (int64_t)nt * p.bn;
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
-            for (int c0 = 0; c0 < p.bn; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld_32x32b_x16(taddr + c0, v);
-                tmem_ld_wait();
-                float4* d4 = reinterpret_cast<float4*>(dst + c0);
+            for (int t = 0; t < MT; ++t) {
+                if (mt + t >= p.m_tiles) break;
+                const int row = (mt + t) * 256 + (int)rank * 128 + (int)(q * 32 + lane);
+                float* dst = p.part + (int64_t)sp * p.part_split + (int64_t)row * p.part_ld +
+                             (int64_t)nt * p.bn;
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + (acc * MT + t) * p.bn;
+                for (int c0 = 0; c0 < p.bn; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(taddr + c0, v);
+                    tmem_ld_wait();
+                    float4* d4 = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj)
-                    d4[jj] = make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
-                                         __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3]));
+                    for (int jj = 0; jj < 4; ++jj)
+                        d4[jj] = make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
+                                             __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3]));
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -243,9 +258,18 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
     }
 }
 
+int wgrad_mt_env() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_WGRAD_MT");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 struct WPlan {
     int64_t Cp, Kp, kdim;
-    int bn, m_tiles, n_tiles, splits, kb_per_split, total_kb, stages;
+    int mt;  // m-tiles per unit (1 or 2)
+    int bn, m_tiles, m_groups, n_tiles, splits, kb_per_split, total_kb, stages;
     int64_t x_elems, gy_elems, part_elems;
 };
 
@@ -257,15 +281,22 @@ WPlan wplan(const Geo& g) {
     w.n_tiles = (int)ceil_div(w.Kp, 256);
     w.bn = (int)(ceil_div(ceil_div(w.Kp, w.n_tiles), 64) * 64);
     w.m_tiles = (int)ceil_div(w.kdim, 256);
-    w.total_kb = (int)ceil_div(g.M, kPix);
-    const int64_t tiles = (int64_t)w.m_tiles * w.n_tiles;
+    // two m-tiles per unit can share the B stage (PT_B200_WGRAD_MT=2); measured slower on
+    // convnet L1-L3 (L2 wgrad 1.00 -> 1.42 ms: the 32-pixel boxes it needs to keep the ring
+    // depth halve the bytes per TMA request), so one m-tile per unit is the default
+    w.mt = (wgrad_mt_env() == 2 && w.bn <= 128 && w.m_tiles >= 2) ? 2 : 1;
+    w.m_groups = (int)ceil_div(w.m_tiles, w.mt);
+    const int kp = kPix / w.mt;
+    w.total_kb = (int)ceil_div(g.M, kp);
+    const int64_t tiles = (int64_t)w.m_groups * w.n_tiles;
     const int64_t target_units = 2 * (int64_t)sm_count();  // ~4 units per CTA pair
     int64_t splits = ceil_div(target_units, tiles);
     int64_t kbps = ceil_div(w.total_kb, splits);
-    if (kbps < 8) kbps = 8;  // >= 512 pixels per unit to amortise the epilogue
+    if (kbps < 8 * w.mt) kbps = 8 * w.mt;  // >= 512 pixels per unit to amortise the epilogue
     w.kb_per_split = (int)kbps;
     w.splits = (int)ceil_div(w.total_kb, kbps);
-    w.stages = (kSmemLimit - 1024 - 256) / (int)(kStageA + (w.bn / 64) * kBox);
+    const int box = kp * 128;
+    w.stages = (kSmemLimit - 1024 - 256) / (int)(w.mt * 4 * box + (w.bn / 64) * box);
     if (w.stages > 8) w.stages = 8;
     w.x_elems = g.N * g.HW * w.Cp;
     w.gy_elems = g.M * w.Kp;
@@ -315,13 +346,13 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     {
         const uint64_t dims[2] = {(uint64_t)w.Kp, (uint64_t)g.M};
         const uint64_t strides[1] = {(uint64_t)w.Kp * 4};
-        const uint32_t box[2] = {32, kPix};
+        const uint32_t box[2] = {32, (uint32_t)(kPix / w.mt)};
         tmap_tiled(&p.tmap_gy, gyh, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
     // a zero-bordered copy carries (part of) the padding itself
     const int64_t xH = g.H + 2 * xph, xW = g.W + 2 * xpw, epH = g.pH - xph, epW = g.pW - xpw;
     tmap_im2col(&p.tmap_x, xh, g.N, xH, xW, w.Cp, (int)g.kH, (int)g.kW, (int)epH, (int)epW,
-                (int)g.sH, (int)g.sW, 32, kPix, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+                (int)g.sH, (int)g.sW, 32, kPix / w.mt, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     p.oH = (int)g.oH;
     p.oW = (int)g.oW;
     p.sH = (int)g.sH;
@@ -332,23 +363,27 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     p.taps = (int)(g.kH * g.kW);
     p.Cp = (int)w.Cp;
     p.m_tiles = w.m_tiles;
+    p.m_groups = w.m_groups;
     p.n_tiles = w.n_tiles;
     p.splits = w.splits;
     p.kb_per_split = w.kb_per_split;
     p.total_kb = w.total_kb;
     p.bn = w.bn;
     p.stages = w.stages;
-    p.stage_b = (uint32_t)(w.bn / 64) * kBox;
-    p.tmem_cols = 2 * w.bn <= 256 ? 256 : 512;
+    p.stage_b = (uint32_t)(w.bn / 64) * (uint32_t)(kPix / w.mt) * 128u;
+    p.tmem_cols = 2 * w.mt * w.bn <= 256 ? 256 : 512;
     p.part = part;
     p.part_ld = (int64_t)w.n_tiles * w.bn;
     p.part_split = (int64_t)w.m_tiles * 256 * p.part_ld;
-    const size_t smem = 1024 + (size_t)p.stages * (kStageA + p.stage_b) + (2 * p.stages + 4) * 8 + 16;
-    const int units = w.m_tiles * w.n_tiles * w.splits;
+    const size_t smem = 1024 + (size_t)p.stages * (w.mt * 4 * (kPix / w.mt) * 128 + p.stage_b) +
+                        (2 * p.stages + 4) * 8 + 16;
+    const int units = w.m_groups * w.n_tiles * w.splits;
     const int pairs = std::min(units, sm_count() / 2);
     static bool attr = false;
     if (!attr) {
-        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemLimit));
+        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
         attr = true;
     }
@@ -366,7 +401,8 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     cfg.numAttrs = 1;
     {
         ProfScope prof("umma_wgrad", st, alg_flops >= 0 ? alg_flops : 2.0 * g.M * g.K * g.CRS, 0.0);
-        PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel, p));
+        if (w.mt == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<2>, p));
+        else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1>, p));
         after_launch("umma_wgrad");
     }
     const int64_t n = g.K * g.CRS;
