@@ -26,7 +26,6 @@ namespace {
 
 using namespace umma;
 
-constexpr int kPix = 64;                     // pixels (reduction rows) per stage
 constexpr int kThreadsW = 192;
 constexpr int kSmemLimit = 232448;
 
@@ -46,10 +45,9 @@ struct UWgradParams {
 // MT = 2: one unit computes two 256-column m-tiles into two accumulators from the same
 // gradOutput (B) stage — B is fetched once for both, and each stage covers 32 pixels so
 // the smem ring keeps its depth (opt-in; see wplan).
-template <int MT>
+template <int MT, int KP>  // KP: pixels (reduction rows) per stage
 __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_constant__ UWgradParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-    constexpr int KP = kPix / MT;             // pixels (reduction rows) per stage
     constexpr uint32_t BOX = KP * 128;        // one KP-pixel x 32-channel box
     constexpr uint32_t STAGE_A = MT * 4 * BOX;
     extern __shared__ uint8_t smem_raw[];
@@ -258,6 +256,18 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
     }
 }
 
+int wgrad_kp_env() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_WGRAD_KPIX");
+        // 128-pixel boxes: the kernel is bound by TMA requests more than bytes (64 -> 128
+        // pixels per box: convnet L2 wgrad 0.99 -> 0.89 ms, L3 0.37 -> 0.32 ms), even though
+        // the 96 KB stages leave a 2-deep ring
+        const int k = e ? std::atoi(e) : 128;
+        return k == 64 ? 64 : 128;
+    }();
+    return v;
+}
+
 int wgrad_mt_env() {
     static const int v = [] {
         const char* e = std::getenv("PT_B200_WGRAD_MT");
@@ -269,6 +279,7 @@ int wgrad_mt_env() {
 struct WPlan {
     int64_t Cp, Kp, kdim;
     int mt;  // m-tiles per unit (1 or 2)
+    int kp;  // pixels per pipeline stage
     int bn, m_tiles, m_groups, n_tiles, splits, kb_per_split, total_kb, stages;
     int64_t x_elems, gy_elems, part_elems;
 };
@@ -285,8 +296,9 @@ WPlan wplan(const Geo& g) {
     // convnet L1-L3 (L2 wgrad 1.00 -> 1.42 ms: the 32-pixel boxes it needs to keep the ring
     // depth halve the bytes per TMA request), so one m-tile per unit is the default
     w.mt = (wgrad_mt_env() == 2 && w.bn <= 128 && w.m_tiles >= 2) ? 2 : 1;
+    w.kp = w.mt == 2 ? 32 : wgrad_kp_env();
     w.m_groups = (int)ceil_div(w.m_tiles, w.mt);
-    const int kp = kPix / w.mt;
+    const int kp = w.kp;
     w.total_kb = (int)ceil_div(g.M, kp);
     const int64_t tiles = (int64_t)w.m_groups * w.n_tiles;
     const int64_t target_units = 2 * (int64_t)sm_count();  // ~4 units per CTA pair
@@ -346,13 +358,13 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     {
         const uint64_t dims[2] = {(uint64_t)w.Kp, (uint64_t)g.M};
         const uint64_t strides[1] = {(uint64_t)w.Kp * 4};
-        const uint32_t box[2] = {32, (uint32_t)(kPix / w.mt)};
+        const uint32_t box[2] = {32, (uint32_t)w.kp};
         tmap_tiled(&p.tmap_gy, gyh, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
     // a zero-bordered copy carries (part of) the padding itself
     const int64_t xH = g.H + 2 * xph, xW = g.W + 2 * xpw, epH = g.pH - xph, epW = g.pW - xpw;
     tmap_im2col(&p.tmap_x, xh, g.N, xH, xW, w.Cp, (int)g.kH, (int)g.kW, (int)epH, (int)epW,
-                (int)g.sH, (int)g.sW, 32, kPix / w.mt, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+                (int)g.sH, (int)g.sW, 32, w.kp, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     p.oH = (int)g.oH;
     p.oW = (int)g.oW;
     p.sH = (int)g.sH;
@@ -370,20 +382,22 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     p.total_kb = w.total_kb;
     p.bn = w.bn;
     p.stages = w.stages;
-    p.stage_b = (uint32_t)(w.bn / 64) * (uint32_t)(kPix / w.mt) * 128u;
+    p.stage_b = (uint32_t)(w.bn / 64) * (uint32_t)w.kp * 128u;
     p.tmem_cols = 2 * w.mt * w.bn <= 256 ? 256 : 512;
     p.part = part;
     p.part_ld = (int64_t)w.n_tiles * w.bn;
     p.part_split = (int64_t)w.m_tiles * 256 * p.part_ld;
-    const size_t smem = 1024 + (size_t)p.stages * (w.mt * 4 * (kPix / w.mt) * 128 + p.stage_b) +
+    const size_t smem = 1024 + (size_t)p.stages * (w.mt * 4 * w.kp * 128 + p.stage_b) +
                         (2 * p.stages + 4) * 8 + 16;
     const int units = w.m_groups * w.n_tiles * w.splits;
     const int pairs = std::min(units, sm_count() / 2);
     static bool attr = false;
     if (!attr) {
-        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
-        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kSmemLimit));
+        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
         attr = true;
     }
@@ -401,8 +415,9 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     cfg.numAttrs = 1;
     {
         ProfScope prof("umma_wgrad", st, alg_flops >= 0 ? alg_flops : 2.0 * g.M * g.K * g.CRS, 0.0);
-        if (w.mt == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<2>, p));
-        else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1>, p));
+        if (w.mt == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<2, 32>, p));
+        else if (w.kp == 128) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1, 128>, p));
+        else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1, 64>, p));
         after_launch("umma_wgrad");
     }
     const int64_t n = g.K * g.CRS;
