@@ -74,7 +74,9 @@ void tmap_tiled(CUtensorMap* m, const float* base, int rank, const uint64_t* dim
         e[i] = 1;
         if (i + 1 < rank) s[i] = strides_bytes[i];
     }
-    bytes = (size_t)dims[rank - 1] * (rank > 1 ? strides_bytes[rank - 2] : 4);
+    // footprint of the whole view (strides need not be monotone, e.g. a channel-block dim)
+    bytes = (size_t)dims[0] * 4;
+    for (int i = 1; i < rank; ++i) bytes += (size_t)(dims[i] - 1) * strides_bytes[i - 1];
     CUresult r = g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(base), d, s,
                                 b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

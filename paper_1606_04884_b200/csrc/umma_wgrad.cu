@@ -103,7 +103,6 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const int nbB = p.bn / 64;  // gy boxes per CTA
             for (int u = cluster; u < units; u += nclusters) {
                 int mt, nt, sp;
                 decode(u, mt, nt, sp);
@@ -139,8 +138,8 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
                     for (int t = 0; t < 4 * MT; ++t)
                         tma_load_im2col_4d_cg2(a + t * BOX, &p.tmap_x, &full[stage], bc[t], wc, hc, n,
                                                (uint16_t)bs[t], (uint16_t)br[t]);
-                    for (int t = 0; t < nbB; ++t)
-                        tma_load_2d_cg2(b + t * BOX, &p.tmap_gy, &full[stage], kbase + t * 32, m);
+                    // all of this CTA's gy channel boxes in one 3-D request: {32 ch, KP px, nbB}
+                    tma_load_3d_cg2(b, &p.tmap_gy, &full[stage], 0, m, kbase / 32);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -356,10 +355,12 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     UWgradParams p;
     memset(&p, 0, sizeof p);
     {
-        const uint64_t dims[2] = {(uint64_t)w.Kp, (uint64_t)g.M};
-        const uint64_t strides[1] = {(uint64_t)w.Kp * 4};
-        const uint32_t box[2] = {32, (uint32_t)w.kp};
-        tmap_tiled(&p.tmap_gy, gyh, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        // gy NHWC [M][Kp] viewed as {32 ch, M px, Kp/32 channel blocks} so one box carries
+        // every 32-channel block a CTA needs, laid out [block][px][32] as the MMA expects
+        const uint64_t dims[3] = {32, (uint64_t)g.M, (uint64_t)(w.Kp / 32)};
+        const uint64_t strides[2] = {(uint64_t)w.Kp * 4, 128};
+        const uint32_t box[3] = {32, (uint32_t)w.kp, (uint32_t)(w.bn / 64)};
+        tmap_tiled(&p.tmap_gy, gyh, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
     // a zero-bordered copy carries (part of) the padding itself
     const int64_t xH = g.H + 2 * xph, xW = g.W + 2 * xpw, epH = g.pH - xph, epW = g.pW - xpw;
