@@ -133,10 +133,9 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                     for (int cc = 0; cc < p.chunks; cc += CPS) {
                         mbar_wait(&aempty[as], aph ^ 1);
                         if (leader) mbar_arrive_expect_tx(&afull[as], atx);
-#pragma unroll
-                        for (int c = 0; c < CPS; ++c)
-                            tma_load_2d_cg2(sA + (size_t)as * p.stage_a + c * p.box_a, &p.tmap_a, &afull[as],
-                                            (cc + c) * 32, (int)(pix0 + (int64_t)r * p.Wp));
+                        // one 3-D request for the CPS chunk runs: {32 ch, rbox px, CPS chunks}
+                        tma_load_3d_cg2(sA + (size_t)as * p.stage_a, &p.tmap_a, &afull[as], 0,
+                                        (int)(pix0 + (int64_t)r * p.Wp), cc);
                         if (++as == p.sa) {
                             as = 0;
                             aph ^= 1;
@@ -147,10 +146,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             // PAIR: this CTA's tap is s + rank (past the row: the zero tap)
                             const int tap = PAIR ? (s + (int)rank < p.kW ? r * p.kW + s + (int)rank : p.zero_tap)
                                                  : r * p.kW + s;
-#pragma unroll
-                            for (int c = 0; c < CPS; ++c)
-                                tma_load_2d_cg2(sB + (size_t)bs * p.stage_b + c * p.box_b, &p.tmap_b, &bfull[bs],
-                                                tap * p.cin_p + (cc + c) * 32, brow);
+                            tma_load_3d_cg2(sB + (size_t)bs * p.stage_b, &p.tmap_b, &bfull[bs], 0, brow,
+                                            tap * (p.cin_p / 32) + cc);
                             if (++bs == p.sb) {
                                 bs = 0;
                                 bph ^= 1;
@@ -308,18 +305,21 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     const int64_t npx = N * Hp * Wp;
     PTB_REQUIRE(npx < (1ll << 31), "hconv: activation too large");
     {
-        const uint64_t dims[2] = {(uint64_t)pl.cin_p, (uint64_t)npx};
-        const uint64_t strides[1] = {(uint64_t)pl.cin_p * 4};
-        const uint32_t box[2] = {32, (uint32_t)rbox};
-        tmap_tiled(&p.tmap_a, act, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        // {32 ch, pixels, 32-channel chunks}: one box = the CPS chunk runs of a stage
+        const uint64_t dims[3] = {32, (uint64_t)npx, (uint64_t)(pl.cin_p / 32)};
+        const uint64_t strides[2] = {(uint64_t)pl.cin_p * 4, 128};
+        const uint32_t box[3] = {32, (uint32_t)rbox, (uint32_t)(pl.cin_p / 32 % 2 == 0 ? 2 : 1)};
+        tmap_tiled(&p.tmap_a, act, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
     const bool pair = pl.tap_pair;
     {
+        // {32, weight rows, 32-wide k blocks}: one box = the CPS chunks of one tap
         const uint64_t kdim = (uint64_t)pl.kdim;
-        const uint64_t dims[2] = {kdim, (uint64_t)pl.n_pad};
-        const uint64_t strides[1] = {kdim * 4};
-        const uint32_t box[2] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2)};
-        tmap_tiled(&p.tmap_b, wt, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        const uint64_t dims[3] = {32, (uint64_t)pl.n_pad, kdim / 32};
+        const uint64_t strides[2] = {kdim * 4, 128};
+        const uint32_t box[3] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2),
+                                 (uint32_t)(pl.cin_p / 32 % 2 == 0 ? 2 : 1)};
+        tmap_tiled(&p.tmap_b, wt, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
     p.span = pair ? 254 : 256;
     p.zero_tap = (int)pl.taps;
