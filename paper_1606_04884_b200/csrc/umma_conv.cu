@@ -81,7 +81,10 @@ struct KCursor {
     }
 };
 
-template <int CB, int CG>
+// SPS: (tap, 32-channel chunk) slots per pipeline stage on the CTA-pair path (2 or 4).
+// Four slots (K = 128 per stage) halve the barrier round trips per MMA and keep more
+// bytes per request in flight; used when two such stages fit in shared memory.
+template <int CB, int CG, int SPS = 2>
 __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_constant__ UConvParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     static_assert(CG == 1 || CB == 32, "CTA pairs only on the SW128 path");
@@ -151,14 +154,14 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
                     if constexpr (CG == 2) {
                         if (leader) mbar_arrive_expect_tx(&full[stage], tx);
 #pragma unroll
-                        for (int t = 0; t < 2; ++t) {
-                            // past the last k-slot: any valid tap (the weights there are 0)
+                        for (int t = 0; t < SPS; ++t) {
+                            // past the last k-slot: any valid tap (the weights there are 0 / OOB)
                             const bool live = slot < p.slots;
                             tma_load_im2col_4d_cg2(a + t * kBoxA, &p.tmap_a, &full[stage],
                                                    live ? kc.cc * 32 : 0, wc, hc, n0,
                                                    (uint16_t)(live ? kc.s : 0),
                                                    (uint16_t)(live ? kc.r : 0));
-                            tma_load_2d_cg2(b + t * (p.stage_b / 2), &p.tmap_b, &full[stage],
+                            tma_load_2d_cg2(b + t * (p.stage_b / SPS), &p.tmap_b, &full[stage],
                                             slot * 32, brow);
                             ++slot;
                             kc.next(p.chunks, p.kW);
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
             // ===== MMA issuer =====
             const uint32_t idesc = idesc_tf32(kTileMC, p.bn, 0, 0);
             constexpr uint32_t kHiSW128 = desc_hi(1024, kSwizzle128B), kHiNone = desc_hi(128, kSwizzleNone);
-            const uint32_t bhalf16 = (p.stage_b / 2) >> 4;      // CG=2: second box of B
+            const uint32_t bhalf16 = (p.stage_b / SPS) >> 4;    // CG=2: next slot's box of B
             const uint32_t bstep4 = (uint32_t)(2 * p.bn * 16) >> 4;  // CB=4: next K=8 slab of B
             int stage = 0;
             uint32_t phase = 0;
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
                     if constexpr (CG == 2) {
                         const uint32_t alo = desc_lo(a, 16), blo = desc_lo(b, 16);
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) {
+                        for (int k = 0; k < 4 * SPS; ++k) {
                             const uint32_t ao = ((k >> 2) * kBoxA + (k & 3) * 32) >> 4;
                             const uint32_t bo = (k >> 2) * bhalf16 + (uint32_t)(k & 3) * 2u;
                             mma_tf32_cg2_warp(d, desc_make(alo + ao, kHiSW128), desc_make(blo + bo, kHiSW128),
@@ -288,6 +291,14 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
 }
 
 // ---- host ----
+int conv_sps_env() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_CONV_SPS");
+        return e ? std::atoi(e) : 2;  // 4 measured slower (convnet L3 fwd 0.255 -> 0.299 ms)
+    }();
+    return v;
+}
+
 uint32_t tmem_cols_for(int bn) {
     const int need = 2 * bn;
     uint32_t c = 32;
@@ -295,11 +306,11 @@ uint32_t tmem_cols_for(int bn) {
     return c;
 }
 
-template <int CB, int CG>
+template <int CB, int CG, int SPS = 2>
 void launch_k(const UConvParams& p, int grid, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        PTB_CUDA(cudaFuncSetAttribute(umma_conv_kernel<CB, CG>,
+        PTB_CUDA(cudaFuncSetAttribute(umma_conv_kernel<CB, CG, SPS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
         attr = true;
     }
@@ -315,7 +326,7 @@ void launch_k(const UConvParams& p, int grid, size_t smem, cudaStream_t st) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_conv_kernel<CB, CG>, p));
+    PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_conv_kernel<CB, CG, SPS>, p));
 }
 
 void encode_weights(CUtensorMap* m, const float* wt, const UmmaPlan& pl) {
@@ -355,14 +366,19 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
     p.kW = kW;
     p.chunks = (int)(pl.cin_p / pl.cb);
     p.slots = (int)(pl.taps * p.chunks);
-    const int slots_per_stage = pl.cb == 32 ? pl.cg : 8;
+    // CTA pairs: 4 slots per stage when two such stages fit (see umma_conv_kernel)
+    const uint32_t b_slot = (uint32_t)(pl.bn / 2) * 128u;
+    const int sps = (pl.cb == 32 && pl.cg == 2)
+                        ? ((conv_sps_env() == 4 && 2 * 4 * (kBoxA + b_slot) <= (uint32_t)kSmemLimit - 2048) ? 4 : 2)
+                        : 0;
+    const int slots_per_stage = pl.cb == 32 ? (pl.cg == 2 ? sps : 1) : 8;
     p.num_kb = (int)ceil_div(p.slots, slots_per_stage);
     p.n_rows = (int)pl.n_rows;
     p.bn = pl.bn;
     p.n_tiles = pl.n_tiles;
     p.m_tiles = (int)ceil_div(M, (int64_t)kTileM * pl.cg);
-    p.stage_a = pl.cb == 32 ? kBoxA * pl.cg : kBoxA;  // CG=2: two 32-deep boxes per stage
-    p.stage_b = pl.cb == 32 ? (uint32_t)(pl.bn / pl.cg) * 128u * pl.cg : (uint32_t)pl.bn * 128u;
+    p.stage_a = pl.cb == 32 ? kBoxA * slots_per_stage : kBoxA;  // CG=2: sps 32-deep boxes per stage
+    p.stage_b = pl.cb == 32 ? (uint32_t)(pl.bn / pl.cg) * 128u * slots_per_stage : (uint32_t)pl.bn * 128u;
     int s = (kSmemLimit - 1024 - 256) / (int)(p.stage_a + p.stage_b);
     p.stages = s > 8 ? 8 : s;
     p.tmem_cols = tmem_cols_for(pl.bn);
@@ -375,6 +391,7 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
     const int clusters = std::min(num_tiles, sm_count() / pl.cg);
     ProfScope prof("umma_conv", st, alg_flops, 0.0);
     if (pl.cb == 4) launch_k<4, 1>(p, clusters, smem, st);
+    else if (pl.cg == 2 && sps == 4) launch_k<32, 2, 4>(p, 2 * clusters, smem, st);
     else if (pl.cg == 2) launch_k<32, 2>(p, 2 * clusters, smem, st);
     else launch_k<32, 1>(p, clusters, smem, st);
     after_launch("umma_conv");
