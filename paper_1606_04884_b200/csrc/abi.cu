@@ -93,8 +93,7 @@ void bwd_data_impl(const Geo& g, const float* gy, const float* w, float* gx, int
     if (math == PT_MATH_TF32) {
         const UmmaPlan pl = umma_plan(g, true);
         if (pl.ok) {
-            const bool same_layout =
-                pl.cb == 32 && pl.cin_p == umma_wgrad_kp(g) && pl.hankel == pre_padded;
+            const bool same_layout = pl.cb == 32 && pl.cin_p == umma_wgrad_kp(g);
             umma_conv_bwd_data(g, pl, gy, w, gx, ws, st, same_layout ? gyh_pre : nullptr);
             return;
         }
@@ -174,8 +173,8 @@ size_t finput_layout(const Geo& g, int math, int64_t* ph = nullptr, int64_t* pw 
         return 0;
     const UmmaPlan pl = umma_plan(g, false);
     if (!pl.ok || pl.cb != 32 || pl.cin_p != (g.C + 31) / 32 * 32) return 0;
-    if (ph) *ph = pl.hankel ? pl.aph : 0;
-    if (pw) *pw = pl.hankel ? pl.apw : 0;
+    if (ph) *ph = 0;  // every engine keeps x dense (a Hankel border is TMA out-of-bounds fill)
+    if (pw) *pw = 0;
     return align_up((size_t)pl.act_elems * 4, 256);
 }
 
@@ -248,32 +247,13 @@ void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, flo
             float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
             char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
             char* wws = dws + align_up(bwd_data_ws(g, math), 256);
-            // a Hankel dgrad reads gy zero-bordered: the same pass writes that copy too
-            // (placed where that engine keeps its activation copy inside the dgrad workspace)
-            NhwcDst dpad{};
-            {
-                UmmaPlan dpl;
-                size_t off = 0;
-                if (dgrad_row(g, math)) {
-                    rowdgrad_ok(g, &dpl);
-                    off = rowdgrad_act_offset(g);
-                } else {
-                    dpl = umma_plan(g, true);
-                }
-                if (dpl.ok && dpl.hankel && dpl.cin_p == umma_wgrad_kp(g))
-                    dpad = NhwcDst::padded(reinterpret_cast<float*>(dws + off), g.oH, g.oW, dpl.aph,
-                                           dpl.apw);
-            }
             {
                 PassScope pass("bwd");
-                ProfScope prof("layout", st, 0.0,
-                               4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g) +
-                                      (dpad.p ? g.N * dpad.img * umma_wgrad_kp(g) : 0)));
-                nchw_to_nhwc_padded(gy, NhwcDst::dense(gyh, g.oHW), dpad, g.N, g.K, g.oH, g.oW,
-                                    umma_wgrad_kp(g), gb, scale, accumulate, part, st);
+                ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
+                nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate, part,
+                                  st);
             }
-            if (dpad.p) bwd_data_impl(g, gy, w, gx, math, dws, st, dpad.p, true);
-            else bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
+            bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
             if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, st, finput, fph, fpw);
             else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st, finput, fph, fpw);
             return;

@@ -82,8 +82,8 @@ struct UmmaPlan {
     int64_t n_pad = 0;    // n_tiles * bn
     int64_t act_elems = 0, wt_elems = 0;  // workspace floats
     size_t ws_bytes = 0;
-    // Hankel pixel-run engine (umma_hconv.cu): stride 1, 32-channel chunks, CTA pair.
-    // The activation is then stored zero-bordered: [N][aHp][aWp][cin_p], border (aph, apw).
+    // Hankel pixel-run engine (umma_hconv.cu): stride 1, 32-channel chunks, CTA pair. The
+    // activation stays dense NHWC; the (aph, apw) border is TMA out-of-bounds fill.
     bool hankel = false;
     int64_t aH = 0, aW = 0, aph = 0, apw = 0, aHp = 0, aWp = 0;
     // <= 64 output rows: pair taps (s, s+1) in one N = 2*bn MMA (umma_hconv.cu); the packed
@@ -95,11 +95,12 @@ struct HConvTiling {
     int64_t P_img = 0;  // positions per image
     int64_t tiles = 0;  // 256-position pair tiles
 };
-HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH, int64_t span = 256);
-// act: zero-bordered NHWC [N][Hp][Wp][cin_p]; stride-1 kH x kW conv -> oH x oW NCHW.
-void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, int64_t Hp,
-               int64_t Wp, int kH, int kW, int64_t oH, int64_t oW, float* out, const float* bias,
-               double alg_flops, cudaStream_t st);
+HConvTiling hconv_tiling(int64_t N, int64_t Wp, int64_t oH, int64_t cta_span = 128);
+// act: dense NHWC [N][aH][aW][cin_p]; the (aph, apw) zero border comes from TMA
+// out-of-bounds fill. Stride-1 kH x kW conv -> oH x oW NCHW.
+void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, int64_t aH,
+               int64_t aW, int64_t aph, int64_t apw, int kH, int kW, int64_t oH, int64_t oW,
+               float* out, const float* bias, double alg_flops, cudaStream_t st);
 // fprop: act = x (C channels, HxW), n_rows = K.
 // dgrad, kDgradTconv: act = gy (K channels, oHxoW), n_rows = C, flipped weights,
 //   pad' = k-1-pad (stride 1).  kDgradGcol (small C / strided): gcol = W^T gy as a

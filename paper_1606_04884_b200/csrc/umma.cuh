@@ -206,6 +206,14 @@ __device__ __forceinline__ void tma_load_3d_cg2(void* dst, const void* tmap, uin
         "l"(tmap), "r"(leader_bar(bar)), "r"(x), "r"(y), "r"(z)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_cg2(void* dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                                int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(leader_bar(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_im2col_4d_cg2(void* dst, const void* tmap, uint64_t* bar, int c,
                                                        int w, int h, int n, uint16_t off_w,
                                                        uint16_t off_h) {

@@ -452,11 +452,12 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
                  int64_t oH, int64_t oW) {
     if (pl.cb != 32 || pl.cg != 2 || kW < 3 || kW > 120 || hconv_env() == 0) return;
     const int64_t Hp = aH + 2 * ph, Wp = aW + 2 * pw;
-    if (N * Hp * Wp >= (1ll << 31)) return;
+    if (Wp > 256 || N * aH * aW >= (1ll << 31)) return;  // a padded row is one TMA box dimension
     // efficiency from the geometry alone (not N) so a batch and its per-image slices
-    // always take the same engine (batched == per-image bitwise)
-    const double eff = (double)(oH * oW) /
-                       (double)std::min(Hp * Wp, ceil_div(oH * Wp, 256) * 256);
+    // always take the same engine (batched == per-image bitwise): each image's
+    // rows split into two halves walked in 128-position CTA runs
+    const int64_t R = (oH + 1) / 2;
+    const double eff = (double)(oH * oW) / (double)(2 * ceil_div(R * Wp, 128) * 128);
     // measured (convnet L2/L3/L5): the pixel-run kernel wins at >= 0.85 of positions valid,
     // ties near 0.8 and loses below, where the im2col kernel's zero waste pays for its
     // L2->SM traffic
@@ -480,7 +481,7 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
     pl.apw = pw;
     pl.aHp = Hp;
     pl.aWp = Wp;
-    pl.act_elems = N * Hp * Wp * pl.cin_p;
+    pl.act_elems = N * aH * aW * pl.cin_p;  // dense: the border is TMA out-of-bounds fill
 }
 
 }  // namespace
@@ -538,24 +539,17 @@ void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float
                    const float* b, float* y, void* ws, cudaStream_t st, float* act_out) {
     float* act = act_out ? act_out : reinterpret_cast<float*>(ws);
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
-    if (pl.hankel) {
-        {
-            ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + pl.act_elems));
-            nchw_to_nhwc_padded(x, NhwcDst::padded(act, g.H, g.W, g.pH, g.pW), NhwcDst{}, g.N, g.C,
-                                g.H, g.W, pl.cin_p, nullptr, 1.f, 0, nullptr, st);
-        }
-        pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackFprop, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
-                     pl.wt_elems, true, st);
-        run_hconv(pl, act, wt, g.N, pl.aHp, pl.aWp, (int)g.kH, (int)g.kW, g.oH, g.oW, y, b,
-                  2.0 * g.M * g.K * g.CRS, st);
-        return;
-    }
     {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + g.N * g.HW * pl.cin_p));
         nchw_to_nhwc(x, act, g.N, g.C, g.HW, pl.cin_p, true, st);
     }
     pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackFprop, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
                  pl.wt_elems, true, st);
+    if (pl.hankel) {
+        run_hconv(pl, act, wt, g.N, g.H, g.W, g.pH, g.pW, (int)g.kH, (int)g.kW, g.oH, g.oW, y, b,
+                  2.0 * g.M * g.K * g.CRS, st);
+        return;
+    }
     run_umma(pl, act, wt, g.N, g.H, g.W, (int)g.kH, (int)g.kW, (int)g.pH, (int)g.pW, (int)g.sH,
              (int)g.sW, g.oH, g.oW, y, b, 2.0 * g.M * g.K * g.CRS, st);
 }
@@ -567,10 +561,6 @@ void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
     if (gyh_pre) {
         act = const_cast<float*>(gyh_pre);
-    } else if (pl.hankel) {
-        ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.K * g.oHW + pl.act_elems));
-        nchw_to_nhwc_padded(gy, NhwcDst::padded(act, g.oH, g.oW, pl.aph, pl.apw), NhwcDst{}, g.N, g.K,
-                            g.oH, g.oW, pl.cin_p, nullptr, 1.f, 0, nullptr, st);
     } else {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.K * g.oHW + g.N * g.oHW * pl.cin_p));
         nchw_to_nhwc(gy, act, g.N, g.K, g.oHW, pl.cin_p, true, st);
@@ -578,8 +568,8 @@ void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const
     if (pl.hankel) {
         pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackDgradFlip, pl.cb, pl.n_pad, pl.cin_p,
                      pl.slots_p, pl.wt_elems, true, st);
-        run_hconv(pl, act, wt, g.N, pl.aHp, pl.aWp, (int)g.kH, (int)g.kW, g.H, g.W, gx, nullptr,
-                  alg_flops, st);
+        run_hconv(pl, act, wt, g.N, g.oH, g.oW, pl.aph, pl.apw, (int)g.kH, (int)g.kW, g.H, g.W, gx,
+                  nullptr, alg_flops, st);
         return;
     }
     if (pl.mode == UmmaPlan::kDgradTconv) {

@@ -45,14 +45,18 @@ constexpr int kThreadsH = 192;
 constexpr int kSmemLimitH = 232448;
 
 struct HConvParams {
-    CUtensorMap tmap_a;  // act, 2-D: {Cp, N*Hp*Wp}, box {32, rbox}, SW128
-    CUtensorMap tmap_b;  // packed weights, 2-D: {kdim, n_pad}, box {32, BN/2}, SW128
-    int N, Hp, Wp, kH, kW, chunks, cin_p;
+    CUtensorMap tmap_a;  // act NHWC [N][aH][aW][Cp], 5-D {32, aW, aH, N, Cp/32}, box {32, Wp, NR, 1, CPS}
+    CUtensorMap tmap_a2; // same with NR - 1 rows: runs starting early in a row need one row less
+    CUtensorMap tmap_b;  // packed weights, 3-D {32, n_pad, kdim/32}, box {32, rows, CPS}, SW128
+    int N, kH, kW, chunks, cin_p;
+    int aph, apw;        // zero border the TMA out-of-bounds fill supplies (top, left)
+    int Wp;              // padded row width = position-space row stride
     int oH, oW;          // valid output extent
-    int64_t P_img;       // positions per image in the tiling
-    int64_t img_px;      // Hp*Wp
-    int tiles;           // pair tiles of `span` positions
-    int span;            // positions per pair tile: 256, or 254 with tap pairing
+    int R;               // rows per image half: CTA 0 covers rows [0, R), CTA 1 rows [R, 2R)
+    int m;               // positions per half = R * Wp
+    int tpi;             // pair tiles per image
+    int nr_split;        // runs starting at column < nr_split fit NR - 1 rows
+    int tiles;           // N * tpi
     int zero_tap;        // PAIR: packed-weight tap index holding zeros (odd kW)
     int n_rows, bn, n_tiles;
     int sa, sb;          // ring depths
@@ -93,6 +97,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     const bool leader = rank == 0;
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.tmap_a);
+        tma_prefetch(&p.tmap_a2);
         tma_prefetch(&p.tmap_b);
         for (int i = 0; i < p.sa; ++i) {
             mbar_init(&afull[i], 1);  // armed by the leader only
@@ -125,17 +130,26 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             const uint32_t atx = 2 * p.stage_a, btx = 2 * p.stage_b;
             for (int u = cid; u < num_units; u += ncl) {
                 const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
-                const int64_t g0 = (int64_t)t * p.span + (int64_t)rank * kCtaSpan;
-                const int64_t n = g0 / p.P_img;
-                const int64_t pix0 = n * p.img_px + (g0 - n * p.P_img);
+                // image half `rank`, offset qh inside it; both CTAs share the column w0
+                const int n = t / p.tpi, qh = (t - n * p.tpi) * kCtaSpan;
+                const int row0 = (int)rank * p.R + qh / p.Wp;
+                // both CTAs share the start column, hence the row count and the byte count
+                const bool short_run = qh % p.Wp < p.nr_split;
+                const CUtensorMap* amap = short_run ? &p.tmap_a2 : &p.tmap_a;
+                const uint32_t atx_t = short_run ? atx - 2 * (uint32_t)CPS * (uint32_t)p.Wp * 128u : atx;
                 const int brow = PAIR ? 0 : nt * p.bn + (int)rank * (p.bn / 2);
                 for (int r = 0; r < p.kH; ++r) {
                     for (int cc = 0; cc < p.chunks; cc += CPS) {
                         mbar_wait(&aempty[as], aph ^ 1);
-                        if (leader) mbar_arrive_expect_tx(&afull[as], atx);
-                        // one 3-D request for the CPS chunk runs: {32 ch, rbox px, CPS chunks}
-                        tma_load_3d_cg2(sA + (size_t)as * p.stage_a, &p.tmap_a, &afull[as], 0,
-                                        (int)(pix0 + (int64_t)r * p.Wp), cc);
+                        if (leader) mbar_arrive_expect_tx(&afull[as], atx_t);
+                        // NR full padded rows from the dense NHWC tensor (out-of-bounds = the zero
+                        // border) for the CPS chunks: {32 ch, Wp px, NR rows, 1, CPS}
+                        // (one request per chunk: the short map's smaller box would change the
+                        // chunk stride inside a multi-chunk box)
+#pragma unroll
+                        for (int c = 0; c < CPS; ++c)
+                            tma_load_5d_cg2(sA + (size_t)as * p.stage_a + c * p.box_a, amap, &afull[as], 0,
+                                            -p.apw, row0 + r - p.aph, n, cc + c);
                         if (++as == p.sa) {
                             as = 0;
                             aph ^= 1;
@@ -170,6 +184,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * (PAIR ? 2 * p.bn : p.bn);
+                const int t = u / p.n_tiles;
+                const uint32_t w0 = (uint32_t)(((t % p.tpi) * kCtaSpan) % p.Wp);  // run start column
                 uint32_t accum = 0;
                 const uint32_t box_a16 = p.box_a >> 4, box_b16 = p.box_b >> 4;
                 for (int r = 0; r < p.kH; ++r) {
@@ -181,8 +197,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             if (p.exp != 4 || s == 0) mbar_wait(&bfull[bs], bph);
                             tc_fence_after();
                             // tap s: the same pixel run, s rows (s*128 B) further in
-                            const uint32_t a_s = alo + (p.exp == 2 ? 0u : p.exp == 3 ? (uint32_t)(s & ~7) * 8u
-                                                                                   : (uint32_t)s * 8u);
+                            const uint32_t a_s = alo + (w0 + (uint32_t)s) * 8u;
                             const uint32_t blo = desc_lo(smem_u32(sB + (size_t)bs * p.stage_b), 16);
 #pragma unroll
                             for (int k = 0; k < 4 * CPS; ++k) {
@@ -217,13 +232,12 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             tc_fence_after();
             const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
-            const int64_t gpos = (int64_t)t * p.span + (int64_t)rank * kCtaSpan + q * 32 + lane;
-            const int64_t n = gpos / p.P_img;
-            const int64_t qq = gpos - n * p.P_img;
-            const int64_t i = qq / p.Wp, j = qq - i * p.Wp;
-            const bool valid = n < p.N && i < p.oH && j < p.oW && (!PAIR || q * 32 + lane < 127);
+            const int n = t / p.tpi;
+            const int qq = (t - n * p.tpi) * kCtaSpan + (int)(q * 32 + lane);  // position in the half
+            const int i = (int)rank * p.R + qq / p.Wp, j = qq % p.Wp;
+            const bool valid = qq < p.m && i < p.oH && j < p.oW && (!PAIR || q * 32 + lane < 127);
             const int ch0 = nt * p.bn;
-            const int64_t base = (n * p.n_rows + ch0) * ohw + i * p.oW + j;
+            const int64_t base = ((int64_t)n * p.n_rows + ch0) * ohw + (int64_t)i * p.oW + j;
             if constexpr (!PAIR) {
                 const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
                 store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base : 0), ohw, p.bias, ch0,
@@ -278,76 +292,82 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
 
 }  // namespace
 
-// Tiling of the position space: per image vs flat, whichever computes fewer positions.
-HConvTiling hconv_tiling(int64_t N, int64_t Hp, int64_t Wp, int64_t oH, int64_t span) {
+// Tiling: each image's output rows are split into two halves of R rows; CTA 0 of a pair
+// walks the top half and CTA 1 the bottom half at the same offset, so both CTAs' pixel
+// runs start at the same column and one shared descriptor addresses both.
+HConvTiling hconv_tiling(int64_t N, int64_t Wp, int64_t oH, int64_t cta_span) {
     HConvTiling t;
-    const int64_t per_img = ceil_div(oH * Wp, span) * span;
-    const int64_t tiles_img = N * per_img / span;
-    const int64_t tiles_flat = ceil_div((N - 1) * Hp * Wp + oH * Wp, span);
-    if (tiles_flat < tiles_img) {
-        t.P_img = Hp * Wp;
-        t.tiles = tiles_flat;
-    } else {
-        t.P_img = per_img;
-        t.tiles = tiles_img;
-    }
+    const int64_t R = (oH + 1) / 2;
+    t.P_img = R * Wp;                                // positions per half
+    t.tiles = N * ceil_div(t.P_img, cta_span);       // pair tiles
     return t;
 }
 
-void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, int64_t Hp,
-               int64_t Wp, int kH, int kW, int64_t oH, int64_t oW, float* out, const float* bias,
-               double alg_flops, cudaStream_t st) {
+void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, int64_t aH,
+               int64_t aW, int64_t aph, int64_t apw, int kH, int kW, int64_t oH, int64_t oW,
+               float* out, const float* bias, double alg_flops, cudaStream_t st) {
     PTB_REQUIRE(pl.cb == 32 && pl.cg == 2, "hconv: needs the 32-channel CTA-pair plan");
-    PTB_REQUIRE(kW <= 120, "hconv: filter too wide for one pixel-run box");
+    const int64_t Wp = aW + 2 * apw;
+    PTB_REQUIRE(Wp <= 256 && kW <= 120, "hconv: padded row too wide for one TMA box");
+    const bool pair = pl.tap_pair;
+    const int cta_span = pair ? 127 : 128;
+    // rows a CTA's run (128 + kW - 1 positions from any column) can touch
+    const int NR = (int)(1 + (Wp - 1 + 128 + kW - 2) / Wp);
+    PTB_REQUIRE(NR <= 256 && N * aH * aW * pl.cin_p < (1ll << 40), "hconv: geometry out of range");
     HConvParams p;
     memset(&p, 0, sizeof p);
-    const int rbox = (int)align_up((size_t)(128 + kW - 1), 8);
-    const int64_t npx = N * Hp * Wp;
-    PTB_REQUIRE(npx < (1ll << 31), "hconv: activation too large");
+    // CPS: two channel chunks per stage unless the A stage would not leave room for a ring
+    const uint32_t box_a = (uint32_t)(NR * Wp) * 128u;
+    const uint32_t box_b = (uint32_t)align_up((size_t)(pair ? pl.bn : pl.bn / 2), 8) * 128u;
+    const int budget = kSmemLimitH - 1024 - 512 - 8 * 48 * 4;
+    int cps = (pl.cin_p / 32) % 2 == 0 ? 2 : 1;
+    if (cps == 2 && 2 * 2 * (int)box_a + 4 * 2 * (int)box_b > budget) cps = 1;
+    PTB_REQUIRE(2 * (int)box_a + 3 * (int)box_b <= budget, "hconv: shared memory too small for the rings");
     {
-        // {32 ch, pixels, 32-channel chunks}: one box = the CPS chunk runs of a stage
-        const uint64_t dims[3] = {32, (uint64_t)npx, (uint64_t)(pl.cin_p / 32)};
-        const uint64_t strides[2] = {(uint64_t)pl.cin_p * 4, 128};
-        const uint32_t box[3] = {32, (uint32_t)rbox, (uint32_t)(pl.cin_p / 32 % 2 == 0 ? 2 : 1)};
-        tmap_tiled(&p.tmap_a, act, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        const uint64_t dims[5] = {32, (uint64_t)aW, (uint64_t)aH, (uint64_t)N, (uint64_t)(pl.cin_p / 32)};
+        const uint64_t strides[4] = {(uint64_t)pl.cin_p * 4, (uint64_t)(aW * pl.cin_p * 4),
+                                     (uint64_t)(aH * aW * pl.cin_p * 4), 128};
+        const uint32_t box[5] = {32, (uint32_t)Wp, (uint32_t)NR, 1, 1};
+        tmap_tiled(&p.tmap_a, act, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        const uint32_t box2[5] = {32, (uint32_t)Wp, (uint32_t)std::max(1, NR - 1), 1, 1};
+        tmap_tiled(&p.tmap_a2, act, 5, dims, strides, box2, CU_TENSOR_MAP_SWIZZLE_128B);
     }
-    const bool pair = pl.tap_pair;
     {
         // {32, weight rows, 32-wide k blocks}: one box = the CPS chunks of one tap
         const uint64_t kdim = (uint64_t)pl.kdim;
         const uint64_t dims[3] = {32, (uint64_t)pl.n_pad, kdim / 32};
         const uint64_t strides[2] = {kdim * 4, 128};
-        const uint32_t box[3] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2),
-                                 (uint32_t)(pl.cin_p / 32 % 2 == 0 ? 2 : 1)};
+        const uint32_t box[3] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2), (uint32_t)cps};
         tmap_tiled(&p.tmap_b, wt, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
-    p.span = pair ? 254 : 256;
     p.zero_tap = (int)pl.taps;
     PTB_REQUIRE(!pair || ((int64_t)pl.taps + 1) * pl.cin_p <= pl.kdim, "hconv: no zero tap packed");
-    const HConvTiling tl = hconv_tiling(N, Hp, Wp, oH, p.span);
-    PTB_REQUIRE(tl.tiles * (int64_t)pl.n_tiles < (1ll << 31), "hconv: too many tiles");
+    const HConvTiling tl = hconv_tiling(N, Wp, oH, cta_span);
+    PTB_REQUIRE(tl.tiles * (int64_t)pl.n_tiles < (1ll << 31) && tl.P_img < (1ll << 30), "hconv: too many tiles");
     p.N = (int)N;
-    p.Hp = (int)Hp;
     p.Wp = (int)Wp;
+    p.aph = (int)aph;
+    p.apw = (int)apw;
     p.kH = kH;
     p.kW = kW;
     p.cin_p = (int)pl.cin_p;
     p.chunks = (int)(pl.cin_p / 32);
     p.oH = (int)oH;
     p.oW = (int)oW;
-    p.P_img = tl.P_img;
-    p.img_px = Hp * Wp;
+    p.R = (int)((oH + 1) / 2);
+    p.m = (int)tl.P_img;
+    p.tpi = (int)ceil_div(tl.P_img, cta_span);
+    // a run from column w0 spans rows 0 .. (w0 + 128 + kW - 2) / Wp: one row less below
+    p.nr_split = NR > 1 ? (int)std::max<int64_t>(0, (NR - 1) * Wp - (128 + kW - 2)) : 0;
     p.tiles = (int)tl.tiles;
     p.n_rows = (int)pl.n_rows;
     p.bn = pl.bn;
     p.n_tiles = pl.n_tiles;
-    const int cps = p.chunks % 2 == 0 ? 2 : 1;
-    p.box_a = (uint32_t)rbox * 128u;
-    p.box_b = (uint32_t)align_up((size_t)(pair ? pl.bn : pl.bn / 2), 8) * 128u;
+    p.box_a = box_a;
+    p.box_b = box_b;
     p.stage_a = cps * p.box_a;
     p.stage_b = cps * p.box_b;
     // B ring: enough stages to cover two filter rows' worth of taps; A ring: the rest
-    const int budget = kSmemLimitH - 1024 - 512;
     int sb = std::min(16, std::max(4, pair ? kW + 1 : 2 * kW));
     while (sb > 3 && budget - sb * (int)p.stage_b < 2 * (int)p.stage_a) --sb;
     int sa = (budget - sb * (int)p.stage_b) / (int)p.stage_a;

@@ -174,7 +174,6 @@ void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws
               const float* gyh_pre, bool pre_padded) {
     UmmaPlan pl;
     PTB_REQUIRE(rowdgrad_ok(g, &pl), "rowdgrad: unsupported geometry");
-    if (pl.hankel != pre_padded) gyh_pre = nullptr;  // not the layout the engine reads
     const Geo e = dgrad_rows_geo(g);
     char* base = reinterpret_cast<char*>(ws);
     float* we = reinterpret_cast<float*>(base);
