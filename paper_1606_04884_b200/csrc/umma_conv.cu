@@ -506,7 +506,20 @@ UmmaPlan umma_plan(const Geo& g, bool dgrad) {
         const bool tconv_ok = g.sH == 1 && g.sW == 1 && g.pH <= g.kH - 1 && g.pW <= g.kW - 1 &&
                               g.kH <= 129 && g.kW <= 129 && g.C <= 65536;
         const bool gcol_ok = g.CRS <= 1024 && g.K <= 65536;
-        if (gcol_ok && (g.C < 16 || !tconv_ok)) {
+        // a Hankel transposed conv (tap-paired for few output channels) beats gcol + col2im
+        // even for small C: no CRS-wide column buffer round trip through HBM
+        bool hankel_tconv = false;
+        if (tconv_ok) {
+            UmmaPlan t;
+            t.mode = UmmaPlan::kDgradTconv;
+            t.n_rows = g.C;
+            t.taps = g.kH * g.kW;
+            plan_channels(t, g.K);
+            plan_rows(t);
+            plan_hankel(t, g.N, g.oH, g.oW, g.kH - 1 - g.pH, g.kW - 1 - g.pW, g.kW, g.H, g.W);
+            hankel_tconv = t.hankel;
+        }
+        if (gcol_ok && !hankel_tconv && (g.C < 16 || !tconv_ok)) {
             // gcol[n] = W^T(CRS x K) * gy[n] as a 1x1 conv over NHWC gy, then col2im
             pl.mode = UmmaPlan::kDgradGcol;
             pl.n_rows = g.CRS;

@@ -14,6 +14,8 @@
 // tf32 operand: that layout needs the 32-byte-atom swizzle.)
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace ptb {
@@ -86,6 +88,41 @@ __global__ void remap_rows_kernel(const float* __restrict__ gwe, float* __restri
     }
 }
 
+// W[k][c][r][s] -> W'[k][r*C + c][0][s]: the filter of the (1 x kW) column-expanded conv.
+__global__ void expand_filter_v_kernel(const float* __restrict__ w, float* __restrict__ we, int64_t K, int C,
+                                       int kH, int kW) {
+    const int64_t total = K * C * kH * kW;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i % kW), r = (int)((i / kW) % kH), c = (int)((i / ((int64_t)kW * kH)) % C);
+        const int64_t k = i / ((int64_t)kW * kH * C);
+        we[((k * kH + r) * C + c) * kW + s] = w[i];
+    }
+}
+
+// gx[n][c][h][w] = sum_{r=0..kH-1} gxe[n][r*C + c][h + pH - r][w + pW]   (r in fixed order)
+// gxe: [N][kH*C][oH][Wp]. One gx row per (blockIdx.x, threadIdx.y); threads sweep w.
+__global__ void fold_cols_kernel(const float* __restrict__ gxe, float* __restrict__ gx, int rows, int C,
+                                 int H, int W, int oH, int Wp, int kH, int pH, int pW) {
+    const int row = blockIdx.x * blockDim.y + threadIdx.y;  // (n, c, h)
+    if (row >= rows) return;
+    const int h = row % H;
+    const int c = (row / H) % C;
+    const int n = row / (H * C);
+    const int64_t plane = (int64_t)oH * Wp;
+    const float* src = gxe + ((int64_t)n * kH * C + c) * plane + pW;
+    float* dst = gx + (int64_t)row * W;
+    for (int w = threadIdx.x; w < W; w += blockDim.x) {
+        float acc = 0.f;
+#pragma unroll 4
+        for (int r = 0; r < kH; ++r) {
+            const int i = h + pH - r;
+            if (i >= 0 && i < oH) acc += __ldg(src + (int64_t)r * C * plane + (int64_t)i * Wp + w);
+        }
+        dst[w] = acc;
+    }
+}
+
 // W[k][c][r][s] -> W''[k][s*C + c][r][0]: the filter of the (kH x 1) row-expanded conv.
 __global__ void expand_filter_kernel(const float* __restrict__ w, float* __restrict__ we, int64_t K, int C,
                                      int kH, int kW) {
@@ -134,8 +171,24 @@ __global__ void fold_rows_kernel(const float* __restrict__ gxe, float* __restric
     }
 }
 
-// dgrad of the row-expanded (kH x 1) conv: its input has kW*C channels and width oW.
+// Two expansions of a small-C stride-1 layer for its input gradient:
+//  * horizontal (row): x'[(s,c)][h][j] = x[c][h][j+s-pW], a (kH x 1) conv, fold over s;
+//  * vertical (col): x'[(r,c)][i][w] = xpad[c][i+r][w], a (1 x kW) conv, fold over r.
+// The vertical form's (1 x kW) transposed conv is a Hankel pixel-run job (kW taps share
+// one run, tap-paired for <= 64 output rows), reading gy dense with the kW-1 border as
+// TMA out-of-bounds fill; the horizontal form (kH x 1) has no horizontal taps to share.
+bool dgrad_vertical(const Geo& g) {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_ROWDGRAD");
+        return e ? std::atoi(e) : 1;  // 1 = vertical, 0 = horizontal
+    }();
+    return v != 0 && g.kW >= 3;
+}
 Geo dgrad_rows_geo(const Geo& g) {
+    if (dgrad_vertical(g)) {
+        pt_conv_geom e{g.N, g.kH * g.C, g.oH, g.W + 2 * g.pW, g.K, 1, g.kW, 0, 0, 1, 1};
+        return Geo(e);
+    }
     pt_conv_geom e{g.N, g.kW * g.C, g.H, g.oW, g.K, g.kH, 1, g.pH, 0, g.sH, 1};
     return Geo(e);
 }
@@ -151,7 +204,8 @@ int64_t ce_of(const Geo& g) { return (g.kW * g.C + 31) / 32 * 32; }
 
 // ---- small-C dgrad: tensor-core tconv of the row-expanded layer + 1-D fold over s ----
 bool rowdgrad_ok(const Geo& g, UmmaPlan* plan) {
-    if (!(g.C <= 4 && g.sH == 1 && g.sW == 1 && g.kW * g.C <= 256)) return false;
+    if (!(g.C <= 4 && g.sH == 1 && g.sW == 1 && g.kW * g.C <= 256 && g.kH * g.C <= 256)) return false;
+    if (g.N * g.kH * g.C * g.H >= (1ll << 31) || g.N * g.C * g.H >= (1ll << 31)) return false;
     const UmmaPlan pl = umma_plan(dgrad_rows_geo(g), true);
     if (plan) *plan = pl;
     return pl.ok && pl.mode == UmmaPlan::kDgradTconv;
@@ -161,13 +215,13 @@ size_t rowdgrad_workspace(const Geo& g) {
     UmmaPlan pl;
     if (!rowdgrad_ok(g, &pl)) return 0;
     const Geo e = dgrad_rows_geo(g);
-    return align_up((size_t)(g.K * e.C * g.kH) * 4, 256) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256) +
+    return align_up((size_t)(g.K * g.CRS) * 4, 256) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256) +
            align_up(pl.ws_bytes, 256);
 }
 
 size_t rowdgrad_act_offset(const Geo& g) {
     const Geo e = dgrad_rows_geo(g);
-    return align_up((size_t)(g.K * e.C * g.kH) * 4, 256) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256);
+    return align_up((size_t)(g.K * g.CRS) * 4, 256) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256);
 }
 
 void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st,
@@ -177,15 +231,25 @@ void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws
     const Geo e = dgrad_rows_geo(g);
     char* base = reinterpret_cast<char*>(ws);
     float* we = reinterpret_cast<float*>(base);
-    float* gxe = reinterpret_cast<float*>(base + align_up((size_t)(g.K * e.C * g.kH) * 4, 256));
+    float* gxe = reinterpret_cast<float*>(base + align_up((size_t)(g.K * g.CRS) * 4, 256));
     char* dws = reinterpret_cast<char*>(gxe) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256);
     const int64_t nw = g.K * g.CRS;
-    expand_filter_kernel<<<(unsigned)std::min<int64_t>(ceil_div(nw, 256), 4 * (int64_t)sm_count()), 256, 0, st>>>(
-        w, we, g.K, (int)g.C, (int)g.kH, (int)g.kW);
+    const unsigned wb = (unsigned)std::min<int64_t>(ceil_div(nw, 256), 4 * (int64_t)sm_count());
+    const bool vert = dgrad_vertical(g);
+    if (vert) expand_filter_v_kernel<<<wb, 256, 0, st>>>(w, we, g.K, (int)g.C, (int)g.kH, (int)g.kW);
+    else expand_filter_kernel<<<wb, 256, 0, st>>>(w, we, g.K, (int)g.C, (int)g.kH, (int)g.kW);
     after_launch("expand_filter");
     umma_conv_bwd_data(e, pl, gy, we, gxe, dws, st, gyh_pre, 2.0 * g.M * g.K * g.CRS);
     const int64_t total = g.N * g.C * g.HW;
     ProfScope prof("layout", st, 0.0, 4.0 * (e.N * e.C * e.H * e.W + total));
+    if (vert) {
+        const int rows = (int)(g.N * g.C * g.H);
+        const int tx = g.W >= 128 ? 128 : g.W >= 64 ? 64 : 32;
+        fold_cols_kernel<<<(unsigned)ceil_div(rows, 256 / tx), dim3(tx, 256 / tx), 0, st>>>(
+            gxe, gx, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.oH, (int)e.W, (int)g.kH, (int)g.pH, (int)g.pW);
+        after_launch("fold_cols");
+        return;
+    }
     const int64_t rows = g.N * g.C * g.H;
     fold_rows_kernel<<<(unsigned)std::min<int64_t>(rows, 128 * (int64_t)sm_count()), 128, 0, st>>>(
         gxe, gx, g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.oW, (int)g.kW, (int)g.pW, (int)g.sW);
