@@ -366,7 +366,10 @@ def main():
     L.lib().pt_b200_profile_enable(0)
     tf32_cublas = measure_cublas_tf32(torch) if rank == 0 else None
     tf32_derived = peaks.get("bf16_tflops", 1590.0) / 2.0
-    peak_tf = max(tf32_derived, tf32_cublas or 0.0)
+    # denominator: the measured TF32 tensor-pipe ceiling of this GPU (back-to-back MMAs,
+    # pt_b200_tf32_mma_peak); cuBLAS TF32 and MEASURED_PEAKS bf16/2 are reported beside it
+    tf32_mma = float(L.lib().pt_b200_tf32_mma_peak()) if rank == 0 else -1.0
+    peak_tf = max(tf32_mma, tf32_derived, tf32_cublas or 0.0)
     dom = max(per, key=lambda k: per[k][0])
     dms, dn, dfl, _ = per[dom]
     avg_ms = dms / dn
@@ -378,8 +381,10 @@ def main():
     roof["avg_launch_ms"] = avg_ms
     roof["flops_per_launch"] = dfl / dn
     roof["share_of_step"] = dms / ms if ms > 0 else None
-    roof["peak_source"] = (f"max(cuBLAS TF32 8192^3 on this box = {tf32_cublas}, "
+    roof["peak_source"] = (f"max(measured TF32 MMA ceiling on this box = {tf32_mma:.1f} "
+                           f"[pt_b200_tf32_mma_peak], cuBLAS TF32 8192^3 = {tf32_cublas}, "
                            f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})")
+    roof["frac_vs_bf16_half"] = roof["achieved"] / tf32_derived
     roof["per_launch"] = {k: {"ms": v[0] / v[1], "tflops": v[2] / v[0] * 1e-9}
                           for k, v in sorted(per.items())}
 

@@ -163,6 +163,11 @@ int pt_b200_reduce_dim(int op, const float* base, const pt_view* view, int dim, 
 /* Number of kernels this library launched on the calling process (bench gpu_launches). */
 int64_t pt_b200_launch_count(void);
 
+/* Measured TF32 tensor-pipe ceiling (TFLOP/s) of the current device at its current
+ * clocks: back-to-back M=256 N=256 K=8 kind::tf32 MMAs from shared memory on every SM
+ * pair (the roofline denominator bench.py reports against). < 0 on failure. */
+double pt_b200_tf32_mma_peak(void);
+
 /* ---- live kernel timing (bench.py roofline) ----
  * When enabled, the library brackets each launch of its hot kernels with CUDA events
  * on the launching stream and records the algorithmic work of that launch. Reading

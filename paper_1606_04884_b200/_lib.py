@@ -93,6 +93,7 @@ _SIGS = {
     "pt_b200_reduce_all": (C.c_int, [C.c_int, _P, C.POINTER(PtView), _P, _P]),
     "pt_b200_reduce_dim": (C.c_int, [C.c_int, _P, C.POINTER(PtView), C.c_int, _P, _P]),
     "pt_b200_launch_count": (C.c_int64, []),
+    "pt_b200_tf32_mma_peak": (C.c_double, []),
     "pt_b200_profile_enable": (C.c_int, [C.c_int]),
     "pt_b200_profile_reset": (C.c_int, []),
     "pt_b200_profile_tag": (C.c_int, [C.c_char_p]),

@@ -32,7 +32,10 @@ def read(path):
     r = {"kernel": vals[h.index("Kernel Name")][:60]}
     for i, name in enumerate(h):
         if name in METRICS:
-            v = float(vals[i].replace(",", ""))
+            try:
+                v = float(vals[i].replace(",", ""))
+            except ValueError:
+                continue
             u = units[i]
             if u.split("/")[0] in SCALE:
                 v *= SCALE[u.split("/")[0]]
