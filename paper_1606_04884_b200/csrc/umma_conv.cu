@@ -461,7 +461,11 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
     // measured (convnet L2/L3/L5): the pixel-run kernel wins at >= 0.85 of positions valid,
     // ties near 0.8 and loses below, where the im2col kernel's zero waste pays for its
     // L2->SM traffic
-    if (hconv_env() != 1 && eff < 0.84) return;
+    // With <= 64 output rows the Hankel kernel also pairs taps (N = 2*bn beats the N=64
+    // MMA floor the im2col kernel sits at), which pays for more border waste: AlexNet conv2
+    // dgrad (71% valid) 0.151 -> 0.122 ms.
+    const bool will_pair = pl.n_rows <= hconv_pair_max() && hconv_pair_env() != 0;
+    if (hconv_env() != 1 && eff < (will_pair ? 0.6 : 0.84)) return;
     pl.hankel = true;
     // pairing doubles N: for <= 64 rows it beats the N=64 MMA floor (L2 dgrad 1.27 ->
     // 0.92 ms). Allowed up to 128 rows (N=256) by PT_B200_HCONV_PAIR_MAX, but measured
