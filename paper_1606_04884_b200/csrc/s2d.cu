@@ -20,25 +20,26 @@ namespace ptb {
 
 namespace {
 
-// One output row (n, (c,a,b), I) per (blockIdx.x, threadIdx.y); threads sweep J. 32-bit
-// index maths only once per row: the per-element 64-bit div/mod chain made this pass
-// ALU-bound (0.45 TB/s).
+// One block per (n, c, a, I): the padded input row s*I + a - pH is read once, coalesced,
+// and scattered into the s phase planes b of x' (thread t = padded column: plane t % s,
+// column t / s). Reading each phase plane's row separately would stride the loads by s.
+template <int S>
 __global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict__ xs, int rows, int C,
-                                 int H, int W, int s, int pH, int pW, int Hs, int Ws) {
-    const int Cs = C * s * s;
-    const int row = blockIdx.x * blockDim.y + threadIdx.y;
-    if (row >= rows) return;
+                                 int H, int W, int pH, int pW, int Hs, int Ws) {
+    const int row = blockIdx.x;  // (n, c, a, I)
     const int I = row % Hs;
-    const int cs = (row / Hs) % Cs;
-    const int n = row / (Hs * Cs);
-    const int c = cs / (s * s), a = (cs / s) % s, b = cs % s;
-    const int h = s * I + a - pH;
-    float* dst = xs + (int64_t)row * Ws;
+    const int a = (row / Hs) % S;
+    const int c = (row / (Hs * S)) % C;
+    const int n = row / (Hs * S * C);
+    const int h = S * I + a - pH;
     const bool hin = h >= 0 && h < H;
     const float* src = x + (((int64_t)n * C + c) * H + (hin ? h : 0)) * W;
-    for (int J = threadIdx.x; J < Ws; J += blockDim.x) {
-        const int w = s * J + b - pW;
-        dst[J] = (hin && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
+    const int64_t plane = (int64_t)Hs * Ws;
+    float* dst = xs + (((int64_t)n * C * S * S + (int64_t)(c * S + a) * S) * Hs + I) * Ws;
+    for (int t = threadIdx.x; t < Ws * S; t += blockDim.x) {
+        const int w = t - pW;
+        const float v = (hin && w >= 0 && w < W) ? __ldg(src + w) : 0.f;
+        dst[(t % S) * plane + t / S] = v;
     }
 }
 
@@ -58,24 +59,24 @@ __global__ void s2d_weight_kernel(const float* __restrict__ w, float* __restrict
     }
 }
 
-// gx[n][c][h][w] = gx'[n][(c, (h+pH)%s, (w+pW)%s)][(h+pH)/s][(w+pW)/s]; one gx row per
-// (blockIdx.x, threadIdx.y), threads sweep w.
+// gx[n][c][h][w] = gx'[n][(c, (h+pH)%S, (w+pW)%S)][(h+pH)/S][(w+pW)/S]; one gx row per
+// (blockIdx.x, threadIdx.y), threads sweep w (compile-time S: no runtime divisions).
+template <int S>
 __global__ void d2s_grad_kernel(const float* __restrict__ gxs, float* __restrict__ gx, int rows, int C,
-                                int H, int W, int s, int pH, int pW, int Hs, int Ws) {
+                                int H, int W, int pH, int pW, int Hs, int Ws) {
     const int row = blockIdx.x * blockDim.y + threadIdx.y;  // (n, c, h)
     if (row >= rows) return;
     const int h = row % H;
     const int c = (row / H) % C;
     const int n = row / (H * C);
-    const int Cs = C * s * s;
-    const int hh = h + pH, I = hh / s;
+    const int hh = h + pH, I = hh / S;
     float* dst = gx + (int64_t)row * W;
     // pixels past the last output's receptive field get no gradient
-    const float* src = gxs + (((int64_t)n * Cs + (c * s + hh % s) * s) * Hs + I) * (int64_t)Ws;
+    const float* src = gxs + (((int64_t)n * C * S * S + (c * S + hh % S) * S) * Hs + I) * (int64_t)Ws;
     const int64_t plane = (int64_t)Hs * Ws;
     for (int w = threadIdx.x; w < W; w += blockDim.x) {
-        const int ww = w + pW, J = ww / s;
-        dst[w] = (I < Hs && J < Ws) ? __ldg(src + (ww % s) * plane + J) : 0.f;
+        const int ww = w + pW, J = ww / S;
+        dst[w] = (I < Hs && J < Ws) ? __ldg(src + (ww % S) * plane + J) : 0.f;
     }
 }
 
@@ -105,7 +106,7 @@ unsigned blocks_for(int64_t total) {
 
 bool s2d_applies(const Geo& g) {
     const int64_t s = g.sH;
-    if (s < 2 || g.sW != s || g.C * s * s > 64 || g.kH < s || g.kW < s) return false;
+    if (!(s == 2 || s == 3 || s == 4 || s == 8) || g.sW != s || g.C * s * s > 64 || g.kH < s || g.kW < s) return false;
     if (g.N * g.C * g.H >= (1ll << 31)) return false;  // 32-bit row indices
     const Geo e = s2d_geo(g);
     // the regrouped filter may not inflate the contraction by more than 1.5x
@@ -122,9 +123,16 @@ Geo s2d_geo(const Geo& g) {
 void s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st) {
     const Geo e = s2d_geo(g);
     ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + e.N * e.C * e.HW));
-    const int rows = (int)(e.N * e.C * e.H);
-    s2d_input_kernel<<<(unsigned)ceil_div(rows, 4), dim3(64, 4), 0, st>>>(
-        x, xs, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H, (int)e.W);
+    const int rows = (int)(g.N * g.C * g.sH * e.H);  // (n, c, a, I)
+    const int tb = (int)std::min<int64_t>(256, align_up((size_t)(e.W * g.sH), 32));
+#define PTB_S2D_IN(S_)                                                                             \
+    s2d_input_kernel<S_><<<(unsigned)rows, tb, 0, st>>>(x, xs, rows, (int)g.C, (int)g.H, (int)g.W, \
+                                                        (int)g.pH, (int)g.pW, (int)e.H, (int)e.W)
+    if (g.sH == 2) PTB_S2D_IN(2);
+    else if (g.sH == 3) PTB_S2D_IN(3);
+    else if (g.sH == 4) PTB_S2D_IN(4);
+    else PTB_S2D_IN(8);
+#undef PTB_S2D_IN
     after_launch("s2d_input");
 }
 
@@ -139,8 +147,14 @@ void d2s_grad(const Geo& g, const float* gxs, float* gx, cudaStream_t st) {
     const Geo e = s2d_geo(g);
     ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW * 2));
     const int rows = (int)(g.N * g.C * g.H);
-    d2s_grad_kernel<<<(unsigned)ceil_div(rows, 2), dim3(128, 2), 0, st>>>(
-        gxs, gx, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.sH, (int)g.pH, (int)g.pW, (int)e.H, (int)e.W);
+#define PTB_D2S(S_)                                                                                    \
+    d2s_grad_kernel<S_><<<(unsigned)ceil_div(rows, 2), dim3(128, 2), 0, st>>>(                         \
+        gxs, gx, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.pH, (int)g.pW, (int)e.H, (int)e.W)
+    if (g.sH == 2) PTB_D2S(2);
+    else if (g.sH == 3) PTB_D2S(3);
+    else if (g.sH == 4) PTB_D2S(4);
+    else PTB_D2S(8);
+#undef PTB_D2S
     after_launch("d2s_grad");
 }
 
