@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2u * p.stage_bytes);
                     tma_load_3d_cg2(sA + (size_t)stage * p.stage_a, &p.tmap_x, &full[stage], 0,
-                                    seg * 4, prow + r);
+                                    seg * 2, prow + r);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -252,12 +252,13 @@ struct RowPlan {
 RowPlan rplan(const Geo& g) {
     RowPlan r;
     r.Hp = (int)(g.H + 2 * g.pH);
-    r.Wa = (int)((g.W + 2 * g.pW + 31) / 32 * 32);
+    r.Wa = (int)((g.W + 2 * g.pW + 63) / 64 * 64);
     r.S2 = (int)((g.kW + 1) / 2 * 2);
     r.Np = (int)((g.K + 15) / 16 * 16);
     r.segs = (int)ceil_div(g.oW, 128);
-    r.seg_chunks = (128 + r.S2 - 1 + 31) / 32;  // 32 pixels (512 B) per chunk
-    r.xp_elems = g.N * r.Hp * r.Wa * 4 + 128 * r.seg_chunks;  // slack for the last segment
+    // 64 pixels (1 KB) per TMA chunk: the per-row request count, not bytes, paced the loads
+    r.seg_chunks = (128 + r.S2 - 1 + 63) / 64;
+    r.xp_elems = g.N * r.Hp * r.Wa * 4 + 256 * r.seg_chunks;  // slack for the last segment
     const int64_t wf = g.kH * r.S2 * (r.Np / 2) * 4;
     r.w_chunks = (int)ceil_div(wf, 128);
     r.w_half = (int64_t)r.w_chunks * 128;
@@ -307,17 +308,17 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     RowConvParams p;
     memset(&p, 0, sizeof p);
     {
-        const uint64_t dims[3] = {128, (uint64_t)rp.Wa * 4 / 128, (uint64_t)(g.N * rp.Hp)};
-        const uint64_t strides[2] = {512, (uint64_t)rp.Wa * 16};
+        const uint64_t dims[3] = {256, (uint64_t)rp.Wa * 4 / 256, (uint64_t)(g.N * rp.Hp)};
+        const uint64_t strides[2] = {1024, (uint64_t)rp.Wa * 16};
         // one stage = rps padded rows of seg_chunks x 512 B
         p.rps = (int)g.kH;
-        while (p.rps > 1 && (size_t)p.rps * rp.seg_chunks * 512 * 3 >
+        while (p.rps > 1 && (size_t)p.rps * rp.seg_chunks * 1024 * 3 >
                                 (size_t)(kSmemLimit - 2048 - (int)align_up(rp.w_half * 4, 1024)))
             p.rps = (p.rps + 1) / 2;
-        const uint32_t box[3] = {128, (uint32_t)rp.seg_chunks, (uint32_t)p.rps};
+        const uint32_t box[3] = {256, (uint32_t)rp.seg_chunks, (uint32_t)p.rps};
         tmap_tiled(&p.tmap_x, xp, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
-        p.stage_bytes = (uint32_t)(p.rps * rp.seg_chunks * 512);
-        p.row16 = (uint32_t)(rp.seg_chunks * 512) >> 4;
+        p.stage_bytes = (uint32_t)(p.rps * rp.seg_chunks * 1024);
+        p.row16 = (uint32_t)(rp.seg_chunks * 1024) >> 4;
     }
     {
         const uint64_t dims[3] = {128, (uint64_t)rp.w_chunks, 2};
