@@ -167,3 +167,73 @@ def test_finput_reuse_bitwise(g):
     gx1, gw1, gb1 = pt.conv_backward(G, _d(x), _d(gy), _d(w), finput=fin)
     for a, c, what in ((y0, y1, "y"), (gx0, gx1, "gx"), (gw0, gw1, "gw"), (gb0, gb1, "gb")):
         np.testing.assert_array_equal(_h(a), _h(c), err_msg=f"{gstr(g)} {what} (finput {nb} B)")
+
+
+# Geometries aimed at the Hankel engine's edge cases: odd output heights (unequal image
+# halves), asymmetric kernels/pads, padded rows near the 256-pixel TMA box limit, tap
+# pairing with odd kW, multi-chunk stages, rows that need NR vs NR-1 boxes.
+HANKEL_EDGE = [
+    po.geom(2, 32, 13, 37, 48, 5, 7, 2, 3, 1, 1),
+    po.geom(1, 64, 9, 250, 64, 3, 3, 1, 1, 1, 1),
+    po.geom(3, 96, 11, 30, 160, 3, 5, 0, 2, 1, 1),
+    po.geom(2, 128, 17, 17, 64, 9, 9, 4, 4, 1, 1),
+    po.geom(1, 32, 40, 61, 32, 11, 11, 5, 5, 1, 1),
+]
+
+_HANKEL_SCRIPT = r"""
+import sys, json
+sys.path[:0] = sys.argv[1:4]
+import numpy as np, torch
+import paper_1606_04884_b200 as pt, pyoracle as po
+from helpers import conv_inputs
+out = []
+for spec in json.loads(sys.argv[4]):
+    g = po.geom(*spec)
+    x, w, b, gy = conv_inputs(g, 91)
+    G = pt.ConvGeometry(*spec)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    y = pt.conv_forward(G, d(x), d(w), d(b))
+    gx, gw, gb = pt.conv_backward(G, d(x), d(gy), d(w))
+    torch.cuda.synchronize()
+    rel = lambda a, r: float(np.linalg.norm(a.cpu().numpy().astype(np.float64) - r) /
+                             max(np.linalg.norm(r), 1e-30))
+    out.append([rel(y, po.conv_direct(g, x, w, b, f64=True)),
+                rel(gx, po.conv_backward_input(g, gy, w)),
+                rel(gw, po.conv_backward_weight(g, x, gy)[0])])
+print(json.dumps(out))
+"""
+
+
+def test_hankel_engine_forced_edge_geometries():
+    """PT_B200_HCONV=1 forces the Hankel engine for every eligible pass (the engine
+    choice is read once per process, hence the subprocess); TF32 tolerance vs oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW]
+             for g in HANKEL_EDGE]
+    env = dict(os.environ, PT_B200_HCONV="1")
+    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
+                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    errs = json.loads(r.stdout.strip().splitlines()[-1])
+    for g, e in zip(HANKEL_EDGE, errs):
+        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
+
+
+@pytest.mark.parametrize("g", HANKEL_EDGE, ids=gstr)
+def test_hankel_edge_default_engines(g):
+    """The same edge geometries through whatever engines the default plan picks."""
+    x, w, b, gy = conv_inputs(g, 92)
+    pt = _pt()
+    G = _g(g)
+    y = pt.conv_forward(G, _d(x), _d(w), _d(b))
+    gx, gw, gb = pt.conv_backward(G, _d(x), _d(gy), _d(w))
+    check_tf32(_h(y), po.conv_direct(g, x, w, b, f64=True), "fwd")
+    check_tf32(_h(gx), po.conv_backward_input(g, gy, w), "dgrad")
+    rgw, rgb = po.conv_backward_weight(g, x, gy)
+    check_tf32(_h(gw), rgw, "wgrad")
+    np.testing.assert_allclose(_h(gb), rgb, rtol=1e-5, atol=1e-4)
