@@ -86,9 +86,9 @@ struct UmmaPlan {
     // activation stays dense NHWC; the (aph, apw) border is TMA out-of-bounds fill.
     bool hankel = false;
     int64_t aH = 0, aW = 0, aph = 0, apw = 0, aHp = 0, aWp = 0;
-    // <= 64 output rows: pair taps (s, s+1) in one N = 2*bn MMA (umma_hconv.cu); the packed
-    // weights then carry one extra all-zero tap (index `taps`) for odd kW
-    bool tap_pair = false;
+    // <= 128 output rows: group G taps (s .. s+G-1) in one N = G*bn MMA (umma_hconv.cu);
+    // the packed weights then carry one extra all-zero tap (index `taps`) for kW % G != 0
+    int tap_group = 1;  // taps per MMA (1, or 2..4: output-shift grouping)
     int64_t kdim = 0;  // packed weight row length (floats)
 };
 struct HConvTiling {

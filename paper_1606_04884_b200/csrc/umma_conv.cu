@@ -440,6 +440,18 @@ int hconv_pair_env() {
     return v;
 }
 
+int hconv_group_max() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_HCONV_GROUP_MAX");
+        // groups of 3-4 taps (N up to 256) are opt-in: by MMA cycles they should win (L1 dgrad
+        // G=4: 240 vs 384 cycles per 11 taps) but measured slower (L1 0.55 -> 0.58 ms, L2 G=3
+        // 0.93 -> 1.26 ms), so pairs stay the default
+        const int g = e ? std::atoi(e) : 2;
+        return g < 2 ? 2 : g > 4 ? 4 : g;
+    }();
+    return v;
+}
+
 int hconv_pair_max() {
     static const int v = [] {
         const char* e = std::getenv("PT_B200_HCONV_PAIR_MAX");
@@ -470,10 +482,26 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
     // pairing doubles N: for <= 64 rows it beats the N=64 MMA floor (L2 dgrad 1.27 ->
     // 0.92 ms). Allowed up to 128 rows (N=256) by PT_B200_HCONV_PAIR_MAX, but measured
     // slower there (L2 fwd 0.65 -> 0.75 ms)
-    if (pl.n_rows <= hconv_pair_max() && hconv_pair_env() != 0) {
-        // tap pairing: one N tile of all the rows, one extra zero tap in the packing
-        pl.tap_pair = true;
-        pl.bn = (int)((pl.n_rows + 7) / 8 * 8);
+    if (will_pair) {
+        // tap grouping: G taps per MMA (N = G*bn), one N tile of all the rows, one extra zero
+        // tap in the packing. An N <= 128 MMA costs ~64 cycles whatever N is; with groups
+        // above 2 enabled (PT_B200_HCONV_GROUP_MAX) pick G minimising
+        // ceil(kW / G) * max(64, G*bn/2)
+        const int bn8 = (int)((pl.n_rows + 7) / 8 * 8), bn16 = (int)((pl.n_rows + 15) / 16 * 16);
+        int best_g = 2, best_bn = bn8;
+        double best_cost = 1e30;
+        for (int G = 2; G <= hconv_group_max(); ++G) {
+            const int bn = (G % 2 == 1) ? bn16 : bn8;
+            if (G * bn > 256 || (G * bn) % 16 != 0) continue;
+            const double cost = (double)ceil_div(kW, G) * std::max(64.0, G * bn / 2.0);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best_g = G;
+                best_bn = bn;
+            }
+        }
+        pl.tap_group = best_g;
+        pl.bn = best_bn;
         pl.n_tiles = 1;
         pl.n_pad = pl.bn;
         pl.kdim = ceil_div((pl.taps + 1) * pl.cin_p, 64) * 64;

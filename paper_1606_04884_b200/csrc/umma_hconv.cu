@@ -43,11 +43,14 @@ using namespace umma;
 
 constexpr int kThreadsH = 192;
 constexpr int kSmemLimitH = 232448;
+// epilogue neighbour exchange: [bn/16 chunks][3 warps][G-1 deltas][G-1 lanes][16] floats
+inline int xch_bytes(int G, int bn) { return G > 1 ? (bn / 16 + 1) * 3 * (G - 1) * (G - 1) * 16 * 4 : 0; }
 
 struct HConvParams {
     CUtensorMap tmap_a;  // act NHWC [N][aH][aW][Cp], 5-D {32, aW, aH, N, Cp/32}, box {32, Wp, NR, 1, CPS}
     CUtensorMap tmap_a2; // same with NR - 1 rows: runs starting early in a row need one row less
     CUtensorMap tmap_b;  // packed weights, 3-D {32, n_pad, kdim/32}, box {32, rows, CPS}, SW128
+    CUtensorMap tmap_bh; // G = 3: box {32, bn/2, 1} for the half-tap segments
     int N, kH, kW, chunks, cin_p;
     int aph, apw;        // zero border the TMA out-of-bounds fill supplies (top, left)
     int Wp;              // padded row width = position-space row stride
@@ -57,7 +60,7 @@ struct HConvParams {
     int tpi;             // pair tiles per image
     int nr_split;        // runs starting at column < nr_split fit NR - 1 rows
     int tiles;           // N * tpi
-    int zero_tap;        // PAIR: packed-weight tap index holding zeros (odd kW)
+    int zero_tap;        // G > 1: packed-weight tap index holding zeros (kW % G != 0)
     int n_rows, bn, n_tiles;
     int sa, sb;          // ring depths
     uint32_t stage_a, stage_b;  // bytes per stage (CPS boxes)
@@ -69,13 +72,14 @@ struct HConvParams {
 };
 
 // CPS: 32-channel chunks per pipeline stage (1 or 2).
-// PAIR (output-shift tap pairing, for <= 128 output channels: an N=64 MMA costs as much
-// as N=128, and an N=256 MMA reads the A tile once for two taps): one MMA computes taps s and s+1 from the SAME pixel run (shift s) —
-// CTA 0 stages tap s's weights, CTA 1 tap s+1's, N = 2*bn. Column half 1 then holds tap
-// s+1's contribution to the position one to the LEFT, so the epilogue forms
-// out[q] = D0[q] + D1[q+1]; each CTA's last lane lacks its right neighbour and is
-// dropped (tiles advance 127 positions per CTA).
-template <int CPS, bool PAIR>
+// G > 1 (output-shift tap grouping, for <= 128 output channels): one MMA computes taps
+// s .. s+G-1 from the SAME pixel run (shift s) with N = G*bn — the weight rows (delta, c)
+// are split between the two CTAs. Column group delta then holds tap s+delta's
+// contribution to the position delta to the LEFT, so the epilogue forms
+// out[q] = sum_delta D_delta[q + delta]; each CTA's last G-1 lanes lack right neighbours
+// and are dropped (tiles advance 129 - G positions per CTA). An N <= 128 MMA costs the
+// same ~64 cycles whatever N is, so grouping cuts the MMA count up to G-fold.
+template <int CPS, int G>
 __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_constant__ HConvParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ uint8_t smem_raw[];
@@ -90,7 +94,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     uint64_t* tfull = bempty + p.sb;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // PAIR: [8 chunks][3 warps][16]
+    float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // G > 1: [8 chunks][3 warps][G-1][G-1][16]
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     const uint32_t tmem_base = *tmem_holder;
     const int num_units = p.tiles * p.n_tiles;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    constexpr int kCtaSpan = PAIR ? 127 : 128;  // positions a CTA advances per tile
+    constexpr int kCtaSpan = 129 - G;  // positions a CTA advances per tile
 
     if (warp == 0) {
         if (lane == 0) {
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 const bool short_run = qh % p.Wp < p.nr_split;
                 const CUtensorMap* amap = short_run ? &p.tmap_a2 : &p.tmap_a;
                 const uint32_t atx_t = short_run ? atx - 2 * (uint32_t)CPS * (uint32_t)p.Wp * 128u : atx;
-                const int brow = PAIR ? 0 : nt * p.bn + (int)rank * (p.bn / 2);
+                const int brow = G > 1 ? 0 : nt * p.bn + (int)rank * (p.bn / 2);
                 for (int r = 0; r < p.kH; ++r) {
                     for (int cc = 0; cc < p.chunks; cc += CPS) {
                         mbar_wait(&aempty[as], aph ^ 1);
@@ -154,14 +158,35 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             as = 0;
                             aph ^= 1;
                         }
-                        for (int s = 0; s < p.kW; s += PAIR ? 2 : 1) {
+                        for (int s = 0; s < p.kW; s += G) {
                             mbar_wait(&bempty[bs], bph ^ 1);
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
-                            // PAIR: this CTA's tap is s + rank (past the row: the zero tap)
-                            const int tap = PAIR ? (s + (int)rank < p.kW ? r * p.kW + s + (int)rank : p.zero_tap)
-                                                 : r * p.kW + s;
-                            tma_load_3d_cg2(sB + (size_t)bs * p.stage_b, &p.tmap_b, &bfull[bs], 0, brow,
-                                            tap * (p.cin_p / 32) + cc);
+                            uint8_t* bdst = sB + (size_t)bs * p.stage_b;
+                            if constexpr (G == 1) {
+                                tma_load_3d_cg2(bdst, &p.tmap_b, &bfull[bs], 0, brow,
+                                                (r * p.kW + s) * (p.cin_p / 32) + cc);
+                            } else if constexpr (G == 2) {
+                                // this CTA's rows are exactly tap s + rank: one request, all chunks
+                                const int tap = s + (int)rank < p.kW ? r * p.kW + s + (int)rank : p.zero_tap;
+                                tma_load_3d_cg2(bdst, &p.tmap_b, &bfull[bs], 0, 0, tap * (p.cin_p / 32) + cc);
+                            } else {
+                                // this CTA's weight rows [rank*G*bn/2, (rank+1)*G*bn/2) of the
+                                // (delta, c) stack, in whole-tap (and for G = 3 half-tap) pieces
+                                const int half = G * p.bn / 2;
+                                int n0 = (int)rank * half;
+                                while (n0 < ((int)rank + 1) * half) {
+                                    const int delta = n0 / p.bn, c0 = n0 - delta * p.bn;
+                                    const int len = (G % 2 == 1 && (c0 != 0 || n0 + p.bn > ((int)rank + 1) * half))
+                                                        ? p.bn / 2 : p.bn;
+                                    const int tap = s + delta < p.kW ? r * p.kW + s + delta : p.zero_tap;
+                                    const CUtensorMap* bm = len == p.bn ? &p.tmap_b : &p.tmap_bh;
+#pragma unroll
+                                    for (int c = 0; c < CPS; ++c)
+                                        tma_load_3d_cg2(bdst + c * p.box_b + (n0 - (int)rank * half) * 128, bm,
+                                                        &bfull[bs], 0, c0, tap * (p.cin_p / 32) + cc + c);
+                                    n0 += len;
+                                }
+                            }
                             if (++bs == p.sb) {
                                 bs = 0;
                                 bph ^= 1;
@@ -174,7 +199,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     } else if (warp == 1) {
         if (leader) {
             // ===== MMA issuer (whole warp, converged; one elected lane issues) =====
-            const uint32_t idesc = idesc_tf32(256, PAIR ? 2 * p.bn : p.bn, 0, 0);
+            const uint32_t idesc = idesc_tf32(256, G * p.bn, 0, 0);
             constexpr uint32_t kHi = desc_hi(1024, kSwizzle128B);
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
@@ -183,7 +208,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 const uint32_t acc = it & 1;
                 mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem_base + acc * (PAIR ? 2 * p.bn : p.bn);
+                const uint32_t d = tmem_base + acc * (G * p.bn);
                 const int t = u / p.n_tiles;
                 const uint32_t w0 = (uint32_t)(((t % p.tpi) * kCtaSpan) % p.Wp);  // run start column
                 uint32_t accum = 0;
@@ -193,8 +218,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                         mbar_wait(&afull[as], aph);
                         tc_fence_after();
                         const uint32_t alo = desc_lo(smem_u32(sA + (size_t)as * p.stage_a), 16);
-                        for (int s = 0; s < p.kW; s += PAIR ? 2 : 1) {
-                            if (p.exp != 4 || s == 0) mbar_wait(&bfull[bs], bph);
+                        for (int s = 0; s < p.kW; s += G) {
+                            mbar_wait(&bfull[bs], bph);
                             tc_fence_after();
                             // tap s: the same pixel run, s rows (s*128 B) further in
                             const uint32_t a_s = alo + (w0 + (uint32_t)s) * 8u;
@@ -235,33 +260,50 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             const int n = t / p.tpi;
             const int qq = (t - n * p.tpi) * kCtaSpan + (int)(q * 32 + lane);  // position in the half
             const int i = (int)rank * p.R + qq / p.Wp, j = qq % p.Wp;
-            const bool valid = qq < p.m && i < p.oH && j < p.oW && (!PAIR || q * 32 + lane < 127);
+            const bool valid = qq < p.m && i < p.oH && j < p.oW && (int)(q * 32 + lane) < kCtaSpan;
             const int ch0 = nt * p.bn;
             const int64_t base = ((int64_t)n * p.n_rows + ch0) * ohw + (int64_t)i * p.oW + j;
-            if constexpr (!PAIR) {
+            if constexpr (G == 1) {
                 const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
                 store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base : 0), ohw, p.bias, ch0,
                                         p.n_rows, valid);
             } else {
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * 2 * p.bn;
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * G * p.bn;
                 float* o = p.out + (valid ? base : 0);
                 for (int c0 = 0; c0 < p.bn; c0 += 16) {
-                    uint32_t v0[16], v1[16];
-                    tmem_ld_32x32b_x16(taddr + c0, v0);
-                    tmem_ld_32x32b_x16(taddr + p.bn + c0, v1);
-                    tmem_ld_wait();
-                    // right neighbour's tap-(s+1) half: next lane, or the next warp's lane 0
-                    float nb[16];
-                    float* slot = xch + (c0 >> 4) * 48;
+                    uint32_t vd[G][16];
+                    float acc_v[16];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        nb[e] = __shfl_down_sync(0xffffffffu, __uint_as_float(v1[e]), 1);
-                        if (lane == 0 && q > 0) slot[(q - 1) * 16 + e] = __uint_as_float(v1[e]);
+                    for (int dl = 0; dl < G; ++dl) tmem_ld_32x32b_x16(taddr + dl * p.bn + c0, vd[dl]);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) acc_v[e] = __uint_as_float(vd[0][e]);
+                    // column group delta: the right neighbour delta lanes over, or (past lane
+                    // 31) the next warp's first lanes through shared memory
+                    float* slot = xch + (c0 >> 4) * (3 * (G - 1) * (G - 1) * 16);
+#pragma unroll
+                    for (int dl = 1; dl < G; ++dl) {
+                        float* sd = slot + (dl - 1) * (G - 1) * 16;
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const float v = __uint_as_float(vd[dl][e]);
+                            const float nb = __shfl_down_sync(0xffffffffu, v, dl);
+                            if (lane < 32 - dl) acc_v[e] += nb;
+                            if ((int)lane < dl && q > 0)
+                                sd[((q - 1) * (G - 1) * (G - 1) + lane) * 16 + e] = v;
+                        }
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (lane == 31 && q < 3) {
+                    if (q < 3) {
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) nb[e] = slot[q * 16 + e];
+                        for (int dl = 1; dl < G; ++dl) {
+                            if ((int)lane >= 32 - dl) {
+                                const float* sd = slot + (dl - 1) * (G - 1) * 16 +
+                                                  (q * (G - 1) * (G - 1) + (lane + dl - 32)) * 16;
+#pragma unroll
+                                for (int e = 0; e < 16; ++e) acc_v[e] += sd[e];
+                            }
+                        }
                     }
                     if (valid) {
 #pragma unroll
@@ -269,7 +311,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             const int ch = ch0 + c0 + e;
                             if (ch < p.n_rows)
                                 __stcs(o + (int64_t)(c0 + e) * ohw,
-                                       __uint_as_float(v0[e]) + nb[e] + (p.bias ? __ldg(p.bias + ch) : 0.f));
+                                       acc_v[e] + (p.bias ? __ldg(p.bias + ch) : 0.f));
                         }
                     }
                 }
@@ -309,8 +351,9 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     PTB_REQUIRE(pl.cb == 32 && pl.cg == 2, "hconv: needs the 32-channel CTA-pair plan");
     const int64_t Wp = aW + 2 * apw;
     PTB_REQUIRE(Wp <= 256 && kW <= 120, "hconv: padded row too wide for one TMA box");
-    const bool pair = pl.tap_pair;
-    const int cta_span = pair ? 127 : 128;
+    const int G = pl.tap_group;
+    const bool pair = G > 1;
+    const int cta_span = 129 - G;
     // rows a CTA's run (128 + kW - 1 positions from any column) can touch
     const int NR = (int)(1 + (Wp - 1 + 128 + kW - 2) / Wp);
     PTB_REQUIRE(NR <= 256 && N * aH * aW * pl.cin_p < (1ll << 40), "hconv: geometry out of range");
@@ -318,8 +361,9 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     memset(&p, 0, sizeof p);
     // CPS: two channel chunks per stage unless the A stage would not leave room for a ring
     const uint32_t box_a = (uint32_t)(NR * Wp) * 128u;
-    const uint32_t box_b = (uint32_t)align_up((size_t)(pair ? pl.bn : pl.bn / 2), 8) * 128u;
-    const int budget = kSmemLimitH - 1024 - 512 - 8 * 48 * 4;
+    // B per CTA: G*bn/2 rows of the (delta, c) stack (G > 1), else bn/2 rows of one tap
+    const uint32_t box_b = (uint32_t)align_up((size_t)(pair ? G * pl.bn / 2 : pl.bn / 2), 8) * 128u;
+    const int budget = kSmemLimitH - 1024 - 512 - xch_bytes(G, pl.bn);
     int cps = (pl.cin_p / 32) % 2 == 0 ? 2 : 1;
     if (cps == 2 && 2 * 2 * (int)box_a + 4 * 2 * (int)box_b > budget) cps = 1;
     PTB_REQUIRE(2 * (int)box_a + 3 * (int)box_b <= budget, "hconv: shared memory too small for the rings");
@@ -337,11 +381,16 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         const uint64_t kdim = (uint64_t)pl.kdim;
         const uint64_t dims[3] = {32, (uint64_t)pl.n_pad, kdim / 32};
         const uint64_t strides[2] = {kdim * 4, 128};
-        const uint32_t box[3] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2), (uint32_t)cps};
+        // G > 1 loads one tap (bn rows; bn/2 for G = 3's split tap) per request and chunk
+        const uint32_t box[3] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2), (uint32_t)(G <= 2 ? cps : 1)};
         tmap_tiled(&p.tmap_b, wt, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        const uint32_t boxh[3] = {32, (uint32_t)std::max(8, pl.bn / 2), 1};
+        tmap_tiled(&p.tmap_bh, wt, 3, dims, strides, boxh, CU_TENSOR_MAP_SWIZZLE_128B);
     }
     p.zero_tap = (int)pl.taps;
     PTB_REQUIRE(!pair || ((int64_t)pl.taps + 1) * pl.cin_p <= pl.kdim, "hconv: no zero tap packed");
+    PTB_REQUIRE(!pair || (G * pl.bn % 16 == 0 && G * pl.bn <= 256 && (G % 2 == 0 || pl.bn % 16 == 0)),
+                "hconv: bad tap group");
     const HConvTiling tl = hconv_tiling(N, Wp, oH, cta_span);
     PTB_REQUIRE(tl.tiles * (int64_t)pl.n_tiles < (1ll << 31) && tl.P_img < (1ll << 30), "hconv: too many tiles");
     p.N = (int)N;
@@ -368,7 +417,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.stage_a = cps * p.box_a;
     p.stage_b = cps * p.box_b;
     // B ring: enough stages to cover two filter rows' worth of taps; A ring: the rest
-    int sb = std::min(16, std::max(4, pair ? kW + 1 : 2 * kW));
+    int sb = std::min(16, std::max(4, pair ? 2 * (int)ceil_div(kW, G) : 2 * kW));
     while (sb > 3 && budget - sb * (int)p.stage_b < 2 * (int)p.stage_a) --sb;
     int sa = (budget - sb * (int)p.stage_b) / (int)p.stage_a;
     sa = std::min(sa, 8);
@@ -376,7 +425,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.sa = sa;
     p.sb = sb;
     p.tmem_cols = 32;
-    while ((int)p.tmem_cols < (pair ? 4 : 2) * pl.bn) p.tmem_cols <<= 1;
+    while ((int)p.tmem_cols < 2 * G * pl.bn) p.tmem_cols <<= 1;
     PTB_REQUIRE(p.tmem_cols <= 512, "hconv: accumulators exceed TMEM");
     p.out = out;
     p.bias = bias;
@@ -385,19 +434,15 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         p.exp = e ? std::atoi(e) : 0;
     }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
-                        (2 * sa + 2 * sb + 4) * 8 + 16 + 8 * 48 * 4;
+                        (2 * sa + 2 * sb + 4) * 8 + 16 + xch_bytes(G, pl.bn);
     const int units = p.tiles * p.n_tiles;
     const int ncl = std::min(units, sm_count() / 2);
     static bool attr = false;
     if (!attr) {
-        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<1, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
-        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<2, false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
-        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<1, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
-        PTB_CUDA(cudaFuncSetAttribute(umma_hconv_kernel<2, true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
+        for (auto fn : {umma_hconv_kernel<1, 1>, umma_hconv_kernel<1, 2>, umma_hconv_kernel<1, 3>,
+                        umma_hconv_kernel<1, 4>, umma_hconv_kernel<2, 1>, umma_hconv_kernel<2, 2>,
+                        umma_hconv_kernel<2, 3>, umma_hconv_kernel<2, 4>})
+            PTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -413,14 +458,19 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ProfScope prof("umma_conv", st, alg_flops, 0.0);
-    if (pair) {
-        PTB_REQUIRE(p.bn <= 128, "hconv: tap pairing needs <= 128 output channels");
-        if (cps == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<2, true>, p));
-        else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<1, true>, p));
+#define PTB_HCONV_LAUNCH(CPS_, G_) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<CPS_, G_>, p))
+    if (cps == 2) {
+        if (G == 1) PTB_HCONV_LAUNCH(2, 1);
+        else if (G == 2) PTB_HCONV_LAUNCH(2, 2);
+        else if (G == 3) PTB_HCONV_LAUNCH(2, 3);
+        else PTB_HCONV_LAUNCH(2, 4);
     } else {
-        if (cps == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<2, false>, p));
-        else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<1, false>, p));
+        if (G == 1) PTB_HCONV_LAUNCH(1, 1);
+        else if (G == 2) PTB_HCONV_LAUNCH(1, 2);
+        else if (G == 3) PTB_HCONV_LAUNCH(1, 3);
+        else PTB_HCONV_LAUNCH(1, 4);
     }
+#undef PTB_HCONV_LAUNCH
     after_launch("umma_hconv");
 }
 
