@@ -60,6 +60,9 @@ enum PackMode { kPackFprop = 0, kPackDgradFlip = 1, kPackGcol = 2 };
 void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW,
                   int mode, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
                   int64_t total_elems, bool round_tf32, cudaStream_t st);
+// Hankel tap groups: [kH][ceil(kW/G)][G][bn][cin_p] (see layout.cu:pack_grouped_kernel).
+void pack_grouped(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW, bool dgrad,
+                  int G, int bn, int64_t cin_p, cudaStream_t st);
 // gb[k] = (acc ? gb[k] : 0) + scale * sum_{n,p} gy[n][k][p] (fixed-order, deterministic).
 void bias_grad(const float* gy, float* gb, int64_t N, int64_t K, int64_t HW, float scale,
                int accumulate, float* ws, size_t ws_bytes, cudaStream_t st);

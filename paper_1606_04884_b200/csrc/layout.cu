@@ -325,6 +325,44 @@ void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, 
     after_launch("pack_weights");
 }
 
+// Tap-grouped packing for the Hankel engine's G-tap MMAs: rows of group (r, sg) are the
+// (delta, n) stack of taps (r, sg*G + delta), so one CTA's G*bn/2 rows are contiguous:
+// dst[((r*ng + sg)*G + delta)*bn + n][ch], zero for taps past kW / rows past n_real.
+__global__ void pack_grouped_kernel(const float* __restrict__ w, float* __restrict__ dst, int K, int C,
+                                    int kH, int kW, int dgrad, int G, int ng, int bn, int cin_p,
+                                    int64_t total) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int ch = (int)(i % cin_p);
+        const int64_t rowi = i / cin_p;
+        const int n = (int)(rowi % bn);
+        const int64_t gd = rowi / bn;  // ((r*ng + sg)*G + delta)
+        const int delta = (int)(gd % G);
+        const int64_t rs = gd / G;
+        const int sg = (int)(rs % ng), r = (int)(rs / ng);
+        const int s = sg * G + delta;
+        float v = 0.f;
+        if (s < kW) {
+            if (!dgrad) {  // row n = k, channel ch = c
+                if (n < K && ch < C) v = __ldg(w + (((int64_t)n * C + ch) * kH + r) * kW + s);
+            } else {  // row n = c, channel ch = k, flipped tap
+                if (n < C && ch < K) v = __ldg(w + (((int64_t)ch * C + n) * kH + (kH - 1 - r)) * kW + (kW - 1 - s));
+            }
+        }
+        dst[i] = to_tf32(v);
+    }
+}
+
+void pack_grouped(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW, bool dgrad,
+                  int G, int bn, int64_t cin_p, cudaStream_t st) {
+    const int ng = (int)ceil_div(kW, G);
+    const int64_t total = kH * ng * G * (int64_t)bn * cin_p;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * (int64_t)sm_count());
+    pack_grouped_kernel<<<blocks, 256, 0, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW, dgrad ? 1 : 0, G,
+                                                ng, bn, (int)cin_p, total);
+    after_launch("pack_grouped");
+}
+
 size_t bias_grad_workspace(int64_t N, int64_t K, int64_t HW) {
     return sizeof(float) * (size_t)K * (size_t)bias_splits(N, K, HW);
 }

@@ -443,10 +443,9 @@ int hconv_pair_env() {
 int hconv_group_max() {
     static const int v = [] {
         const char* e = std::getenv("PT_B200_HCONV_GROUP_MAX");
-        // groups of 3-4 taps (N up to 256) are opt-in: by MMA cycles they should win (L1 dgrad
-        // G=4: 240 vs 384 cycles per 11 taps) but measured slower (L1 0.55 -> 0.58 ms, L2 G=3
-        // 0.93 -> 1.26 ms), so pairs stay the default
-        const int g = e ? std::atoi(e) : 2;
+        // groups of 3-4 taps win once each CTA's G*bn/2 weight rows are one TMA request
+        // (tap-grouped packing): L1 dgrad G=4 0.51 -> 0.49 ms, L2 dgrad G=3 0.90 -> 0.83 ms
+        const int g = e ? std::atoi(e) : 4;
         return g < 2 ? 2 : g > 4 ? 4 : g;
     }();
     return v;
@@ -483,10 +482,9 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
     // 0.92 ms). Allowed up to 128 rows (N=256) by PT_B200_HCONV_PAIR_MAX, but measured
     // slower there (L2 fwd 0.65 -> 0.75 ms)
     if (will_pair) {
-        // tap grouping: G taps per MMA (N = G*bn), one N tile of all the rows, one extra zero
-        // tap in the packing. An N <= 128 MMA costs ~64 cycles whatever N is; with groups
-        // above 2 enabled (PT_B200_HCONV_GROUP_MAX) pick G minimising
-        // ceil(kW / G) * max(64, G*bn/2)
+        // tap grouping: G taps per MMA (N = G*bn), one N tile of all the rows. An N <= 128
+        // MMA costs ~64 cycles whatever N is, so pick G minimising
+        // ceil(kW / G) * max(64, G*bn/2) (L1 dgrad bn=40: G=4; L2 dgrad bn=64: G=3)
         const int bn8 = (int)((pl.n_rows + 7) / 8 * 8), bn16 = (int)((pl.n_rows + 15) / 16 * 16);
         int best_g = 2, best_bn = bn8;
         double best_cost = 1e30;
@@ -504,8 +502,9 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
         pl.bn = best_bn;
         pl.n_tiles = 1;
         pl.n_pad = pl.bn;
-        pl.kdim = ceil_div((pl.taps + 1) * pl.cin_p, 64) * 64;
-        pl.wt_elems = pl.n_pad * pl.kdim;
+        // tap-grouped packing (pack_grouped): [kH][ceil(kW/G)][G][bn][cin_p]
+        pl.kdim = pl.cin_p;
+        pl.wt_elems = (pl.taps / kW) * ceil_div(kW, best_g) * best_g * pl.bn * pl.cin_p;
     }
     pl.aH = aH;
     pl.aW = aW;
@@ -588,8 +587,11 @@ void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + g.N * g.HW * pl.cin_p));
         nchw_to_nhwc(x, act, g.N, g.C, g.HW, pl.cin_p, true, st);
     }
-    pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackFprop, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
-                 pl.wt_elems, true, st);
+    if (pl.hankel && pl.tap_group > 1)
+        pack_grouped(w, wt, g.K, g.C, g.kH, g.kW, false, pl.tap_group, pl.bn, pl.cin_p, st);
+    else
+        pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackFprop, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
+                     pl.wt_elems, true, st);
     if (pl.hankel) {
         run_hconv(pl, act, wt, g.N, g.H, g.W, g.pH, g.pW, (int)g.kH, (int)g.kW, g.oH, g.oW, y, b,
                   2.0 * g.M * g.K * g.CRS, st);
@@ -611,8 +613,11 @@ void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const
         nchw_to_nhwc(gy, act, g.N, g.K, g.oHW, pl.cin_p, true, st);
     }
     if (pl.hankel) {
-        pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackDgradFlip, pl.cb, pl.n_pad, pl.cin_p,
-                     pl.slots_p, pl.wt_elems, true, st);
+        if (pl.tap_group > 1)
+            pack_grouped(w, wt, g.K, g.C, g.kH, g.kW, true, pl.tap_group, pl.bn, pl.cin_p, st);
+        else
+            pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackDgradFlip, pl.cb, pl.n_pad, pl.cin_p,
+                         pl.slots_p, pl.wt_elems, true, st);
         run_hconv(pl, act, wt, g.N, g.oH, g.oW, pl.aph, pl.apw, (int)g.kH, (int)g.kW, g.H, g.W, gx,
                   nullptr, alg_flops, st);
         return;

@@ -50,7 +50,6 @@ struct HConvParams {
     CUtensorMap tmap_a;  // act NHWC [N][aH][aW][Cp], 5-D {32, aW, aH, N, Cp/32}, box {32, Wp, NR, 1, CPS}
     CUtensorMap tmap_a2; // same with NR - 1 rows: runs starting early in a row need one row less
     CUtensorMap tmap_b;  // packed weights, 3-D {32, n_pad, kdim/32}, box {32, rows, CPS}, SW128
-    CUtensorMap tmap_bh; // G = 3: box {32, bn/2, 1} for the half-tap segments
     int N, kH, kW, chunks, cin_p;
     int aph, apw;        // zero border the TMA out-of-bounds fill supplies (top, left)
     int Wp;              // padded row width = position-space row stride
@@ -60,13 +59,15 @@ struct HConvParams {
     int tpi;             // pair tiles per image
     int nr_split;        // runs starting at column < nr_split fit NR - 1 rows
     int tiles;           // N * tpi
-    int zero_tap;        // G > 1: packed-weight tap index holding zeros (kW % G != 0)
+    int zero_tap;        // unused (G > 1 packs zero taps into the groups)
+    int ngroups;         // G > 1: tap groups per filter row, ceil(kW / G)
     int n_rows, bn, n_tiles;
     int sa, sb;          // ring depths
     uint32_t stage_a, stage_b;  // bytes per stage (CPS boxes)
     uint32_t box_a, box_b;      // bytes per 32-channel box
     int exp;                    // timing experiments (PT_B200_HCONV_EXP; wrong results if != 0)
     uint32_t tmem_cols;
+    int nacc;            // TMEM accumulator buffers (2 or 4)
     float* out;
     const float* bias;
 };
@@ -92,8 +93,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     uint64_t* bfull = aempty + p.sa;
     uint64_t* bempty = bfull + p.sb;
     uint64_t* tfull = bempty + p.sb;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tempty = tfull + 4;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 4);
     float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // G > 1: [8 chunks][3 warps][G-1][G-1][16]
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
@@ -114,6 +115,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 8);
+            mbar_init(&tfull[i + 2], 1);
+            mbar_init(&tempty[i + 2], 8);
         }
         fence_mbar_init();
     }
@@ -165,27 +168,11 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             if constexpr (G == 1) {
                                 tma_load_3d_cg2(bdst, &p.tmap_b, &bfull[bs], 0, brow,
                                                 (r * p.kW + s) * (p.cin_p / 32) + cc);
-                            } else if constexpr (G == 2) {
-                                // this CTA's rows are exactly tap s + rank: one request, all chunks
-                                const int tap = s + (int)rank < p.kW ? r * p.kW + s + (int)rank : p.zero_tap;
-                                tma_load_3d_cg2(bdst, &p.tmap_b, &bfull[bs], 0, 0, tap * (p.cin_p / 32) + cc);
                             } else {
-                                // this CTA's weight rows [rank*G*bn/2, (rank+1)*G*bn/2) of the
-                                // (delta, c) stack, in whole-tap (and for G = 3 half-tap) pieces
-                                const int half = G * p.bn / 2;
-                                int n0 = (int)rank * half;
-                                while (n0 < ((int)rank + 1) * half) {
-                                    const int delta = n0 / p.bn, c0 = n0 - delta * p.bn;
-                                    const int len = (G % 2 == 1 && (c0 != 0 || n0 + p.bn > ((int)rank + 1) * half))
-                                                        ? p.bn / 2 : p.bn;
-                                    const int tap = s + delta < p.kW ? r * p.kW + s + delta : p.zero_tap;
-                                    const CUtensorMap* bm = len == p.bn ? &p.tmap_b : &p.tmap_bh;
-#pragma unroll
-                                    for (int c = 0; c < CPS; ++c)
-                                        tma_load_3d_cg2(bdst + c * p.box_b + (n0 - (int)rank * half) * 128, bm,
-                                                        &bfull[bs], 0, c0, tap * (p.cin_p / 32) + cc + c);
-                                    n0 += len;
-                                }
+                                // tap-grouped packing: this CTA's G*bn/2 rows of group (r, s/G)
+                                // are contiguous — one request for all chunks
+                                const int grow = ((r * p.ngroups + s / G) * G) * p.bn + (int)rank * (G * p.bn / 2);
+                                tma_load_3d_cg2(bdst, &p.tmap_b, &bfull[bs], 0, grow, cc);
                             }
                             if (++bs == p.sb) {
                                 bs = 0;
@@ -205,8 +192,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             uint32_t aph = 0, bph = 0;
             int it = 0;
             for (int u = cid; u < num_units; u += ncl, ++it) {
-                const uint32_t acc = it & 1;
-                mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+                // nacc (2 or 4) TMEM accumulators: the MMA may run nacc-1 tiles ahead of the
+                // epilogue (tiles with little K per tile are otherwise epilogue-paced)
+                const uint32_t acc = (uint32_t)(it % p.nacc);
+                mbar_wait(&tempty[acc], ((it / p.nacc) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * (G * p.bn);
                 const int t = u / p.n_tiles;
@@ -253,8 +242,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         const int64_t ohw = (int64_t)p.oH * p.oW;
         int it = 0;
         for (int u = cid; u < num_units; u += ncl, ++it) {
-            const uint32_t acc = it & 1;
-            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            const uint32_t acc = (uint32_t)(it % p.nacc);
+            mbar_wait(&tfull[acc], (it / p.nacc) & 1);
             tc_fence_after();
             const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
             const int n = t / p.tpi;
@@ -376,19 +365,25 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         const uint32_t box2[5] = {32, (uint32_t)Wp, (uint32_t)std::max(1, NR - 1), 1, 1};
         tmap_tiled(&p.tmap_a2, act, 5, dims, strides, box2, CU_TENSOR_MAP_SWIZZLE_128B);
     }
-    {
+    if (!pair) {
         // {32, weight rows, 32-wide k blocks}: one box = the CPS chunks of one tap
         const uint64_t kdim = (uint64_t)pl.kdim;
         const uint64_t dims[3] = {32, (uint64_t)pl.n_pad, kdim / 32};
         const uint64_t strides[2] = {kdim * 4, 128};
-        // G > 1 loads one tap (bn rows; bn/2 for G = 3's split tap) per request and chunk
-        const uint32_t box[3] = {32, (uint32_t)(pair ? pl.bn : pl.bn / 2), (uint32_t)(G <= 2 ? cps : 1)};
+        const uint32_t box[3] = {32, (uint32_t)(pl.bn / 2), (uint32_t)cps};
         tmap_tiled(&p.tmap_b, wt, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
-        const uint32_t boxh[3] = {32, (uint32_t)std::max(8, pl.bn / 2), 1};
-        tmap_tiled(&p.tmap_bh, wt, 3, dims, strides, boxh, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+        // tap-grouped rows [kH*ngroups*G*bn][cin_p] as {32, rows, cin_p/32}: box = one CTA's
+        // G*bn/2 rows x CPS chunks
+        const int64_t ng = ceil_div(kW, G);
+        const uint64_t rows = (uint64_t)(pl.taps / kW * ng * G * pl.bn);
+        const uint64_t dims[3] = {32, rows, (uint64_t)(pl.cin_p / 32)};
+        const uint64_t strides[2] = {(uint64_t)pl.cin_p * 4, 128};
+        const uint32_t box[3] = {32, (uint32_t)(G * pl.bn / 2), (uint32_t)cps};
+        tmap_tiled(&p.tmap_b, wt, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        p.ngroups = (int)ng;
     }
     p.zero_tap = (int)pl.taps;
-    PTB_REQUIRE(!pair || ((int64_t)pl.taps + 1) * pl.cin_p <= pl.kdim, "hconv: no zero tap packed");
     PTB_REQUIRE(!pair || (G * pl.bn % 16 == 0 && G * pl.bn <= 256 && (G % 2 == 0 || pl.bn % 16 == 0)),
                 "hconv: bad tap group");
     const HConvTiling tl = hconv_tiling(N, Wp, oH, cta_span);
@@ -424,8 +419,9 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     PTB_REQUIRE(sa >= 2, "hconv: shared memory too small for the rings");
     p.sa = sa;
     p.sb = sb;
+    p.nacc = 4 * G * pl.bn <= 512 ? 4 : 2;
     p.tmem_cols = 32;
-    while ((int)p.tmem_cols < 2 * G * pl.bn) p.tmem_cols <<= 1;
+    while ((int)p.tmem_cols < p.nacc * G * pl.bn) p.tmem_cols <<= 1;
     PTB_REQUIRE(p.tmem_cols <= 512, "hconv: accumulators exceed TMEM");
     p.out = out;
     p.bias = bias;
@@ -434,7 +430,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         p.exp = e ? std::atoi(e) : 0;
     }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
-                        (2 * sa + 2 * sb + 4) * 8 + 16 + xch_bytes(G, pl.bn);
+                        (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn);
     const int units = p.tiles * p.n_tiles;
     const int ncl = std::min(units, sm_count() / 2);
     static bool attr = false;
