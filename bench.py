@@ -363,6 +363,14 @@ def main():
                 v = L.profile_read(f"{cls}@{s_['name']}.{ps}")
                 if v[1] > 0:
                     per[f"{cls}@{s_['name']}.{ps}"] = v
+    # HBM-bound layout passes (NCHW<->NHWC, space-to-depth) per (layer, pass)
+    lay = {}
+    for s_ in st:
+        for ps in ("fwd", "bwd", "dgrad", "wgrad"):
+            v = L.profile_read(f"layout@{s_['name']}.{ps}")
+            if v[1] > 0:
+                lay[f"{s_['name']}.{ps}"] = {"ms": v[0] / args.steps, "launches": v[1] // args.steps,
+                                             "gbs": v[3] / (v[0] * 1e-3) / 1e9 if v[0] > 0 else None}
     L.lib().pt_b200_profile_enable(0)
     tf32_cublas = measure_cublas_tf32(torch) if rank == 0 else None
     tf32_derived = peaks.get("bf16_tflops", 1590.0) / 2.0
@@ -404,6 +412,7 @@ def main():
                         if v[0] > 0 and v[2] > 0 else None,
                         "gbs": (v[3] / (v[0] * 1e-3) / 1e9) if v[0] > 0 and v[3] > 0 else None}
                     for c, v in prof.items()},
+        "layout_per_pass": lay,
     }
 
     # e2e through the public API with HOST buffers (pinned), copies inside the timed region

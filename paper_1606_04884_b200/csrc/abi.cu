@@ -140,7 +140,8 @@ size_t bwd_ws(const Geo& g, int math) {
 // accumulate), gb takes (bscale, bacc) — equal except under the s2d wrapper, whose remap
 // applies the caller's scale to gw.
 void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, float* gb, float scale,
-                     int accumulate, int math, char* ws, cudaStream_t st, float bscale, int bacc) {
+                     int accumulate, int math, char* ws, cudaStream_t st, float bscale, int bacc,
+                     const float* xh_pre = nullptr) {
     PassScope pass("wgrad");
     if (wgrad_tc(g, math)) {
         float* gyh = reinterpret_cast<float*>(ws);
@@ -150,7 +151,7 @@ void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, f
             nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, bscale, bacc, part, st);
         }
         wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, ws + gyh_bytes(g) + bias_part_bytes(g),
-                     st);
+                     st, xh_pre);
         return;
     }
     simt_conv_bwd_filter(g, x, gy, gw, scale, accumulate, reinterpret_cast<float*>(ws), st);
@@ -167,8 +168,14 @@ bool s2d_on(const Geo& g, int math);
 // Here it is the forward engine's NHWC copy of x, shareable when the weight-gradient
 // kernel reads the same layout (32-channel chunks; a Hankel forward's copy carries its
 // zero border, which the wgrad im2col descriptor absorbs). 0 = not shareable.
+int64_t s2d_fwd_cp(const Geo& g, int math);
 size_t finput_layout(const Geo& g, int math, int64_t* ph = nullptr, int64_t* pw = nullptr) {
-    if (math != PT_MATH_TF32 || s2d_on(g, math) || fwd_rowconv(g, math) || wgrad_row(g, math) ||
+    if (s2d_on(g, math)) {
+        // the space-to-depth input x', NHWC (written by the forward, read by the wgrad)
+        const Geo e = s2d_geo(g);
+        return s2d_fwd_cp(g, math) ? finput_layout(e, math, ph, pw) : 0;
+    }
+    if (math != PT_MATH_TF32 || fwd_rowconv(g, math) || wgrad_row(g, math) ||
         !umma_wgrad_ok(g))
         return 0;
     const UmmaPlan pl = umma_plan(g, false);
@@ -200,9 +207,18 @@ bool s2d_on(const Geo& g, int math) {
     static const bool off = std::getenv("PT_B200_NO_S2D") != nullptr;  // A/B switch
     return math == PT_MATH_TF32 && !off && s2d_applies(g);
 }
-size_t s2d_x_bytes(const Geo& g) {
+size_t s2d_x_bytes(const Geo& g) {  // x' as NCHW or as NHWC with 32-padded channels
     const Geo e = s2d_geo(g);
-    return align_up((size_t)(e.N * e.C * e.HW) * 4, 256);
+    return align_up((size_t)(e.N * (e.C + 31) / 32 * 32 * e.HW) * 4, 256);
+}
+// Cp of the NHWC x' the stride-1 plan reads when s2d_input_nhwc can write it directly
+// (32-channel-chunk tensor-core plan), else 0 (x' as NCHW, relaid by the engine).
+int64_t s2d_fwd_cp(const Geo& g, int math) {
+    const Geo e = s2d_geo(g);
+    if (fwd_rowconv(e, math)) return 0;
+    const UmmaPlan pl = umma_plan(e, false);
+    if (!pl.ok || pl.cb != 32 || !s2d_nhwc_ok(g, pl.cin_p)) return 0;
+    return pl.cin_p;
 }
 size_t s2d_w_bytes(const Geo& g) {
     const Geo e = s2d_geo(g);
@@ -260,8 +276,10 @@ void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, flo
         }
         if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
         if (gw) {
-            if (inner_gw_plain) bwd_filter_impl(g, x, gy, gw, gb, 1.f, 0, math, base, st, scale, accumulate);
-            else bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st, scale, accumulate);
+            if (inner_gw_plain)
+                bwd_filter_impl(g, x, gy, gw, gb, 1.f, 0, math, base, st, scale, accumulate, finput);
+            else
+                bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st, scale, accumulate, finput);
         }
 }
 
@@ -407,9 +425,18 @@ static int conv_fwd_entry(const pt_conv_geom* gp, const float* x, const float* w
             char* base = reinterpret_cast<char*>(ws);
             float* xs = reinterpret_cast<float*>(base);
             float* wsd = reinterpret_cast<float*>(base + s2d_x_bytes(g));
+            char* inner = base + s2d_x_bytes(g) + s2d_w_bytes(g);
+            if (const int64_t cp = s2d_fwd_cp(g, math)) {
+                // x' straight into the engine's NHWC layout (into finput when shareable)
+                float* xh = finput && finput_layout(g, math) ? finput : xs;
+                s2d_input_nhwc(g, x, xh, cp, st);
+                s2d_weight(g, w, wsd, st);
+                umma_conv_fwd(e, umma_plan(e, false), nullptr, wsd, b, y, inner, st, xh, true);
+                return;
+            }
             s2d_input(g, x, xs, st);
             s2d_weight(g, w, wsd, st);
-            fwd_core(e, xs, wsd, b, y, math, base + s2d_x_bytes(g) + s2d_w_bytes(g), st);
+            fwd_core(e, xs, wsd, b, y, math, inner, st);
             return;
         }
         fwd_core(g, x, w, b, y, math, ws, st, finput);
@@ -478,9 +505,11 @@ int pt_b200_conv_bwd_filter(const pt_conv_geom* gp, const float* x, const float*
             char* base = reinterpret_cast<char*>(ws);
             float* xs = reinterpret_cast<float*>(base);
             float* gws = reinterpret_cast<float*>(base + s2d_x_bytes(g));
-            s2d_input(g, x, xs, st);
+            const int64_t cp = finput_layout(g, math) ? s2d_fwd_cp(g, math) : 0;
+            if (cp) s2d_input_nhwc(g, x, xs, cp, st);
+            else s2d_input(g, x, xs, st);
             bwd_filter_impl(e, xs, gy, gws, gb, 1.f, 0, math, base + s2d_x_bytes(g) + s2d_w_bytes(g), st,
-                            scale, accumulate);
+                            scale, accumulate, cp ? xs : nullptr);
             d2s_weight_grad(g, gws, gw, scale, accumulate, st);
             return;
         }
@@ -510,10 +539,21 @@ static int conv_bwd_entry(const pt_conv_geom* gp, const float* x, const float* g
             float* gxs = reinterpret_cast<float*>(base + s2d_x_bytes(g) + s2d_w_bytes(g));
             float* gws = reinterpret_cast<float*>(base + 2 * s2d_x_bytes(g) + s2d_w_bytes(g));
             char* inner = base + 2 * s2d_x_bytes(g) + 2 * s2d_w_bytes(g);
-            if (gw) s2d_input(g, x, xs, st);
+            // x' for the wgrad: the forward's NHWC copy (finput), else made here
+            const float* xh = nullptr;
+            if (gw && finput_layout(g, math)) {
+                if (finput) {
+                    xh = finput;
+                } else {
+                    s2d_input_nhwc(g, x, xs, s2d_fwd_cp(g, math), st);
+                    xh = xs;
+                }
+            } else if (gw) {
+                s2d_input(g, x, xs, st);
+            }
             if (gx) s2d_weight(g, w, wsd, st);
             bwd_core(e, xs, gy, wsd, gx ? gxs : nullptr, gw ? gws : nullptr, gb, scale, accumulate, math,
-                     inner, st, /*inner_gw_plain=*/true);
+                     inner, st, /*inner_gw_plain=*/true, xh);
             if (gx) d2s_grad(g, gxs, gx, st);
             if (gw) d2s_weight_grad(g, gws, gw, scale, accumulate, st);
             return;

@@ -111,8 +111,10 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
 UmmaPlan umma_plan(const Geo& g, bool dgrad);
 // act_out: where the NHWC activation copy goes (Torch's finput, reused by the weight
 // gradient); null = the workspace.
+// act_ready: act_out already holds that copy (x unused).
 void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float* w,
-                   const float* b, float* y, void* ws, cudaStream_t st, float* act_out = nullptr);
+                   const float* b, float* y, void* ws, cudaStream_t st, float* act_out = nullptr,
+                   bool act_ready = false);
 // gyh_pre: gy already in the plan's NHWC layout (TF32-rounded; zero-bordered when
 // pl.hankel), or null to transform here.
 void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const float* w,
@@ -160,6 +162,9 @@ int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 bool s2d_applies(const Geo& g);
 Geo s2d_geo(const Geo& g);  // the equivalent stride-1 conv over C*s*s channels
 void s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st);
+// x' directly in NHWC with Cp (zero-padded, TF32-rounded) channels: the engines' layout
+bool s2d_nhwc_ok(const Geo& g, int64_t Cp);
+void s2d_input_nhwc(const Geo& g, const float* x, float* xh, int64_t Cp, cudaStream_t st);
 void s2d_weight(const Geo& g, const float* w, float* ws, cudaStream_t st);
 void d2s_grad(const Geo& g, const float* gxs, float* gx, cudaStream_t st);
 void d2s_weight_grad(const Geo& g, const float* gws, float* gw, float scale, int accumulate,

@@ -43,6 +43,79 @@ __global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict_
     }
 }
 
+__device__ __forceinline__ float to_tf32_s2d(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+}
+
+// x' straight into the tensor-core engines' NHWC layout, channels zero-padded to Cp and
+// rounded to TF32 (what s2d_input + nchw_to_nhwc produce, in one HBM pass). One block per
+// (n, I): the C*S input rows s*I + a - pH are staged in smem (coalesced), then the Ws x Cp
+// output row is written as float4 channel quads (Cp % 4 == 0; S = 4 or 8: a quad is
+// four b phases of one (c, a); S = 2: two (c, a) pairs).
+template <int S>
+__global__ void s2d_input_nhwc_kernel(const float* __restrict__ x, float4* __restrict__ xh, int C, int H,
+                                      int W, int pH, int pW, int Hs, int Ws, int Cp, int vec_load) {
+    extern __shared__ float tile[];  // [C*S][Ws*S]
+    const int I = blockIdx.x % Hs;
+    const int n = blockIdx.x / Hs;
+    const int Wt = Ws * S;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x, nthr = blockDim.x * blockDim.y;
+    // padded columns t < pW or t >= pW + W read as zero
+    const int lo = pW < Wt ? pW : Wt, hi = pW + W < Wt ? pW + W : Wt;
+    for (int e = tid; e < C * S * (Wt - (hi - lo)); e += nthr) {
+        const int nb = Wt - (hi - lo), ca = e / nb, k = e - ca * nb;
+        tile[ca * Wt + (k < lo ? k : k + (hi - lo))] = 0.f;
+    }
+    if (vec_load) {  // W % 4 == 0 and x 16-byte aligned: float4 loads, several in flight
+        const int nq = W / 4;
+#pragma unroll 4
+        for (int e = tid; e < C * S * nq; e += nthr) {
+            const int ca = e / nq, q = e - ca * nq;
+            const int c = ca / S, a = ca - c * S;
+            const int h = S * I + a - pH;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (h >= 0 && h < H) v = __ldg(reinterpret_cast<const float4*>(x + (((int64_t)n * C + c) * H + h) * W) + q);
+            float* t = tile + ca * Wt + pW + 4 * q;
+            const int room = Wt - (pW + 4 * q);
+            if (room >= 4) {
+                t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+            } else {
+                if (room > 0) t[0] = v.x;
+                if (room > 1) t[1] = v.y;
+                if (room > 2) t[2] = v.z;
+            }
+        }
+    } else {  // one (c, a) row per threadIdx.y, threads sweep the columns
+        for (int ca = threadIdx.y; ca < C * S; ca += blockDim.y) {
+            const int c = ca / S, a = ca - c * S;
+            const int h = S * I + a - pH;
+            if (h < 0 || h >= H) {
+                for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) tile[ca * Wt + t] = 0.f;
+                continue;
+            }
+            const float* src = x + (((int64_t)n * C + c) * H + h) * W - pW;
+#pragma unroll 4
+            for (int t = lo + threadIdx.x; t < hi; t += blockDim.x) tile[ca * Wt + t] = __ldg(src + t);
+        }
+    }
+    __syncthreads();
+    const int Cs = C * S * S, q4 = Cp / 4;
+    float4* dst = xh + ((int64_t)n * Hs + I) * Ws * q4;
+    for (int e = tid; e < Ws * q4; e += nthr) {
+        const int J = e / q4, ch0 = (e - J * q4) * 4;
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int ch = ch0 + u;
+            const int ca = ch / S, b = ch - ca * S;
+            v[u] = ch < Cs ? to_tf32_s2d(tile[ca * Wt + J * S + b]) : 0.f;
+        }
+        dst[e] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 __global__ void s2d_weight_kernel(const float* __restrict__ w, float* __restrict__ ws, int64_t K, int C,
                                   int kH, int kW, int s, int kHs, int kWs) {
     const int Cs = C * s * s;
@@ -134,6 +207,31 @@ void s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st) {
     else PTB_S2D_IN(8);
 #undef PTB_S2D_IN
     after_launch("s2d_input");
+}
+
+bool s2d_nhwc_ok(const Geo& g, int64_t Cp) {
+    const Geo e = s2d_geo(g);
+    return Cp % 4 == 0 && Cp >= e.C && (size_t)(g.C * g.sH * e.W * g.sH) * 4 <= 48 * 1024 &&
+           g.N * e.H < (1ll << 31);
+}
+
+void s2d_input_nhwc(const Geo& g, const float* x, float* xh, int64_t Cp, cudaStream_t st) {
+    const Geo e = s2d_geo(g);
+    PTB_REQUIRE(s2d_nhwc_ok(g, Cp), "s2d_input_nhwc: unsupported geometry");
+    ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + e.N * e.HW * Cp));
+    const size_t smem = (size_t)(g.C * g.sH * e.W * g.sH) * 4;
+    const dim3 blk(64, 4);
+#define PTB_S2D_NHWC(S_)                                                                                  \
+    s2d_input_nhwc_kernel<S_><<<(unsigned)(g.N * e.H), blk, smem, st>>>(                                    \
+        x, reinterpret_cast<float4*>(xh), (int)g.C, (int)g.H, (int)g.W, (int)g.pH, (int)g.pW, (int)e.H, \
+        (int)e.W, (int)Cp, vec)
+    const int vec = (g.W % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) ? 1 : 0;
+    if (g.sH == 2) PTB_S2D_NHWC(2);
+    else if (g.sH == 3) PTB_S2D_NHWC(3);
+    else if (g.sH == 4) PTB_S2D_NHWC(4);
+    else PTB_S2D_NHWC(8);
+#undef PTB_S2D_NHWC
+    after_launch("s2d_input_nhwc");
 }
 
 void s2d_weight(const Geo& g, const float* w, float* ws, cudaStream_t st) {

@@ -153,6 +153,8 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
                     uint8_t* b = sB + (size_t)stage * p.stage_b;
                     if constexpr (CG == 2) {
                         if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+                        // the stage's SPS consecutive 32-wide k slots of B: one 3-D box
+                        tma_load_3d_cg2(b, &p.tmap_b, &full[stage], 0, brow, slot);
 #pragma unroll
                         for (int t = 0; t < SPS; ++t) {
                             // past the last k-slot: any valid tap (the weights there are 0 / OOB)
@@ -161,8 +163,6 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
                                                    live ? kc.cc * 32 : 0, wc, hc, n0,
                                                    (uint16_t)(live ? kc.s : 0),
                                                    (uint16_t)(live ? kc.r : 0));
-                            tma_load_2d_cg2(b + t * (p.stage_b / SPS), &p.tmap_b, &full[stage],
-                                            slot * 32, brow);
                             ++slot;
                             kc.next(p.chunks, p.kW);
                         }
@@ -329,8 +329,15 @@ void launch_k(const UConvParams& p, int grid, size_t smem, cudaStream_t st) {
     PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_conv_kernel<CB, CG, SPS>, p));
 }
 
-void encode_weights(CUtensorMap* m, const float* wt, const UmmaPlan& pl) {
-    if (pl.cb == 32) {
+void encode_weights(CUtensorMap* m, const float* wt, const UmmaPlan& pl, int sps) {
+    if (pl.cb == 32 && pl.cg == 2) {
+        // [k slot][bn/2 rows][32]: a stage's sps slots in one request (OOB slots read 0)
+        const uint64_t kdim = (uint64_t)(ceil_div(pl.taps * pl.cin_p, 64) * 64);
+        const uint64_t dims[3] = {32, (uint64_t)pl.n_pad, kdim / 32};
+        const uint64_t strides[2] = {kdim * 4, 128};
+        const uint32_t box[3] = {32, (uint32_t)(pl.bn / 2), (uint32_t)sps};
+        tmap_tiled(m, wt, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else if (pl.cb == 32) {
         const uint64_t kdim = (uint64_t)(ceil_div(pl.taps * pl.cin_p, 64) * 64);
         const uint64_t dims[2] = {kdim, (uint64_t)pl.n_pad};
         const uint64_t strides[1] = {kdim * 4};
@@ -353,7 +360,6 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
     memset(&p, 0, sizeof p);
     tmap_im2col(&p.tmap_a, act, N, aH, aW, pl.cin_p, kH, kW, pH, pW, sH, sW, pl.cb, kTileM,
                 pl.cb == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
-    encode_weights(&p.tmap_b, wt, pl);
     const int64_t M = N * oH * oW;
     PTB_REQUIRE(M < (1ll << 31), "umma conv: too many output pixels");
     p.M = (int)M;
@@ -372,6 +378,7 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
                         ? ((conv_sps_env() == 4 && 2 * 4 * (kBoxA + b_slot) <= (uint32_t)kSmemLimit - 2048) ? 4 : 2)
                         : 0;
     const int slots_per_stage = pl.cb == 32 ? (pl.cg == 2 ? sps : 1) : 8;
+    encode_weights(&p.tmap_b, wt, pl, sps);
     p.num_kb = (int)ceil_div(p.slots, slots_per_stage);
     p.n_rows = (int)pl.n_rows;
     p.bn = pl.bn;
@@ -580,10 +587,11 @@ UmmaPlan umma_plan(const Geo& g, bool dgrad) {
 }
 
 void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float* w,
-                   const float* b, float* y, void* ws, cudaStream_t st, float* act_out) {
+                   const float* b, float* y, void* ws, cudaStream_t st, float* act_out, bool act_ready) {
     float* act = act_out ? act_out : reinterpret_cast<float*>(ws);
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
-    {
+    PTB_REQUIRE(!act_ready || act_out, "umma_conv_fwd: act_ready without act_out");
+    if (!act_ready) {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + g.N * g.HW * pl.cin_p));
         nchw_to_nhwc(x, act, g.N, g.C, g.HW, pl.cin_p, true, st);
     }

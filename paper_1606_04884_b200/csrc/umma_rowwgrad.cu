@@ -101,9 +101,11 @@ __global__ void expand_filter_v_kernel(const float* __restrict__ w, float* __res
 }
 
 // gx[n][c][h][w] = sum_{r=0..kH-1} gxe[n][r*C + c][h + pH - r][w + pW]   (r in fixed order)
-// gxe: [N][kH*C][oH][Wp]. One gx row per (blockIdx.x, threadIdx.y); threads sweep w.
+// gxe: [N][kH*C][oH][Wp]. One gx row per (blockIdx.x, threadIdx.y); each thread owns four
+// consecutive w, so every tap issues four independent loads (kH as small as 3 would
+// otherwise leave too few bytes in flight to cover HBM latency).
 __global__ void fold_cols_kernel(const float* __restrict__ gxe, float* __restrict__ gx, int rows, int C,
-                                 int H, int W, int oH, int Wp, int kH, int pH, int pW) {
+                                 int H, int W, int oH, int Wp, int kH, int pH, int pW, int vec_store) {
     const int row = blockIdx.x * blockDim.y + threadIdx.y;  // (n, c, h)
     if (row >= rows) return;
     const int h = row % H;
@@ -112,14 +114,25 @@ __global__ void fold_cols_kernel(const float* __restrict__ gxe, float* __restric
     const int64_t plane = (int64_t)oH * Wp;
     const float* src = gxe + ((int64_t)n * kH * C + c) * plane + pW;
     float* dst = gx + (int64_t)row * W;
-    for (int w = threadIdx.x; w < W; w += blockDim.x) {
-        float acc = 0.f;
+    const int r0 = max(0, h + pH - oH + 1), r1 = min(kH, h + pH + 1);  // taps with a valid row
+    for (int w0 = threadIdx.x * 4; w0 < W; w0 += blockDim.x * 4) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        const bool full = w0 + 4 <= W;
 #pragma unroll 4
-        for (int r = 0; r < kH; ++r) {
-            const int i = h + pH - r;
-            if (i >= 0 && i < oH) acc += __ldg(src + (int64_t)r * C * plane + (int64_t)i * Wp + w);
+        for (int r = r0; r < r1; ++r) {
+            const float* p = src + (int64_t)r * C * plane + (int64_t)(h + pH - r) * Wp + w0;
+            if (full) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc[u] += __ldg(p + u);
+            } else {
+                for (int u = 0; u < W - w0; ++u) acc[u] += __ldg(p + u);
+            }
         }
-        dst[w] = acc;
+        if (full && vec_store) {
+            *reinterpret_cast<float4*>(dst + w0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        } else {
+            for (int u = 0; u < 4 && w0 + u < W; ++u) dst[w0 + u] = acc[u];
+        }
     }
 }
 
@@ -244,9 +257,10 @@ void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws
     ProfScope prof("layout", st, 0.0, 4.0 * (e.N * e.C * e.H * e.W + total));
     if (vert) {
         const int rows = (int)(g.N * g.C * g.H);
-        const int tx = g.W >= 128 ? 128 : g.W >= 64 ? 64 : 32;
+        const int tx = g.W >= 512 ? 128 : g.W >= 256 ? 64 : 32;  // 4 columns per thread
         fold_cols_kernel<<<(unsigned)ceil_div(rows, 256 / tx), dim3(tx, 256 / tx), 0, st>>>(
-            gxe, gx, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.oH, (int)e.W, (int)g.kH, (int)g.pH, (int)g.pW);
+            gxe, gx, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.oH, (int)e.W, (int)g.kH, (int)g.pH, (int)g.pW,
+            (g.W % 4 == 0 && (reinterpret_cast<uintptr_t>(gx) & 15) == 0) ? 1 : 0);
         after_launch("fold_cols");
         return;
     }
