@@ -25,8 +25,10 @@
 // (weight tiles, one per (r, s, chunk)); the MMA issuer consumes kW B stages per A stage.
 // TMEM holds two BN-column accumulators so the epilogue of tile t overlaps tile t+1.
 //
-// Warp roles (192 threads, 1 CTA/SM, persistent): warp 0 TMA producer, warp 1 TMEM
-// allocator + MMA issuer (pair leader), warps 2..5 epilogue (TMEM -> +bias -> NCHW).
+// Warp roles (320 threads, 1 CTA/SM, persistent): warp 0 TMA producer, warp 1 TMEM
+// allocator + MMA issuer (pair leader), warps 2..9 epilogue (TMEM -> +bias -> NCHW): two
+// warps per TMEM lane quarter, each draining half of the column chunks (layers with a
+// short reduction are epilogue-paced: AlexNet conv1 as s2d spends ~3x its MMA time there).
 #include <cuda.h>
 
 #include <cstdlib>
@@ -41,10 +43,12 @@ namespace {
 
 using namespace umma;
 
-constexpr int kThreadsH = 192;
+constexpr int kThreadsH = 320;
 constexpr int kSmemLimitH = 232448;
-// epilogue neighbour exchange: [bn/16 chunks][3 warps][G-1 deltas][G-1 lanes][16] floats
-inline int xch_bytes(int G, int bn) { return G > 1 ? (bn / 16 + 1) * 3 * (G - 1) * (G - 1) * 16 * 4 : 0; }
+// epilogue neighbour exchange: [tile parity][bn/16 chunks][3 warps][G-1 deltas][G-1 lanes][16]
+// floats (two tile buffers: a warp may write tile t+1's slot while its neighbour still
+// reads tile t's)
+inline int xch_bytes(int G, int bn) { return G > 1 ? 2 * ((bn + 15) / 16) * 3 * (G - 1) * (G - 1) * 16 * 4 : 0; }
 
 struct HConvParams {
     CUtensorMap tmap_a;  // act NHWC [N][aH][aW][Cp], 5-D {32, aW, aH, N, Cp/32}, box {32, Wp, NR, 1, CPS}
@@ -114,9 +118,9 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 8);
+            mbar_init(&tempty[i], 16);  // 8 epilogue warps x 2 CTAs
             mbar_init(&tfull[i + 2], 1);
-            mbar_init(&tempty[i + 2], 8);
+            mbar_init(&tempty[i + 2], 16);
         }
         fence_mbar_init();
     }
@@ -238,7 +242,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         }
     } else {
         // ===== epilogue: TMEM -> registers -> (+bias) -> NCHW, border columns dropped =====
-        const uint32_t q = warp & 3;
+        const uint32_t q = warp & 3;            // TMEM lane quarter
+        const int half = (int)(warp - 2) >> 2;  // column chunks half, 2*k + half
         const int64_t ohw = (int64_t)p.oH * p.oW;
         int it = 0;
         for (int u = cid; u < num_units; u += ncl, ++it) {
@@ -252,24 +257,30 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             const bool valid = qq < p.m && i < p.oH && j < p.oW && (int)(q * 32 + lane) < kCtaSpan;
             const int ch0 = nt * p.bn;
             const int64_t base = ((int64_t)n * p.n_rows + ch0) * ohw + (int64_t)i * p.oW + j;
+            const uint32_t lane_base = tmem_base + ((q * 32u) << 16);
             if constexpr (G == 1) {
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
-                store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base : 0), ohw, p.bias, ch0,
-                                        p.n_rows, valid);
+                for (int c0 = half * 16; c0 < p.bn; c0 += 32)
+                    store_tmem_columns_nchw(lane_base + acc * p.bn + c0, 16,
+                                            p.out + (valid ? base + (int64_t)c0 * ohw : 0), ohw, p.bias,
+                                            ch0 + c0, p.n_rows, valid);
             } else {
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * G * p.bn;
-                float* o = p.out + (valid ? base : 0);
-                for (int c0 = 0; c0 < p.bn; c0 += 16) {
+                const uint32_t taddr = lane_base + acc * G * p.bn;
+                for (int c0 = half * 16; c0 < p.bn; c0 += 32) {
                     uint32_t vd[G][16];
                     float acc_v[16];
 #pragma unroll
                     for (int dl = 0; dl < G; ++dl) tmem_ld_32x32b_x16(taddr + dl * p.bn + c0, vd[dl]);
+                    const int chb = ch0 + c0;
+                    const bool full16 = chb + 16 <= p.n_rows;
+                    float bv[16];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) bv[e] = (p.bias && chb + e < p.n_rows) ? __ldg(p.bias + chb + e) : 0.f;
                     tmem_ld_wait();
 #pragma unroll
                     for (int e = 0; e < 16; ++e) acc_v[e] = __uint_as_float(vd[0][e]);
                     // column group delta: the right neighbour delta lanes over, or (past lane
                     // 31) the next warp's first lanes through shared memory
-                    float* slot = xch + (c0 >> 4) * (3 * (G - 1) * (G - 1) * 16);
+                    float* slot = xch + ((it & 1) * ((p.bn + 15) >> 4) + (c0 >> 4)) * (3 * (G - 1) * (G - 1) * 16);
 #pragma unroll
                     for (int dl = 1; dl < G; ++dl) {
                         float* sd = slot + (dl - 1) * (G - 1) * 16;
@@ -282,7 +293,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                                 sd[((q - 1) * (G - 1) * (G - 1) + lane) * 16 + e] = v;
                         }
                     }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    // the four lane quarters of this column half (named barrier 1 + half)
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
                     if (q < 3) {
 #pragma unroll
                         for (int dl = 1; dl < G; ++dl) {
@@ -295,12 +307,19 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                         }
                     }
                     if (valid) {
+                        float* o = p.out + base + (int64_t)c0 * ohw;
+                        if (full16) {
 #pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            const int ch = ch0 + c0 + e;
-                            if (ch < p.n_rows)
-                                __stcs(o + (int64_t)(c0 + e) * ohw,
-                                       acc_v[e] + (p.bias ? __ldg(p.bias + ch) : 0.f));
+                            for (int e = 0; e < 16; ++e) {
+                                __stcs(o, acc_v[e] + bv[e]);
+                                o += ohw;
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) {
+                                if (chb + e < p.n_rows) __stcs(o, acc_v[e] + bv[e]);
+                                o += ohw;
+                            }
                         }
                     }
                 }
