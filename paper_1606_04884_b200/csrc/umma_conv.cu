@@ -43,7 +43,7 @@ using namespace umma;
 
 constexpr int kTileM = 128;
 constexpr uint32_t kBoxA = kTileM * 32 * 4;  // 16 KB: 128 px x 32 fp32
-constexpr int kThreadsU = 192;
+constexpr int kThreadsU = 320;  // warps 2..9: epilogue, two per TMEM lane quarter
 constexpr int kSmemLimit = 232448;  // 227 KB opt-in per block on sm_100
 
 struct UConvParams {
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4 * CG);
+            mbar_init(&tempty[i], 8 * CG);
         }
         fence_mbar_init();
     }
@@ -252,7 +252,8 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
         }
     } else {
         // ===== epilogue: TMEM -> registers -> (+bias) -> NCHW =====
-        const uint32_t q = warp & 3;
+        const uint32_t q = warp & 3;            // TMEM lane quarter
+        const int half = (int)(warp - 2) >> 2;  // this warp drains column chunks 2*k + half
         int it = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
             const uint32_t acc = it & 1;
@@ -268,8 +269,11 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
             }
             const int ch0 = nt * p.bn;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.bn;
-            store_tmem_columns_nchw(taddr, p.bn, p.out + (valid ? base + (int64_t)ch0 * p.out_hw : 0),
-                                    p.out_hw, p.bias, ch0, p.n_rows, valid);
+            const int nv = ch0 + p.bn < p.n_rows ? ch0 + p.bn : p.n_rows;
+            for (int c0 = half * 16; c0 < p.bn; c0 += 32)
+                store_tmem_columns_nchw(taddr + c0, 16,
+                                        p.out + (valid ? base + (int64_t)(ch0 + c0) * p.out_hw : 0), p.out_hw,
+                                        p.bias, ch0 + c0, nv, valid);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
