@@ -158,6 +158,13 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
                           int64_t xpw = 0);
 int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 
+// ---- umma_swgrad.cu: small-C stride-1 weight gradient (planes of horizontal taps) ----
+bool swgrad_ok(const Geo& g);
+size_t swgrad_workspace(const Geo& g);
+// gyh: gy NHWC with (K+31)/32*32 channels, TF32-rounded (the shared backward transform)
+void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float scale, int accumulate, void* ws,
+            cudaStream_t st);
+
 // ---- s2d.cu: space-to-depth for strided small-C layers ----
 bool s2d_applies(const Geo& g);
 Geo s2d_geo(const Geo& g);  // the equivalent stride-1 conv over C*s*s channels

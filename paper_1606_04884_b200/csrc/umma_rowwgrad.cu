@@ -278,6 +278,7 @@ bool rowwgrad_ok(const Geo& g) {
 }
 
 size_t rowwgrad_workspace(const Geo& g) {
+    if (swgrad_ok(g)) return swgrad_workspace(g);
     const int64_t Ce = ce_of(g);
     const Geo e = expanded_geo(g, Ce);
     return align_up((size_t)(g.N * g.H * g.oW * Ce) * 4, 256) + align_up((size_t)(g.K * Ce * g.kH) * 4, 256) +
@@ -286,6 +287,10 @@ size_t rowwgrad_workspace(const Geo& g) {
 
 void rowwgrad(const Geo& g, const float* x, const float* gyh, float* gw, float scale, int accumulate,
               void* ws, cudaStream_t st) {
+    if (swgrad_ok(g)) {  // planes of horizontal taps, one B box per row group (umma_swgrad.cu)
+        swgrad(g, x, gyh, gw, scale, accumulate, ws, st);
+        return;
+    }
     const int64_t Ce = ce_of(g);
     const Geo e = expanded_geo(g, Ce);
     char* base = reinterpret_cast<char*>(ws);

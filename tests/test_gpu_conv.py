@@ -237,3 +237,34 @@ def test_hankel_edge_default_engines(g):
     rgw, rgb = po.conv_backward_weight(g, x, gy)
     check_tf32(_h(gw), rgw, "wgrad")
     np.testing.assert_allclose(_h(gb), rgb, rtol=1e-5, atol=1e-4)
+
+
+# small-C stride-1 layers: the planes-of-taps weight gradient (umma_swgrad.cu) — odd
+# output extents, padding, C = 1..4, K not a multiple of 32, two N halves (npad = 512)
+SMALLC_GEOMS = [
+    po.geom(2, 3, 37, 45, 64, 3, 3, 1, 1, 1, 1),       # VGG conv1-like, odd oH / oW
+    po.geom(2, 1, 30, 33, 16, 5, 5, 2, 2, 1, 1),       # C = 1
+    po.geom(1, 4, 21, 70, 128, 7, 7, 3, 3, 1, 1),      # C = 4, K = 128 (all TMEM lanes)
+    po.geom(2, 3, 40, 40, 96, 11, 11, 0, 0, 1, 1),     # L1-like: 363 columns, two N halves
+    po.geom(1, 2, 17, 17, 40, 3, 5, 0, 2, 1, 1),       # rectangular filter, Kp = 64
+    po.geom(1, 4, 30, 40, 32, 11, 11, 1, 1, 1, 1),     # 484 columns: two halves of 256
+    po.geom(3, 3, 12, 12, 8, 1, 1, 0, 0, 1, 1),        # 1x1
+]
+
+
+@pytest.mark.parametrize("g", SMALLC_GEOMS, ids=gstr)
+def test_small_c_weight_gradient(g):
+    pt = _pt()
+    x, w, b, gy = conv_inputs(g, 123)
+    G = _g(g)
+    gw, gb = pt.conv_backward_weight(G, _d(x), _d(gy), math="tf32")
+    rgw, rgb = po.conv_backward_weight(g, x, gy)
+    check_tf32(_h(gw), rgw, "wgrad")
+    np.testing.assert_allclose(_h(gb), rgb, rtol=1e-5, atol=1e-4)
+    # fused backward with Torch's accumulate / scale: gw = gw0 + 0.5 * dW
+    gw0 = po.uniform((g.K, g.C, g.kH, g.kW), 9)
+    gb0 = po.uniform((g.K,), 10)
+    gx, agw, agb = pt.conv_backward(G, _d(x), _d(gy), _d(w), gw=_d(gw0), gb=_d(gb0), scale=0.5,
+                                    accumulate=True, math="tf32")
+    check_tf32(_h(agw) - gw0, 0.5 * rgw, "acc wgrad")
+    check_tf32(_h(gx), po.conv_backward_input(g, gy, w), "dgrad")
