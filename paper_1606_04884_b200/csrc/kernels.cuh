@@ -158,6 +158,16 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
                           int64_t xpw = 0);
 int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 
+// ---- umma_hwgrad.cu: stride-1 wide-filter weight gradient (Hankel tap quads) ----
+bool hwgrad_ok(const Geo& g);
+size_t hwgrad_part_bytes(const Geo& g);
+// xh: x NHWC dense with (C+31)/32*32 channels; gyh: gy NHWC with (K+31)/32*32 channels
+void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, float scale, int accumulate,
+                float* part, double alg_flops, cudaStream_t st);
+// fixed-order split reduce of [split][(r*kW+s)*Cp + c][k] partials into KCRS gw
+void wgrad_reduce_launch(const float* part, float* gw, const Geo& g, int64_t Cp, int splits, int64_t ld,
+                         int64_t split_stride, float scale, int accumulate, cudaStream_t st);
+
 // ---- umma_swgrad.cu: small-C stride-1 weight gradient (planes of horizontal taps) ----
 bool swgrad_ok(const Geo& g);
 size_t swgrad_workspace(const Geo& g);

@@ -49,6 +49,7 @@ struct SWParams {
     int P;            // planes (kW*C)
     int nh, nhalf;    // N split into nh MMAs of nhalf columns
     int items, jbs, rgs;  // work items = N * rgs * jbs
+    int per_cta, rem;     // CTA b takes per_cta (+1 for b < rem) consecutive items
     int stages;
     uint32_t stage_a, stage_b, tx, a_lbo, tmem_cols;
     int K;            // output channels (TMEM lanes written)
@@ -88,8 +89,11 @@ __global__ void __launch_bounds__(kThreadsS, 1) umma_swgrad_kernel(const __grid_
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     // this CTA's contiguous share of the work items
-    const int lo = (int)((int64_t)blockIdx.x * p.items / gridDim.x);
-    const int hi = (int)((int64_t)(blockIdx.x + 1) * p.items / gridDim.x);
+    // (32-bit: a 64-bit division is a call, after which the MMA loop's descriptors land in
+    // vector registers and every MMA pays an R2UR + elect)
+    const int b = (int)blockIdx.x;
+    const int lo = b * p.per_cta + (b < p.rem ? b : p.rem);
+    const int hi = lo + p.per_cta + (b < p.rem ? 1 : 0);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -326,6 +330,8 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
     p.nh = w.nh;
     p.nhalf = w.nhalf;
     p.items = w.items;
+    p.per_cta = w.items / w.ctas;
+    p.rem = w.items % w.ctas;
     p.jbs = w.jbs;
     p.rgs = w.rgs;
     p.stages = w.stages;

@@ -257,6 +257,18 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
     }
 }
 
+}  // namespace
+
+void wgrad_reduce_launch(const float* part, float* gw, const Geo& g, int64_t Cp, int splits, int64_t ld,
+                         int64_t split_stride, float scale, int accumulate, cudaStream_t st) {
+    const int64_t n = g.K * g.CRS;
+    wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256, 0, st>>>(
+        part, gw, g.K, g.C, g.kH, g.kW, Cp, splits, ld, split_stride, scale, accumulate);
+    after_launch("wgrad_reduce");
+}
+
+namespace {
+
 int wgrad_kp_env() {
     static const int v = [] {
         const char* e = std::getenv("PT_B200_WGRAD_KPIX");
@@ -333,8 +345,8 @@ bool umma_wgrad_ok(const Geo& g) {
 
 size_t umma_wgrad_workspace(const Geo& g) {
     const WPlan w = wplan(g);
-    return align_up(w.x_elems * 4, 256) + align_up(w.gy_elems * 4, 256) +
-           align_up(w.part_elems * 4, 256);
+    const size_t part = std::max((size_t)w.part_elems * 4, hwgrad_ok(g) ? hwgrad_part_bytes(g) : (size_t)0);
+    return align_up(w.x_elems * 4, 256) + align_up(w.gy_elems * 4, 256) + align_up(part, 256);
 }
 
 int64_t umma_wgrad_kp(const Geo& g) { return (g.K + 31) / 32 * 32; }
@@ -358,6 +370,10 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     }
     if (xh_pre) xh = const_cast<float*>(xh_pre);
     if (gyh_pre) gyh = const_cast<float*>(gyh_pre);
+    if (xph == 0 && xpw == 0 && hwgrad_ok(g)) {  // wide stride-1 filters: Hankel quads (umma_hwgrad.cu)
+        hwgrad_run(g, xh, gyh, gw, scale, accumulate, part, alg_flops, st);
+        return;
+    }
     UWgradParams p;
     memset(&p, 0, sizeof p);
     {

@@ -82,6 +82,26 @@ __global__ void __launch_bounds__(128, 1) bench(P p, unsigned long long* cyc) {
                 else mma_commit(&dummy);
             }
         }
+        if (p.shift >= 7 && p.shift <= 9) {
+            // MN-major tf32 (SW128 with 32-byte atoms; the wgrad operands): K step = 8 pixel
+            // rows = 1 KB. shift 7: A atoms 16 KB apart (one box per 32 channels); shift 8: A
+            // atoms 128 B apart (Hankel taps, overlapping); shift 9: A MN-major, B K-major SW128
+            const uint32_t idesc2 = idesc_tf32(128 * p.cg, p.n, 1, p.shift == 9 ? 0 : 1);
+            constexpr uint32_t kHiM = desc_hi(512, kSwizzle128B_Base32B), kHiK = desc_hi(1024, kSwizzle128B);
+            const uint32_t alo = desc_lo(a, p.shift == 8 ? 128 : 16384), blo = desc_lo(b, p.shift == 9 ? 16 : 16384);
+            for (int i = 0; i < p.iters; i += 8) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint64_t ad = desc_make(alo + (uint32_t)k * 64u, kHiM);
+                    const uint64_t bd = p.shift == 9 ? desc_make(blo + (uint32_t)(k & 3) * 2u, kHiK)
+                                                     : desc_make(blo + (uint32_t)k * 64u, kHiM);
+                    if (CG == 2) mma_tf32_cg2(tmem, ad, bd, idesc2, 1);
+                    else mma_tf32(tmem, ad, bd, idesc2, 1);
+                }
+                if (CG == 2) mma_commit_cg2(&dummy);
+                else mma_commit(&dummy);
+            }
+        }
         for (int i = 0; i < (p.shift >= 4 ? 0 : p.iters); ++i) {
             // shift 1: Hankel-style row shifts; shift 2: walk 4 distinct 16 KB A stages
             const uint32_t sh = p.shift == 1 ? (uint32_t)(i % 9) * 128u
