@@ -268,3 +268,35 @@ def test_small_c_weight_gradient(g):
                                     accumulate=True, math="tf32")
     check_tf32(_h(agw) - gw0, 0.5 * rgw, "acc wgrad")
     check_tf32(_h(gx), po.conv_backward_input(g, gy, w), "dgrad")
+
+
+# Hankel tap-quad weight gradient (umma_hwgrad.cu) forced on: odd chunk counts (C = 96 ->
+# 3 chunks), K = 320 (two n-tiles), kW = 3 / 5 / 11 (1-3 quads, dropped tap slots), padding,
+# rows split into several 128-column segments, non-square outputs
+HWGRAD_EDGE = [
+    po.geom(2, 96, 15, 21, 320, 9, 9, 4, 4, 1, 1),
+    po.geom(1, 64, 9, 140, 64, 3, 5, 1, 2, 1, 1),
+    po.geom(2, 32, 20, 18, 128, 11, 11, 5, 5, 1, 1),
+    po.geom(3, 64, 12, 12, 96, 3, 3, 1, 1, 1, 1),
+    po.geom(1, 128, 7, 9, 256, 7, 7, 3, 3, 1, 1),
+]
+
+
+def test_hwgrad_forced_edge_geometries():
+    """PT_B200_HWGRAD=2 routes every stride-1 C >= 32 weight gradient through the tap-quad
+    kernel (read once per process, hence the subprocess); TF32 tolerance vs oracle."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW]
+             for g in HWGRAD_EDGE]
+    env = dict(os.environ, PT_B200_HWGRAD="2")
+    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
+                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    errs = json.loads(r.stdout.strip().splitlines()[-1])
+    for g, e in zip(HWGRAD_EDGE, errs):
+        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
