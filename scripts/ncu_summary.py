@@ -54,7 +54,8 @@ def read(path):
 
 def main():
     out_md, tag = sys.argv[1], sys.argv[2]
-    tj = os.path.join(os.path.dirname(out_md), "ncu_traffic.json")
+    # the per-launch DRAM bytes bench.py's roofline reads (profiles/ncu_traffic.json)
+    tj = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "ncu_traffic.json")
     traffic = json.load(open(tj)) if os.path.exists(tj) else {}
     lines = [f"| key | kernel | time (us) | DRAM rd+wr (MB) | TMA loads from L2 (GB, TB/s) | L2 tex % | tensor pipe % | smem TC % |",
              "|---|---|---|---|---|---|---|---|"]
