@@ -4,6 +4,8 @@
 //   * weight packing (KCRS -> implicit-GEMM B operand, optionally flipped for dgrad);
 //   * gradBias, a per-channel reduction of gradOutput (the reference's
 //     reduce over gy.select(1,k), proj/src/reference_backend.cpp:115-127).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace ptb {
@@ -20,7 +22,8 @@ __device__ __forceinline__ float to_tf32(float v) {
 // image, moved as 32x32 tiles (reads coalesced along pixels, writes coalesced along
 // channels). With `part` set it also emits the block's per-channel sums of the
 // UNROUNDED source (the gradBias partials, fixed order -> deterministic):
-// part[(n * strips + strip) * C + c]. grid = (strips, ceil(Cp/32), N), block = 32x8.
+// part[c * (N * strips) + n * strips + strip] (channel-major: the final reduce reads each
+// channel's partials contiguously). grid = (strips, ceil(Cp/32), N), block = 32x8.
 constexpr int kStripPx = 128;
 
 // PAD: destinations are zero-bordered (pixel index remapped); TWO: write d1 as well.
@@ -88,7 +91,7 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ src, NhwcDst d0, N
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             const int64_t c = c0 + threadIdx.y + 8 * i;
-            if (threadIdx.x == 0 && c < C) part[(n * gridDim.x + blockIdx.x) * C + c] = v;
+            if (threadIdx.x == 0 && c < C) part[c * (gridDim.z * gridDim.x) + n * gridDim.x + blockIdx.x] = v;
         }
     }
 }
@@ -122,12 +125,14 @@ __global__ void zero_border_kernel(float4* __restrict__ dst, int64_t N, int Hp, 
     }
 }
 
-// gb[k] = (acc ? gb[k] : 0) + scale * sum_r part[r * K + k], r over N*strips in order.
+// gb[k] = (acc ? gb[k] : 0) + scale * sum_r part[k * rows + r], r over N*strips (each
+// thread's strided share in order, then a fixed tree: deterministic).
 __global__ void bias_from_partials_kernel(const float* __restrict__ part, int64_t rows, int64_t K,
                                           float* __restrict__ gb, float scale, int accumulate) {
     const int64_t k = blockIdx.x;
     float acc = 0.f;
-    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) acc += part[r * K + k];
+    const float* pk = part + k * rows;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) acc += __ldg(pk + r);
     __shared__ float red[32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -158,33 +163,35 @@ __global__ void nchw_to_nhwc_small_kernel(const float* __restrict__ src, float* 
     }
 }
 
+// 32-bit index math throughout (a 64-bit division per element made these packs of a few
+// MB take 10-13 us); the caller guarantees total < 2^31.
 __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restrict__ dst,
-                                    int64_t K, int64_t C, int64_t kH, int64_t kW, int mode,
-                                    int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
-                                    int64_t total, int round_tf32) {
-    const int64_t taps = mode == kPackGcol ? 1 : kH * kW;
-    const int64_t n_real = mode == kPackFprop ? K : (mode == kPackDgradFlip ? C : C * kH * kW);
-    const int64_t cin_real = mode == kPackFprop ? C : K;
-    const int64_t chunks = cin_p / 4;
-    const int64_t kdim_p = total / n_pad;  // layout 32: row stride (>= taps*cin_p)
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t row, tap, ch;
+                                    int K, int C, int kH, int kW, int mode,
+                                    int layout, int n_pad, int cin_p, int slots_p,
+                                    int total, int round_tf32) {
+    const int taps = mode == kPackGcol ? 1 : kH * kW;
+    const int n_real = mode == kPackFprop ? K : (mode == kPackDgradFlip ? C : C * kH * kW);
+    const int cin_real = mode == kPackFprop ? C : K;
+    const int chunks = cin_p / 4;
+    const int kdim_p = total / n_pad;  // layout 32: row stride (>= taps*cin_p)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        int row, tap, ch;
         if (layout == 32) {
             row = i / kdim_p;
-            const int64_t kd = i - row * kdim_p;
+            const int kd = i - row * kdim_p;
             tap = kd / cin_p;
             ch = kd - tap * cin_p;
         } else {
-            const int64_t e = i % 4;
-            row = (i / 4) % n_pad;
-            const int64_t slot = i / (4 * n_pad);
+            const int e = i & 3;
+            const int q = i >> 2;
+            row = q % n_pad;
+            const int slot = q / n_pad;
             tap = slot / chunks;
-            ch = (slot % chunks) * 4 + e;
+            ch = (slot - tap * chunks) * 4 + e;
         }
         float v = 0.f;
         if (row < n_real && ch < cin_real && tap < taps) {
-            const int64_t r = tap / kW, s = tap % kW;
+            const int r = tap / kW, s = tap - r * kW;
             if (mode == kPackFprop) {
                 v = __ldg(w + ((row * C + ch) * kH + r) * kW + s);
             } else if (mode == kPackDgradFlip) {  // B[c][(r',s')][k] = W[k][c][kH-1-r'][kW-1-s']
@@ -194,6 +201,38 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restri
             }
         }
         dst[i] = round_tf32 ? to_tf32(v) : v;
+    }
+}
+
+// Layout-32 fprop / dgrad-flip packing, one block per packed row: the row's source
+// weights are staged in smem with coalesced reads (fprop: W[row][c][r][s] is contiguous;
+// dgrad: W[k][row][r][s] is one contiguous run of taps per k), then the packed row
+// dst[row][tap*cin_p + ch] (zero past the real taps / channels) is written coalesced.
+__global__ void pack_rows_kernel(const float* __restrict__ w, float* __restrict__ dst, int K, int C, int kH,
+                                 int kW, int dgrad, int n_real, int cin_p, int kdim_p) {
+    extern __shared__ float sw[];  // [cin_real][taps]
+    const int row = blockIdx.x;
+    const int taps = kH * kW;
+    const int cin_real = dgrad ? K : C;
+    float* out = dst + (int64_t)row * kdim_p;
+    if (row < n_real) {
+        if (!dgrad) {
+            const float* src = w + (int64_t)row * C * taps;
+            for (int e = threadIdx.x; e < C * taps; e += blockDim.x) sw[e] = __ldg(src + e);
+        } else {
+            for (int e = threadIdx.x; e < K * taps; e += blockDim.x) {
+                const int k = e / taps, t = e - k * taps;
+                sw[e] = __ldg(w + ((int64_t)k * C + row) * taps + t);
+            }
+        }
+    }
+    __syncthreads();
+    for (int kd = threadIdx.x; kd < kdim_p; kd += blockDim.x) {
+        const int tap = kd / cin_p, ch = kd - tap * cin_p;
+        float v = 0.f;
+        if (row < n_real && tap < taps && ch < cin_real)
+            v = sw[ch * taps + (dgrad ? taps - 1 - tap : tap)];  // flip = (kH-1-r, kW-1-s)
+        out[kd] = to_tf32(v);
     }
 }
 
@@ -291,7 +330,7 @@ void nchw_to_nhwc_padded(const float* src, const NhwcDst& d0, const NhwcDst& d1,
     }
     after_launch("nchw_to_nhwc_padded");
     if (gb) {
-        bias_from_partials_kernel<<<(unsigned)C, 256, 0, st>>>(part, N * strips, C, gb, scale,
+        bias_from_partials_kernel<<<(unsigned)C, 1024, 0, st>>>(part, N * strips, C, gb, scale,
                                                                accumulate);
         after_launch("bias_from_partials");
     }
@@ -310,7 +349,7 @@ void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64
                                                                      C, HW, Cp, 1, gb ? part : nullptr);
     after_launch("nchw_to_nhwc_bias");
     if (gb) {
-        bias_from_partials_kernel<<<(unsigned)C, 256, 0, st>>>(part, N * strips, C, gb, scale,
+        bias_from_partials_kernel<<<(unsigned)C, 1024, 0, st>>>(part, N * strips, C, gb, scale,
                                                                accumulate);
         after_launch("bias_from_partials");
     }
@@ -319,9 +358,28 @@ void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64
 void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW,
                   int mode, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
                   int64_t total, bool round_tf32, cudaStream_t st) {
-    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * (int64_t)sm_count());
-    pack_weights_kernel<<<blocks, 256, 0, st>>>(w, dst, K, C, kH, kW, mode, layout, n_pad, cin_p,
-                                                slots_p, total, round_tf32);
+    PTB_REQUIRE(total < (1ll << 31) && K * C * kH * kW < (1ll << 31), "pack_weights: weights too large");
+    const size_t row_smem = sizeof(float) * (size_t)(mode == kPackDgradFlip ? K : C) * kH * kW;
+    // one block per packed row measured slower than the flat kernel (too few blocks:
+    // convnet L3 fwd pack 11 -> 26 us); kept for reference behind PT_B200_PACK_ROWS=1
+    static const bool rows_on = std::getenv("PT_B200_PACK_ROWS") != nullptr;
+    if (rows_on && layout == 32 && round_tf32 && (mode == kPackFprop || mode == kPackDgradFlip) &&
+        row_smem <= 96 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            PTB_CUDA(cudaFuncSetAttribute(pack_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            attr = true;
+        }
+        const int n_real = (int)(mode == kPackFprop ? K : C);
+        pack_rows_kernel<<<(unsigned)n_pad, 256, row_smem, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW,
+                                                                 mode == kPackDgradFlip ? 1 : 0, n_real,
+                                                                 (int)cin_p, (int)(total / n_pad));
+        after_launch("pack_rows");
+        return;
+    }
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 32 * (int64_t)sm_count());
+    pack_weights_kernel<<<blocks, 256, 0, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW, mode, layout,
+                                                (int)n_pad, (int)cin_p, (int)slots_p, (int)total, round_tf32);
     after_launch("pack_weights");
 }
 
@@ -330,23 +388,22 @@ void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, 
 // dst[((r*ng + sg)*G + delta)*bn + n][ch], zero for taps past kW / rows past n_real.
 __global__ void pack_grouped_kernel(const float* __restrict__ w, float* __restrict__ dst, int K, int C,
                                     int kH, int kW, int dgrad, int G, int ng, int bn, int cin_p,
-                                    int64_t total) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int ch = (int)(i % cin_p);
-        const int64_t rowi = i / cin_p;
-        const int n = (int)(rowi % bn);
-        const int64_t gd = rowi / bn;  // ((r*ng + sg)*G + delta)
-        const int delta = (int)(gd % G);
-        const int64_t rs = gd / G;
-        const int sg = (int)(rs % ng), r = (int)(rs / ng);
+                                    int total) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int rowi = i / cin_p;
+        const int ch = i - rowi * cin_p;
+        const int gd = rowi / bn;  // ((r*ng + sg)*G + delta)
+        const int n = rowi - gd * bn;
+        const int rs = gd / G;
+        const int delta = gd - rs * G;
+        const int r = rs / ng, sg = rs - r * ng;
         const int s = sg * G + delta;
         float v = 0.f;
         if (s < kW) {
             if (!dgrad) {  // row n = k, channel ch = c
-                if (n < K && ch < C) v = __ldg(w + (((int64_t)n * C + ch) * kH + r) * kW + s);
+                if (n < K && ch < C) v = __ldg(w + ((n * C + ch) * kH + r) * kW + s);
             } else {  // row n = c, channel ch = k, flipped tap
-                if (n < C && ch < K) v = __ldg(w + (((int64_t)ch * C + n) * kH + (kH - 1 - r)) * kW + (kW - 1 - s));
+                if (n < C && ch < K) v = __ldg(w + ((ch * C + n) * kH + (kH - 1 - r)) * kW + (kW - 1 - s));
             }
         }
         dst[i] = to_tf32(v);
@@ -357,9 +414,10 @@ void pack_grouped(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, 
                   int G, int bn, int64_t cin_p, cudaStream_t st) {
     const int ng = (int)ceil_div(kW, G);
     const int64_t total = kH * ng * G * (int64_t)bn * cin_p;
-    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * (int64_t)sm_count());
+    PTB_REQUIRE(total < (1ll << 31) && K * C * kH * kW < (1ll << 31), "pack_grouped: weights too large");
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 32 * (int64_t)sm_count());
     pack_grouped_kernel<<<blocks, 256, 0, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW, dgrad ? 1 : 0, G,
-                                                ng, bn, (int)cin_p, total);
+                                                ng, bn, (int)cin_p, (int)total);
     after_launch("pack_grouped");
 }
 

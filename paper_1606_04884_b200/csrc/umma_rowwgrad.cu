@@ -115,17 +115,31 @@ __global__ void fold_cols_kernel(const float* __restrict__ gxe, float* __restric
     const float* src = gxe + ((int64_t)n * kH * C + c) * plane + pW;
     float* dst = gx + (int64_t)row * W;
     const int r0 = max(0, h + pH - oH + 1), r1 = min(kH, h + pH + 1);  // taps with a valid row
+    // aligned rows (pW % 4 == 0, Wp % 4 == 0): one float4 load per tap
+    const bool vec_load = vec_store && ((pW | Wp) & 3) == 0;
     for (int w0 = threadIdx.x * 4; w0 < W; w0 += blockDim.x * 4) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         const bool full = w0 + 4 <= W;
+        if (full && vec_load) {
 #pragma unroll 4
-        for (int r = r0; r < r1; ++r) {
-            const float* p = src + (int64_t)r * C * plane + (int64_t)(h + pH - r) * Wp + w0;
-            if (full) {
+            for (int r = r0; r < r1; ++r) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(
+                    src + (int64_t)r * C * plane + (int64_t)(h + pH - r) * Wp + w0));
+                acc[0] += t.x;
+                acc[1] += t.y;
+                acc[2] += t.z;
+                acc[3] += t.w;
+            }
+        } else {
+#pragma unroll 4
+            for (int r = r0; r < r1; ++r) {
+                const float* p = src + (int64_t)r * C * plane + (int64_t)(h + pH - r) * Wp + w0;
+                if (full) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) acc[u] += __ldg(p + u);
-            } else {
-                for (int u = 0; u < W - w0; ++u) acc[u] += __ldg(p + u);
+                    for (int u = 0; u < 4; ++u) acc[u] += __ldg(p + u);
+                } else {
+                    for (int u = 0; u < W - w0; ++u) acc[u] += __ldg(p + u);
+                }
             }
         }
         if (full && vec_store) {

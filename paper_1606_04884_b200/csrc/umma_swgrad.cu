@@ -189,7 +189,7 @@ __global__ void expand_planes_kernel(const float* __restrict__ x, float4* __rest
         const int h = (int)(row - n * H);
         const float* xr = x + (n * C * H + h) * (int64_t)W;
         __syncthreads();
-        for (int t = threadIdx.x; t < C * W; t += blockDim.x) {
+        for (int t = threadIdx.y * blockDim.x + threadIdx.x; t < C * W; t += blockDim.x * blockDim.y) {
             const int c = t / W, w = t - c * W;
             uint32_t r;
             asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(__ldg(xr + (int64_t)c * H * W + w)));
@@ -197,35 +197,42 @@ __global__ void expand_planes_kernel(const float* __restrict__ x, float4* __rest
         }
         __syncthreads();
         float4* dst = xe + row * (int64_t)P * q4;
-        for (int e = threadIdx.x; e < P * q4; e += blockDim.x) {
-            const int pl = e / q4, j0 = (e - pl * q4) * 4;
+        // thread -> (plane, float4 column) with the plane decoded once per plane sweep
+        for (int pl = threadIdx.y; pl < P; pl += blockDim.y) {
             const int s = pl / C, c = pl - s * C;
-            float v[4];
+            const float* sr = srow + c * W + s - pW;
+            for (int j4 = threadIdx.x; j4 < q4; j4 += blockDim.x) {
+                const int j0 = j4 * 4;
+                float v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = j0 + u, w = j + s - pW;
-                v[u] = (j < oW && w >= 0 && w < W) ? srow[c * W + w] : 0.f;
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + u, w = j + s - pW;
+                    v[u] = (j < oW && w >= 0 && w < W) ? sr[j] : 0.f;
+                }
+                dst[pl * q4 + j4] = make_float4(v[0], v[1], v[2], v[3]);
             }
-            dst[e] = make_float4(v[0], v[1], v[2], v[3]);
         }
     }
 }
 
-// gw[k][c][r][s] = (acc ? gw : 0) + scale * sum_cta part[cta][k][r*P + s*C + c]  (cta order)
+// gw[k][c][r][s] = (acc ? gw : 0) + scale * sum_cta part[cta][k][r*P + s*C + c]  (cta order).
+// One thread per partial column (k, col): consecutive threads read consecutive columns.
 __global__ void swgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ gw, int K, int C,
                                      int kH, int kW, int npad, int ctas, float scale, int accumulate) {
-    const int64_t total = (int64_t)K * C * kH * kW;
     const int P = kW * C;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int s = (int)(i % kW), r = (int)((i / kW) % kH), c = (int)((i / ((int64_t)kW * kH)) % C);
-        const int k = (int)(i / ((int64_t)kW * kH * C));
-        const float* src = part + (int64_t)k * npad + r * P + s * C + c;
-        const int64_t slab = (int64_t)K * npad;
+    const int total = K * npad;
+    const int64_t slab = (int64_t)K * npad;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int k = i / npad, col = i - k * npad;
+        const int r = col / P, pl = col - r * P;
+        if (r >= kH) continue;
+        const int s = pl / C, c = pl - s * C;
+        const float* src = part + i;
         float acc = 0.f;
 #pragma unroll 8
         for (int b = 0; b < ctas; ++b) acc += __ldg(src + b * slab);
-        gw[i] = (accumulate ? gw[i] : 0.f) + scale * acc;
+        const int64_t o = (((int64_t)k * C + c) * kH + r) * kW + s;
+        gw[o] = (accumulate ? gw[o] : 0.f) + scale * acc;
     }
 }
 
@@ -302,7 +309,9 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
         const int64_t rows = g.N * g.H;
         const size_t smem = sizeof(float) * (size_t)(g.C * g.W);
         PTB_REQUIRE(smem <= 48 * 1024, "expand_planes: input row too wide");
-        expand_planes_kernel<<<(unsigned)std::min<int64_t>(rows, 64 * (int64_t)sm_count()), 256, smem, st>>>(
+        const int tx = w.Wx / 4 >= 32 ? 32 : 16;
+        expand_planes_kernel<<<(unsigned)std::min<int64_t>(rows, 64 * (int64_t)sm_count()), dim3(tx, 256 / tx), smem,
+                               st>>>(
             x, reinterpret_cast<float4*>(xe), rows, (int)g.C, (int)g.H, (int)g.W, (int)g.oW, (int)g.kW,
             (int)g.pW, w.Wx);
         after_launch("expand_planes");
@@ -355,7 +364,7 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
         umma_swgrad_kernel<<<(unsigned)w.ctas, kThreadsS, smem, st>>>(p);
         after_launch("umma_swgrad");
     }
-    const int64_t n = g.K * g.CRS;
+    const int64_t n = g.K * w.npad;
     swgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256, 0, st>>>(
         part, gw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, w.npad, w.ctas, scale, accumulate);
     after_launch("swgrad_reduce");

@@ -237,22 +237,52 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
 }
 
 // gw[k][c][r][s] = (acc ? gw : 0) + scale * sum_sp part[sp][(r*kW+s)*Cp + c][k]
+// (32-bit index math: the caller checks K*CRS < 2^31). Each thread owns four consecutive
+// k of one (c, r, s): float4 partial loads, 8 splits' loads in flight (fixed split order).
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ gw,
-                                    int64_t K, int64_t C, int64_t kH, int64_t kW, int64_t Cp,
+                                    int K, int C, int kH, int kW, int Cp,
                                     int splits, int64_t ld, int64_t split_stride, float scale,
                                     int accumulate) {
-    // thread index: k fastest, so each split's partial row is read coalesced
-    const int64_t total = K * C * kH * kW;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = i % K, crs = i / K;
-        const int64_t s = crs % kW, r = (crs / kW) % kH, c = crs / (kW * kH);
-        const float* src = part + ((r * kW + s) * Cp + c) * ld + k;
+    const int K4 = K / 4;
+    const int taps = kH * kW;
+    const int total = K4 * C * taps;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int crs = i / K4, k = (i - crs * K4) * 4;
+        const int c = crs / taps, rs = crs - c * taps;  // rs = r*kW + s
+        const float* src = part + ((int64_t)rs * Cp + c) * ld + k;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+        for (int sp = 0; sp < splits; ++sp) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (int64_t)sp * split_stride));
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t o = (int64_t)(k + u) * C * taps + crs;
+            gw[o] = (accumulate ? gw[o] : 0.f) + scale * a[u];
+        }
+    }
+}
+
+// the same for K % 4 != 0 (one k per thread)
+__global__ void wgrad_reduce1_kernel(const float* __restrict__ part, float* __restrict__ gw,
+                                     int K, int C, int kH, int kW, int Cp,
+                                     int splits, int64_t ld, int64_t split_stride, float scale,
+                                     int accumulate) {
+    const int total = K * C * kH * kW;
+    const int taps = kH * kW;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int crs = i / K, k = i - crs * K;
+        const int c = crs / taps, rs = crs - c * taps;
+        const float* src = part + ((int64_t)rs * Cp + c) * ld + k;
         float acc = 0.f;
-        // fixed split order; unrolled so the independent loads are in flight together
 #pragma unroll 8
         for (int sp = 0; sp < splits; ++sp) acc += __ldg(src + (int64_t)sp * split_stride);
-        const int64_t o = k * C * kH * kW + crs;
+        const int64_t o = (int64_t)k * C * taps + crs;
         gw[o] = (accumulate ? gw[o] : 0.f) + scale * acc;
     }
 }
@@ -262,8 +292,15 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
 void wgrad_reduce_launch(const float* part, float* gw, const Geo& g, int64_t Cp, int splits, int64_t ld,
                          int64_t split_stride, float scale, int accumulate, cudaStream_t st) {
     const int64_t n = g.K * g.CRS;
-    wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256, 0, st>>>(
-        part, gw, g.K, g.C, g.kH, g.kW, Cp, splits, ld, split_stride, scale, accumulate);
+    PTB_REQUIRE(n < (1ll << 31), "wgrad_reduce: weights too large");
+    if (g.K % 4 == 0 && ld % 4 == 0 && split_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(part) & 15) == 0) {
+        wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n / 4, 256), 8 * (int64_t)sm_count()), 256, 0,
+                              st>>>(part, gw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, (int)Cp, splits, ld,
+                                    split_stride, scale, accumulate);
+    } else {
+        wgrad_reduce1_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256, 0, st>>>(
+            part, gw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, (int)Cp, splits, ld, split_stride, scale, accumulate);
+    }
     after_launch("wgrad_reduce");
 }
 
@@ -443,11 +480,7 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
         else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1, 64>, p));
         after_launch("umma_wgrad");
     }
-    const int64_t n = g.K * g.CRS;
-    wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256,
-                          0, st>>>(part, gw, g.K, g.C, g.kH, g.kW, w.Cp, w.splits, p.part_ld,
-                                   p.part_split, scale, accumulate);
-    after_launch("wgrad_reduce");
+    wgrad_reduce_launch(part, gw, g, w.Cp, w.splits, p.part_ld, p.part_split, scale, accumulate, st);
 }
 
 }  // namespace ptb
