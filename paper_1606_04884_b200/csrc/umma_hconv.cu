@@ -72,6 +72,7 @@ struct HConvParams {
     int exp;                    // timing experiments (PT_B200_HCONV_EXP; wrong results if != 0)
     uint32_t tmem_cols;
     int nacc;            // TMEM accumulator buffers (2 or 4)
+    int mc;              // 1: clusters of two CTA pairs sharing each weight stage by TMA multicast
     float* out;
     const float* bias;
 };
@@ -102,8 +103,12 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // G > 1: [8 chunks][3 warps][G-1][G-1][16]
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
-    const uint32_t rank = cluster_rank();
+    const uint32_t crank = cluster_rank();
+    const uint32_t rank = crank & 1;          // rank in the CTA pair
+    const uint32_t pr = crank >> 1;           // pair in the cluster (mc)
     const bool leader = rank == 0;
+    const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
+    const uint16_t bmask = p.mc ? (uint16_t)0xF : pair_mask;  // who consumes a weight stage
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.tmap_a);
         tma_prefetch(&p.tmap_a2);
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         }
         for (int i = 0; i < p.sb; ++i) {
             mbar_init(&bfull[i], 1);
-            mbar_init(&bempty[i], 1);
+            mbar_init(&bempty[i], p.mc ? 2 : 1);  // mc: both pairs release a shared weight stage
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
@@ -130,7 +135,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const int num_units = p.tiles * p.n_tiles;
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    // pairs per cluster PPC; the pairs of a cluster walk their tiles in lockstep (same count:
+    // a pair past the end runs a dummy tile) because they consume the same weight stages
+    const int PPC = p.mc ? 2 : 1;
+    const int cid = blockIdx.x / (2 * PPC), ncl = gridDim.x / (2 * PPC);
     constexpr int kCtaSpan = 129 - G;  // positions a CTA advances per tile
 
     if (warp == 0) {
@@ -139,7 +147,9 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
             const uint32_t atx = 2 * p.stage_a, btx = 2 * p.stage_b;
-            for (int u = cid; u < num_units; u += ncl) {
+            for (int uu = cid; uu * PPC < num_units; uu += ncl) {
+                const int u0 = uu * PPC + (int)pr;
+                const int u = u0 < num_units ? u0 : num_units - 1;  // dummy tile: any valid coordinates
                 const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
                 // image half `rank`, offset qh inside it; both CTAs share the column w0
                 const int n = t / p.tpi, qh = (t - n * p.tpi) * kCtaSpan;
@@ -169,7 +179,20 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             mbar_wait(&bempty[bs], bph ^ 1);
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
                             uint8_t* bdst = sB + (size_t)bs * p.stage_b;
-                            if constexpr (G == 1) {
+                            if (p.mc) {
+                                // pair 0 loads each CTA-rank half once, multicast to that rank
+                                // in both pairs
+                                if (pr == 0) {
+                                    const uint16_t m = (uint16_t)(rank ? 0xA : 0x5);
+                                    if constexpr (G == 1)
+                                        tma_load_3d_cg2_mc(bdst, &p.tmap_b, &bfull[bs], 0, brow,
+                                                           (r * p.kW + s) * (p.cin_p / 32) + cc, m);
+                                    else
+                                        tma_load_3d_cg2_mc(bdst, &p.tmap_b, &bfull[bs], 0,
+                                                           ((r * p.ngroups + s / G) * G) * p.bn + (int)rank * (G * p.bn / 2),
+                                                           cc, m);
+                                }
+                            } else if constexpr (G == 1) {
                                 tma_load_3d_cg2(bdst, &p.tmap_b, &bfull[bs], 0, brow,
                                                 (r * p.kW + s) * (p.cin_p / 32) + cc);
                             } else {
@@ -195,7 +218,9 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
             int it = 0;
-            for (int u = cid; u < num_units; u += ncl, ++it) {
+            for (int uu = cid; uu * PPC < num_units; uu += ncl, ++it) {
+                const int u0 = uu * PPC + (int)pr;
+                const int u = u0 < num_units ? u0 : num_units - 1;
                 // nacc (2 or 4) TMEM accumulators: the MMA may run nacc-1 tiles ahead of the
                 // epilogue (tiles with little K per tile are otherwise epilogue-paced)
                 const uint32_t acc = (uint32_t)(it % p.nacc);
@@ -224,20 +249,20 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                                              accum);
                                 accum = 1;
                             }
-                            mma_commit_cg2_warp(&bempty[bs]);
+                            mma_commit_cg2_warp_mask(&bempty[bs], bmask);
                             if (++bs == p.sb) {
                                 bs = 0;
                                 bph ^= 1;
                             }
                         }
-                        mma_commit_cg2_warp(&aempty[as]);
+                        mma_commit_cg2_warp_mask(&aempty[as], pair_mask);
                         if (++as == p.sa) {
                             as = 0;
                             aph ^= 1;
                         }
                     }
                 }
-                mma_commit_cg2_warp(&tfull[acc]);
+                mma_commit_cg2_warp_mask(&tfull[acc], pair_mask);
             }
         }
     } else {
@@ -246,7 +271,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         const int half = (int)(warp - 2) >> 2;  // column chunks half, 2*k + half
         const int64_t ohw = (int64_t)p.oH * p.oW;
         int it = 0;
-        for (int u = cid; u < num_units; u += ncl, ++it) {
+        for (int uu = cid; uu * PPC < num_units; uu += ncl, ++it) {
+            const int u0 = uu * PPC + (int)pr;
+            const bool real = u0 < num_units;  // a dummy tile's accumulator is drained, not stored
+            const int u = real ? u0 : num_units - 1;
             const uint32_t acc = (uint32_t)(it % p.nacc);
             mbar_wait(&tfull[acc], (it / p.nacc) & 1);
             tc_fence_after();
@@ -254,7 +282,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             const int n = t / p.tpi;
             const int qq = (t - n * p.tpi) * kCtaSpan + (int)(q * 32 + lane);  // position in the half
             const int i = (int)rank * p.R + qq / p.Wp, j = qq % p.Wp;
-            const bool valid = qq < p.m && i < p.oH && j < p.oW && (int)(q * 32 + lane) < kCtaSpan;
+            const bool valid = real && qq < p.m && i < p.oH && j < p.oW && (int)(q * 32 + lane) < kCtaSpan;
             const int ch0 = nt * p.bn;
             const int64_t base = ((int64_t)n * p.n_rows + ch0) * ohw + (int64_t)i * p.oW + j;
             const uint32_t lane_base = tmem_base + ((q * 32u) << 16);
@@ -328,7 +356,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             __syncwarp();
             if (lane == 0) {
                 if (leader) mbar_arrive(&tempty[acc]);
-                else mbar_arrive_cluster(&tempty[acc], 0);
+                else mbar_arrive_cluster(&tempty[acc], crank & ~1u);
             }
         }
     }
@@ -451,7 +479,15 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
                         (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn);
     const int units = p.tiles * p.n_tiles;
-    const int ncl = std::min(units, sm_count() / 2);
+    {
+        // two pairs per cluster sharing each weight stage by multicast: correct, but measured
+        // 1.8x slower (convnet L2 dgrad 0.85 -> 1.51 ms; the pairs' lockstep couples their
+        // stalls), so opt-in only
+        const char* e = std::getenv("PT_B200_HCONV_MC");
+        p.mc = (e && std::atoi(e) == 1 && units >= 2) ? 1 : 0;
+    }
+    const int cl_ctas = p.mc ? 4 : 2;
+    const int ncl = std::min(p.mc ? (units + 1) / 2 : units, sm_count() / cl_ctas);
     static bool attr = false;
     if (!attr) {
         for (auto fn : {umma_hconv_kernel<1, 1>, umma_hconv_kernel<1, 2>, umma_hconv_kernel<1, 3>,
@@ -461,13 +497,13 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * ncl);
+    cfg.gridDim = dim3(cl_ctas * ncl);
     cfg.blockDim = dim3(kThreadsH);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.x = cl_ctas;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
