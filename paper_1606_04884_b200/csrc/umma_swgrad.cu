@@ -40,7 +40,6 @@ using namespace umma;
 
 constexpr int kThreadsS = 192;
 constexpr int kSmemLimitS = 232448;
-constexpr int kRowsS = 2;  // output rows per pipeline stage
 
 struct SWParams {
     CUtensorMap tmap_gy;  // gy NHWC, 5-D {32, oW, oH, N, Kp/32}, box {32, 32, R, 1, Kp/32}, SW128_32B
@@ -58,6 +57,7 @@ struct SWParams {
     float* part;      // [gridDim.x][K][npad]
 };
 
+template <int kRowsS>  // output rows per pipeline stage (2, 4 or 8: more rows amortise the per-stage cost)
 __global__ void __launch_bounds__(kThreadsS, 1) umma_swgrad_kernel(const __grid_constant__ SWParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ uint8_t smem_raw[];
@@ -237,7 +237,7 @@ __global__ void swgrad_reduce_kernel(const float* __restrict__ part, float* __re
 }
 
 struct SWPlan {
-    int P, Ntot, nh, nhalf, npad, Kp, Wx, jbs, rgs, items, ctas, stages;
+    int P, Ntot, nh, nhalf, npad, Kp, Wx, jbs, rgs, items, ctas, stages, R;
     uint32_t stage_a, stage_b, tmem_cols, pad;
     int64_t xe_elems, part_elems;
 };
@@ -252,19 +252,25 @@ SWPlan swplan(const Geo& g) {
     w.Kp = (int)((g.K + 31) / 32 * 32);
     w.Wx = (int)((g.oW + 3) / 4 * 4);
     w.jbs = (int)ceil_div(g.oW, 32);
-    w.rgs = (int)ceil_div(g.oH, kRowsS);
-    const int64_t items = g.N * w.rgs * w.jbs;
-    w.items = items < (1ll << 31) ? (int)items : -1;
-    w.ctas = (int)std::min<int64_t>(items, sm_count());
-    w.stage_a = (uint32_t)align_up((size_t)(w.Kp / 32) * kRowsS * 32 * 128, 1024);
-    w.stage_b = (uint32_t)align_up((size_t)(kRowsS + g.kH - 1) * w.P * 128, 1024);
-    // overrun past the last stage: B rows up to npad from output row kRowsS-1's start, A
-    // lanes past Kp (4 x 32-channel atoms of M = 128) beyond the stage's own B region
-    const int64_t b_over = ((int64_t)(kRowsS - 1) * w.P + w.npad - (kRowsS + g.kH - 1) * w.P) * 128;
-    const int64_t a_over = (int64_t)(4 - w.Kp / 32) * kRowsS * 32 * 128 - w.stage_b;
-    w.pad = (uint32_t)align_up((size_t)std::max<int64_t>(1024, std::max(b_over, a_over)), 1024);
-    const int budget = kSmemLimitS - 1024 - (int)w.pad - 256;
-    w.stages = std::min(8, budget / (int)(w.stage_a + w.stage_b));
+    // rows per stage: the most (2, 4, 8) that still leave a 3-deep ring (VGG conv1: 8 MMAs
+    // per 2-row stage left the tensor pipe waiting on the per-stage round trip)
+    for (int R : {8, 4, 2}) {
+        w.R = R;
+        w.rgs = (int)ceil_div(g.oH, R);
+        const int64_t items = g.N * w.rgs * w.jbs;
+        w.items = items < (1ll << 31) ? (int)items : -1;
+        w.ctas = (int)std::min<int64_t>(items, sm_count());
+        w.stage_a = (uint32_t)align_up((size_t)(w.Kp / 32) * R * 32 * 128, 1024);
+        w.stage_b = (uint32_t)align_up((size_t)(R + g.kH - 1) * w.P * 128, 1024);
+        // overrun past the last stage: B rows up to npad from output row R-1's start, A lanes
+        // past Kp (4 x 32-channel atoms of M = 128) beyond the stage's own B region
+        const int64_t b_over = ((int64_t)(R - 1) * w.P + w.npad - (R + g.kH - 1) * w.P) * 128;
+        const int64_t a_over = (int64_t)(4 - w.Kp / 32) * R * 32 * 128 - w.stage_b;
+        w.pad = (uint32_t)align_up((size_t)std::max<int64_t>(1024, std::max(b_over, a_over)), 1024);
+        const int budget = kSmemLimitS - 1024 - (int)w.pad - 256;
+        w.stages = std::min(8, budget / (int)(w.stage_a + w.stage_b));
+        if (R == 2 || (w.stages >= 3 && R <= g.oH && R + g.kH - 1 <= 256)) break;
+    }
     uint32_t cols = 32;
     while ((int)cols < w.npad) cols <<= 1;
     w.tmem_cols = cols;
@@ -287,7 +293,7 @@ bool swgrad_ok(const Geo& g) {
     if (!swgrad_env()) return false;
     if (!(g.C <= 4 && g.sH == 1 && g.sW == 1 && g.K <= 128 && g.pH <= 64 && g.pW <= 64)) return false;
     const SWPlan w = swplan(g);
-    if (w.items < 1 || w.npad > 512 || w.P > 256 || kRowsS + g.kH - 1 > 256) return false;
+    if (w.items < 1 || w.npad > 512 || w.P > 256 || w.R + g.kH - 1 > 256) return false;
     if (w.pad > 65536) return false;
     if (g.N * g.H * w.P >= (1ll << 31) || g.M >= (1ll << 31)) return false;
     return w.stages >= 2 && sm_count() >= 1;
@@ -322,14 +328,14 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
         const uint64_t dims[5] = {32, (uint64_t)g.oW, (uint64_t)g.oH, (uint64_t)g.N, (uint64_t)(w.Kp / 32)};
         const uint64_t strides[4] = {(uint64_t)w.Kp * 4, (uint64_t)(g.oW * w.Kp * 4),
                                      (uint64_t)(g.oHW * w.Kp * 4), 128};
-        const uint32_t box[5] = {32, 32, (uint32_t)kRowsS, 1, (uint32_t)(w.Kp / 32)};
+        const uint32_t box[5] = {32, 32, (uint32_t)w.R, 1, (uint32_t)(w.Kp / 32)};
         tmap_tiled(&p.tmap_gy, gyh, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     }
     {
         const uint64_t dims[4] = {(uint64_t)w.Wx, (uint64_t)w.P, (uint64_t)g.H, (uint64_t)g.N};
         const uint64_t strides[3] = {(uint64_t)w.Wx * 4, (uint64_t)(w.P * w.Wx * 4),
                                      (uint64_t)(g.H * w.P * w.Wx * 4)};
-        const uint32_t box[4] = {32, (uint32_t)w.P, (uint32_t)(kRowsS + g.kH - 1), 1};
+        const uint32_t box[4] = {32, (uint32_t)w.P, (uint32_t)(w.R + g.kH - 1), 1};
         tmap_tiled(&p.tmap_xe, xe, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
     p.oH = (int)g.oH;
@@ -346,8 +352,8 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
     p.stages = w.stages;
     p.stage_a = w.stage_a;
     p.stage_b = w.stage_b;
-    p.tx = (uint32_t)((w.Kp / 32) * kRowsS * 32 * 128 + (kRowsS + g.kH - 1) * w.P * 128);
-    p.a_lbo = (uint32_t)(kRowsS * 32 * 128);
+    p.tx = (uint32_t)((w.Kp / 32) * w.R * 32 * 128 + (w.R + g.kH - 1) * w.P * 128);
+    p.a_lbo = (uint32_t)(w.R * 32 * 128);
     p.tmem_cols = w.tmem_cols;
     p.K = (int)g.K;
     p.npad = w.npad;
@@ -356,12 +362,15 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
     const size_t smem = 1024 + (size_t)w.stages * (w.stage_a + w.stage_b) + w.pad + (2 * w.stages + 2) * 8 + 16;
     static bool attr = false;
     if (!attr) {
-        PTB_CUDA(cudaFuncSetAttribute(umma_swgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitS));
+        for (auto fn : {umma_swgrad_kernel<2>, umma_swgrad_kernel<4>, umma_swgrad_kernel<8>})
+            PTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitS));
         attr = true;
     }
     {
         ProfScope prof("umma_wgrad", st, 2.0 * g.M * g.K * g.CRS, 0.0);
-        umma_swgrad_kernel<<<(unsigned)w.ctas, kThreadsS, smem, st>>>(p);
+        if (w.R == 8) umma_swgrad_kernel<8><<<(unsigned)w.ctas, kThreadsS, smem, st>>>(p);
+        else if (w.R == 4) umma_swgrad_kernel<4><<<(unsigned)w.ctas, kThreadsS, smem, st>>>(p);
+        else umma_swgrad_kernel<2><<<(unsigned)w.ctas, kThreadsS, smem, st>>>(p);
         after_launch("umma_swgrad");
     }
     const int64_t n = g.K * w.npad;
