@@ -85,7 +85,11 @@ struct HConvParams {
 // out[q] = sum_delta D_delta[q + delta]; each CTA's last G-1 lanes lack right neighbours
 // and are dropped (tiles advance 129 - G positions per CTA). An N <= 128 MMA costs the
 // same ~64 cycles whatever N is, so grouping cuts the MMA count up to G-fold.
-template <int CPS, int G>
+// RUNS = 2: each unit is two consecutive position tiles sharing every weight stage (their
+// A runs sit side by side in the A stage, two accumulators per unit): the weights —
+// re-read from L2 per tile, the larger share of the operand traffic for 64-128 channel
+// layers — are fetched half as often.
+template <int CPS, int G, int RUNS>
 __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_constant__ HConvParams p) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ uint8_t smem_raw[];
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    const int num_units = p.tiles * p.n_tiles;
+    const int num_units = (int)(((int64_t)p.tiles + RUNS - 1) / RUNS) * p.n_tiles;
     // pairs per cluster PPC; the pairs of a cluster walk their tiles in lockstep (same count:
     // a pair past the end runs a dummy tile) because they consume the same weight stages
     const int PPC = p.mc ? 2 : 1;
@@ -146,18 +150,27 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             // ===== TMA producer (both CTAs; bytes complete on the leader's barriers) =====
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
-            const uint32_t atx = 2 * p.stage_a, btx = 2 * p.stage_b;
+            const uint32_t btx = 2 * p.stage_b;
+            const uint32_t run_bytes = (uint32_t)CPS * p.box_a;  // one run's CPS boxes
             for (int uu = cid; uu * PPC < num_units; uu += ncl) {
                 const int u0 = uu * PPC + (int)pr;
                 const int u = u0 < num_units ? u0 : num_units - 1;  // dummy tile: any valid coordinates
-                const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
-                // image half `rank`, offset qh inside it; both CTAs share the column w0
-                const int n = t / p.tpi, qh = (t - n * p.tpi) * kCtaSpan;
-                const int row0 = (int)rank * p.R + qh / p.Wp;
-                // both CTAs share the start column, hence the row count and the byte count
-                const bool short_run = qh % p.Wp < p.nr_split;
-                const CUtensorMap* amap = short_run ? &p.tmap_a2 : &p.tmap_a;
-                const uint32_t atx_t = short_run ? atx - 2 * (uint32_t)CPS * (uint32_t)p.Wp * 128u : atx;
+                const int tg = u / p.n_tiles, nt = u - tg * p.n_tiles;
+                // per run: image half `rank`, offset qh inside it; both CTAs share the column
+                // w0, hence the row count and the byte count
+                int n_k[RUNS], row0_k[RUNS];
+                bool short_k[RUNS];
+                uint32_t atx_t = 0;
+#pragma unroll
+                for (int k = 0; k < RUNS; ++k) {
+                    int t = tg * RUNS + k;
+                    if (t >= p.tiles) t = p.tiles - 1;  // dummy second run past the end
+                    n_k[k] = t / p.tpi;
+                    const int qh = (t - n_k[k] * p.tpi) * kCtaSpan;
+                    row0_k[k] = (int)rank * p.R + qh / p.Wp;
+                    short_k[k] = qh % p.Wp < p.nr_split;
+                    atx_t += 2 * (short_k[k] ? run_bytes - (uint32_t)CPS * (uint32_t)p.Wp * 128u : run_bytes);
+                }
                 const int brow = G > 1 ? 0 : nt * p.bn + (int)rank * (p.bn / 2);
                 for (int r = 0; r < p.kH; ++r) {
                     for (int cc = 0; cc < p.chunks; cc += CPS) {
@@ -168,9 +181,13 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                         // (one request per chunk: the short map's smaller box would change the
                         // chunk stride inside a multi-chunk box)
 #pragma unroll
-                        for (int c = 0; c < CPS; ++c)
-                            tma_load_5d_cg2(sA + (size_t)as * p.stage_a + c * p.box_a, amap, &afull[as], 0,
-                                            -p.apw, row0 + r - p.aph, n, cc + c);
+                        for (int k = 0; k < RUNS; ++k) {
+                            const CUtensorMap* amap = short_k[k] ? &p.tmap_a2 : &p.tmap_a;
+#pragma unroll
+                            for (int c = 0; c < CPS; ++c)
+                                tma_load_5d_cg2(sA + (size_t)as * p.stage_a + k * run_bytes + c * p.box_a, amap,
+                                                &afull[as], 0, -p.apw, row0_k[k] + r - p.aph, n_k[k], cc + c);
+                        }
                         if (++as == p.sa) {
                             as = 0;
                             aph ^= 1;
@@ -226,9 +243,15 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 const uint32_t acc = (uint32_t)(it % p.nacc);
                 mbar_wait(&tempty[acc], ((it / p.nacc) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t d = tmem_base + acc * (G * p.bn);
-                const int t = u / p.n_tiles;
-                const uint32_t w0 = (uint32_t)(((t % p.tpi) * kCtaSpan) % p.Wp);  // run start column
+                const uint32_t d = tmem_base + acc * (RUNS * G * p.bn);
+                const int tg = u / p.n_tiles;
+                uint32_t w0_k[RUNS];  // run start columns
+#pragma unroll
+                for (int k = 0; k < RUNS; ++k) {
+                    int t = tg * RUNS + k;
+                    if (t >= p.tiles) t = p.tiles - 1;
+                    w0_k[k] = (uint32_t)(((t % p.tpi) * kCtaSpan) % p.Wp);
+                }
                 uint32_t accum = 0;
                 const uint32_t box_a16 = p.box_a >> 4, box_b16 = p.box_b >> 4;
                 for (int r = 0; r < p.kH; ++r) {
@@ -240,13 +263,17 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             mbar_wait(&bfull[bs], bph);
                             tc_fence_after();
                             // tap s: the same pixel run, s rows (s*128 B) further in
-                            const uint32_t a_s = alo + (w0 + (uint32_t)s) * 8u;
                             const uint32_t blo = desc_lo(smem_u32(sB + (size_t)bs * p.stage_b), 16);
 #pragma unroll
                             for (int k = 0; k < 4 * CPS; ++k) {
-                                mma_tf32_cg2_warp(d, desc_make(a_s + (k >> 2) * box_a16 + 2 * (k & 3), kHi),
-                                             desc_make(blo + (k >> 2) * box_b16 + 2 * (k & 3), kHi), idesc,
-                                             accum);
+                                const uint64_t bd = desc_make(blo + (k >> 2) * box_b16 + 2 * (k & 3), kHi);
+#pragma unroll
+                                for (int q = 0; q < RUNS; ++q) {
+                                    const uint32_t a_s = alo + (uint32_t)q * (CPS * box_a16) + (w0_k[q] + (uint32_t)s) * 8u;
+                                    mma_tf32_cg2_warp(d + (uint32_t)(q * G) * p.bn,
+                                                      desc_make(a_s + (k >> 2) * box_a16 + 2 * (k & 3), kHi), bd, idesc,
+                                                      accum);
+                                }
                                 accum = 1;
                             }
                             mma_commit_cg2_warp_mask(&bempty[bs], bmask);
@@ -273,12 +300,18 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         int it = 0;
         for (int uu = cid; uu * PPC < num_units; uu += ncl, ++it) {
             const int u0 = uu * PPC + (int)pr;
-            const bool real = u0 < num_units;  // a dummy tile's accumulator is drained, not stored
-            const int u = real ? u0 : num_units - 1;
+            const bool real_u = u0 < num_units;  // a dummy tile's accumulator is drained, not stored
+            const int u = real_u ? u0 : num_units - 1;
             const uint32_t acc = (uint32_t)(it % p.nacc);
             mbar_wait(&tfull[acc], (it / p.nacc) & 1);
             tc_fence_after();
-            const int t = u / p.n_tiles, nt = u - t * p.n_tiles;
+            const int tg = u / p.n_tiles, nt = u - tg * p.n_tiles;
+#pragma unroll 1
+            for (int run = 0; run < RUNS; ++run) {
+            const int t_raw = tg * RUNS + run;
+            const bool real = real_u && t_raw < p.tiles;
+            const int t = real ? t_raw : p.tiles - 1;
+            const int xpar = (it * RUNS + run) & 1;  // exchange-slot parity
             const int n = t / p.tpi;
             const int qq = (t - n * p.tpi) * kCtaSpan + (int)(q * 32 + lane);  // position in the half
             const int i = (int)rank * p.R + qq / p.Wp, j = qq % p.Wp;
@@ -288,11 +321,11 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
             const uint32_t lane_base = tmem_base + ((q * 32u) << 16);
             if constexpr (G == 1) {
                 for (int c0 = half * 16; c0 < p.bn; c0 += 32)
-                    store_tmem_columns_nchw(lane_base + acc * p.bn + c0, 16,
+                    store_tmem_columns_nchw(lane_base + (acc * RUNS + run) * p.bn + c0, 16,
                                             p.out + (valid ? base + (int64_t)c0 * ohw : 0), ohw, p.bias,
                                             ch0 + c0, p.n_rows, valid);
             } else {
-                const uint32_t taddr = lane_base + acc * G * p.bn;
+                const uint32_t taddr = lane_base + (acc * RUNS + run) * G * p.bn;
                 for (int c0 = half * 16; c0 < p.bn; c0 += 32) {
                     uint32_t vd[G][16];
                     float acc_v[16];
@@ -308,7 +341,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                     for (int e = 0; e < 16; ++e) acc_v[e] = __uint_as_float(vd[0][e]);
                     // column group delta: the right neighbour delta lanes over, or (past lane
                     // 31) the next warp's first lanes through shared memory
-                    float* slot = xch + ((it & 1) * ((p.bn + 15) >> 4) + (c0 >> 4)) * (3 * (G - 1) * (G - 1) * 16);
+                    float* slot = xch + (xpar * ((p.bn + 15) >> 4) + (c0 >> 4)) * (3 * (G - 1) * (G - 1) * 16);
 #pragma unroll
                     for (int dl = 1; dl < G; ++dl) {
                         float* sd = slot + (dl - 1) * (G - 1) * 16;
@@ -352,6 +385,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                     }
                 }
             }
+            }  // run
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -400,9 +434,20 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     // B per CTA: G*bn/2 rows of the (delta, c) stack (G > 1), else bn/2 rows of one tap
     const uint32_t box_b = (uint32_t)align_up((size_t)(pair ? G * pl.bn / 2 : pl.bn / 2), 8) * 128u;
     const int budget = kSmemLimitH - 1024 - 512 - xch_bytes(G, pl.bn);
+    // RUNS = 2 (two position tiles per weight stage) for tiles with a short reduction (their
+    // per-tile fixed costs dominate: VGG-A conv2 fwd, 72 MMAs per tile, 0.289 -> 0.200 ms;
+    // convnet L2 fwd, 648 per tile, unchanged), when both accumulators of a unit still leave
+    // TMEM for double buffering (G*bn <= 128). PT_B200_HCONV_RUNS=1|2 forces.
+    static const int runs_env = [] {
+        const char* e = std::getenv("PT_B200_HCONV_RUNS");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int64_t mmas_per_tile = (int64_t)kH * (pl.cin_p / 32) * ceil_div(kW, G) * 4;
+    int runs = (runs_env == 2 || (runs_env == 0 && mmas_per_tile <= 320)) && G <= 2 && G * pl.bn <= 128 ? 2 : 1;
+    if (runs == 2 && 2 * 2 * (int)box_a + 3 * (int)box_b > budget) runs = 1;  // two-run A stages must fit twice
     int cps = (pl.cin_p / 32) % 2 == 0 ? 2 : 1;
-    if (cps == 2 && 2 * 2 * (int)box_a + 4 * 2 * (int)box_b > budget) cps = 1;
-    PTB_REQUIRE(2 * (int)box_a + 3 * (int)box_b <= budget, "hconv: shared memory too small for the rings");
+    if (cps == 2 && 2 * 2 * runs * (int)box_a + 4 * 2 * (int)box_b > budget) cps = 1;
+    PTB_REQUIRE(2 * runs * (int)box_a + 3 * (int)box_b <= budget, "hconv: shared memory too small for the rings");
     {
         const uint64_t dims[5] = {32, (uint64_t)aW, (uint64_t)aH, (uint64_t)N, (uint64_t)(pl.cin_p / 32)};
         const uint64_t strides[4] = {(uint64_t)pl.cin_p * 4, (uint64_t)(aW * pl.cin_p * 4),
@@ -456,7 +501,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.n_tiles = pl.n_tiles;
     p.box_a = box_a;
     p.box_b = box_b;
-    p.stage_a = cps * p.box_a;
+    p.stage_a = runs * cps * p.box_a;
     p.stage_b = cps * p.box_b;
     // B ring: enough stages to cover two filter rows' worth of taps; A ring: the rest
     int sb = std::min(16, std::max(4, pair ? 2 * (int)ceil_div(kW, G) : 2 * kW));
@@ -466,9 +511,9 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     PTB_REQUIRE(sa >= 2, "hconv: shared memory too small for the rings");
     p.sa = sa;
     p.sb = sb;
-    p.nacc = 4 * G * pl.bn <= 512 ? 4 : 2;
+    p.nacc = 4 * runs * G * pl.bn <= 512 ? 4 : 2;
     p.tmem_cols = 32;
-    while ((int)p.tmem_cols < p.nacc * G * pl.bn) p.tmem_cols <<= 1;
+    while ((int)p.tmem_cols < p.nacc * runs * G * pl.bn) p.tmem_cols <<= 1;
     PTB_REQUIRE(p.tmem_cols <= 512, "hconv: accumulators exceed TMEM");
     p.out = out;
     p.bias = bias;
@@ -478,21 +523,22 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
                         (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn);
-    const int units = p.tiles * p.n_tiles;
+    const int units = (int)ceil_div(p.tiles, runs) * p.n_tiles;
     {
         // two pairs per cluster sharing each weight stage by multicast: correct, but measured
         // 1.8x slower (convnet L2 dgrad 0.85 -> 1.51 ms; the pairs' lockstep couples their
         // stalls), so opt-in only
         const char* e = std::getenv("PT_B200_HCONV_MC");
-        p.mc = (e && std::atoi(e) == 1 && units >= 2) ? 1 : 0;
+        p.mc = (e && std::atoi(e) == 1 && units >= 2 && runs == 1) ? 1 : 0;
     }
     const int cl_ctas = p.mc ? 4 : 2;
     const int ncl = std::min(p.mc ? (units + 1) / 2 : units, sm_count() / cl_ctas);
     static bool attr = false;
     if (!attr) {
-        for (auto fn : {umma_hconv_kernel<1, 1>, umma_hconv_kernel<1, 2>, umma_hconv_kernel<1, 3>,
-                        umma_hconv_kernel<1, 4>, umma_hconv_kernel<2, 1>, umma_hconv_kernel<2, 2>,
-                        umma_hconv_kernel<2, 3>, umma_hconv_kernel<2, 4>})
+        for (auto fn : {umma_hconv_kernel<1, 1, 1>, umma_hconv_kernel<1, 2, 1>, umma_hconv_kernel<1, 3, 1>,
+                        umma_hconv_kernel<1, 4, 1>, umma_hconv_kernel<2, 1, 1>, umma_hconv_kernel<2, 2, 1>,
+                        umma_hconv_kernel<2, 3, 1>, umma_hconv_kernel<2, 4, 1>, umma_hconv_kernel<1, 1, 2>,
+                        umma_hconv_kernel<1, 2, 2>, umma_hconv_kernel<2, 1, 2>, umma_hconv_kernel<2, 2, 2>})
             PTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
         attr = true;
     }
@@ -509,17 +555,25 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     ProfScope prof("umma_conv", st, alg_flops, 0.0);
-#define PTB_HCONV_LAUNCH(CPS_, G_) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<CPS_, G_>, p))
-    if (cps == 2) {
-        if (G == 1) PTB_HCONV_LAUNCH(2, 1);
-        else if (G == 2) PTB_HCONV_LAUNCH(2, 2);
-        else if (G == 3) PTB_HCONV_LAUNCH(2, 3);
-        else PTB_HCONV_LAUNCH(2, 4);
+#define PTB_HCONV_LAUNCH(CPS_, G_, R_) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hconv_kernel<CPS_, G_, R_>, p))
+    if (runs == 2) {
+        if (cps == 2) {
+            if (G == 1) PTB_HCONV_LAUNCH(2, 1, 2);
+            else PTB_HCONV_LAUNCH(2, 2, 2);
+        } else {
+            if (G == 1) PTB_HCONV_LAUNCH(1, 1, 2);
+            else PTB_HCONV_LAUNCH(1, 2, 2);
+        }
+    } else if (cps == 2) {
+        if (G == 1) PTB_HCONV_LAUNCH(2, 1, 1);
+        else if (G == 2) PTB_HCONV_LAUNCH(2, 2, 1);
+        else if (G == 3) PTB_HCONV_LAUNCH(2, 3, 1);
+        else PTB_HCONV_LAUNCH(2, 4, 1);
     } else {
-        if (G == 1) PTB_HCONV_LAUNCH(1, 1);
-        else if (G == 2) PTB_HCONV_LAUNCH(1, 2);
-        else if (G == 3) PTB_HCONV_LAUNCH(1, 3);
-        else PTB_HCONV_LAUNCH(1, 4);
+        if (G == 1) PTB_HCONV_LAUNCH(1, 1, 1);
+        else if (G == 2) PTB_HCONV_LAUNCH(1, 2, 1);
+        else if (G == 3) PTB_HCONV_LAUNCH(1, 3, 1);
+        else PTB_HCONV_LAUNCH(1, 4, 1);
     }
 #undef PTB_HCONV_LAUNCH
     after_launch("umma_hconv");
