@@ -73,6 +73,9 @@ struct HConvParams {
     uint32_t tmem_cols;
     int nacc;            // TMEM accumulator buffers (2 or 4)
     int mc;              // 1: clusters of two CTA pairs sharing each weight stage by TMA multicast
+    int a_run;           // 1: A = the exact pixel run by TMA im2col traversal (tmap_run), else NR full rows
+    int run_px;          // a_run: pixels per run (128 + kW - 1)
+    CUtensorMap tmap_run;  // im2col over the dense NHWC act: {32 ch, run_px positions}, virtual kW = 1
     float* out;
     const float* bias;
 };
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 int n_k[RUNS], row0_k[RUNS];
                 bool short_k[RUNS];
                 uint32_t atx_t = 0;
+                int w0_k[RUNS];
 #pragma unroll
                 for (int k = 0; k < RUNS; ++k) {
                     int t = tg * RUNS + k;
@@ -168,8 +172,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                     n_k[k] = t / p.tpi;
                     const int qh = (t - n_k[k] * p.tpi) * kCtaSpan;
                     row0_k[k] = (int)rank * p.R + qh / p.Wp;
+                    w0_k[k] = qh % p.Wp;
                     short_k[k] = qh % p.Wp < p.nr_split;
-                    atx_t += 2 * (short_k[k] ? run_bytes - (uint32_t)CPS * (uint32_t)p.Wp * 128u : run_bytes);
+                    if (p.a_run) atx_t += 2u * (uint32_t)CPS * (uint32_t)p.run_px * 128u;
+                    else atx_t += 2 * (short_k[k] ? run_bytes - (uint32_t)CPS * (uint32_t)p.Wp * 128u : run_bytes);
                 }
                 const int brow = G > 1 ? 0 : nt * p.bn + (int)rank * (p.bn / 2);
                 for (int r = 0; r < p.kH; ++r) {
@@ -182,11 +188,23 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                         // chunk stride inside a multi-chunk box)
 #pragma unroll
                         for (int k = 0; k < RUNS; ++k) {
-                            const CUtensorMap* amap = short_k[k] ? &p.tmap_a2 : &p.tmap_a;
+                            if (p.a_run) {
+                                // exactly the run: im2col traversal of the padded position space
+                                // (row width Wp) from the tile's first position, filter row r
 #pragma unroll
-                            for (int c = 0; c < CPS; ++c)
-                                tma_load_5d_cg2(sA + (size_t)as * p.stage_a + k * run_bytes + c * p.box_a, amap,
-                                                &afull[as], 0, -p.apw, row0_k[k] + r - p.aph, n_k[k], cc + c);
+                                for (int c = 0; c < CPS; ++c)
+                                    // a tile starting in the phantom row 2R-1 = oH (odd oH) has no valid
+                                    // position; the im2col start must stay inside the traversal range
+                                    tma_load_im2col_4d_cg2(sA + (size_t)as * p.stage_a + k * run_bytes + c * p.box_a,
+                                                           &p.tmap_run, &afull[as], (cc + c) * 32, w0_k[k] - p.apw,
+                                                           min(row0_k[k], p.oH - 1) - p.aph, n_k[k], 0, (uint16_t)r);
+                            } else {
+                                const CUtensorMap* amap = short_k[k] ? &p.tmap_a2 : &p.tmap_a;
+#pragma unroll
+                                for (int c = 0; c < CPS; ++c)
+                                    tma_load_5d_cg2(sA + (size_t)as * p.stage_a + k * run_bytes + c * p.box_a, amap,
+                                                    &afull[as], 0, -p.apw, row0_k[k] + r - p.aph, n_k[k], cc + c);
+                            }
                         }
                         if (++as == p.sa) {
                             as = 0;
@@ -250,7 +268,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 for (int k = 0; k < RUNS; ++k) {
                     int t = tg * RUNS + k;
                     if (t >= p.tiles) t = p.tiles - 1;
-                    w0_k[k] = (uint32_t)(((t % p.tpi) * kCtaSpan) % p.Wp);
+                    w0_k[k] = p.a_run ? 0u : (uint32_t)(((t % p.tpi) * kCtaSpan) % p.Wp);  // a_run: the run starts at the tile
                 }
                 uint32_t accum = 0;
                 const uint32_t box_a16 = p.box_a >> 4, box_b16 = p.box_b >> 4;
@@ -429,8 +447,18 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     PTB_REQUIRE(NR <= 256 && N * aH * aW * pl.cin_p < (1ll << 40), "hconv: geometry out of range");
     HConvParams p;
     memset(&p, 0, sizeof p);
+    // A: the exact pixel run of a tile (im2col traversal) unless PT_B200_HCONV_A=rows; the
+    // NR-full-rows box fetches up to ~2.6x the run for narrow rows (VGG conv2: 3 x 114 px
+    // for a 130-pixel run)
+    static const int a_env = [] {
+        const char* e = std::getenv("PT_B200_HCONV_A");
+        return e && std::string(e) == "rows" ? 0 : 1;
+    }();
+    p.a_run = a_env;
+    p.run_px = 128 + kW - 1;
+    PTB_REQUIRE(!p.a_run || p.run_px <= 256, "hconv: run too long for one im2col box");
     // CPS: two channel chunks per stage unless the A stage would not leave room for a ring
-    const uint32_t box_a = (uint32_t)(NR * Wp) * 128u;
+    const uint32_t box_a = p.a_run ? (uint32_t)align_up((size_t)p.run_px * 128, 1024) : (uint32_t)(NR * Wp) * 128u;
     // B per CTA: G*bn/2 rows of the (delta, c) stack (G > 1), else bn/2 rows of one tap
     const uint32_t box_b = (uint32_t)align_up((size_t)(pair ? G * pl.bn / 2 : pl.bn / 2), 8) * 128u;
     const int budget = kSmemLimitH - 1024 - 512 - xch_bytes(G, pl.bn);
@@ -456,6 +484,9 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         tmap_tiled(&p.tmap_a, act, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
         const uint32_t box2[5] = {32, (uint32_t)Wp, (uint32_t)std::max(1, NR - 1), 1, 1};
         tmap_tiled(&p.tmap_a2, act, 5, dims, strides, box2, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (p.a_run)  // positions (i, j < Wp) -> input (i + r - aph, j - apw): a kH x 1 "conv" with pad (aph, apw)
+            tmap_im2col(&p.tmap_run, act, N, aH, aW, pl.cin_p, kH, 1, (int)aph, (int)apw, 1, 1, 32, p.run_px,
+                        CU_TENSOR_MAP_SWIZZLE_128B);
     }
     if (!pair) {
         // {32, weight rows, 32-wide k blocks}: one box = the CPS chunks of one tap

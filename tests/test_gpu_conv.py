@@ -300,3 +300,23 @@ def test_hwgrad_forced_edge_geometries():
     errs = json.loads(r.stdout.strip().splitlines()[-1])
     for g, e in zip(HWGRAD_EDGE, errs):
         assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
+
+
+def test_hankel_two_runs_forced_edge_geometries():
+    """PT_B200_HCONV=1 + PT_B200_HCONV_RUNS=2: the Hankel engine with two position tiles
+    per weight stage (odd tile counts -> a dummy second run) on the edge geometries."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW]
+             for g in HANKEL_EDGE]
+    env = dict(os.environ, PT_B200_HCONV="1", PT_B200_HCONV_RUNS="2")
+    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
+                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    errs = json.loads(r.stdout.strip().splitlines()[-1])
+    for g, e in zip(HANKEL_EDGE, errs):
+        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
