@@ -471,7 +471,10 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         return e ? std::atoi(e) : 0;
     }();
     const int64_t mmas_per_tile = (int64_t)kH * (pl.cin_p / 32) * ceil_div(kW, G) * 4;
-    int runs = (runs_env == 2 || (runs_env == 0 && mmas_per_tile <= 320)) && G <= 2 && G * pl.bn <= 128 ? 2 : 1;
+    int runs = ((runs_env == 0 && mmas_per_tile <= 320 && G <= 2 && G * pl.bn <= 128) ||
+                (runs_env == 2 && G <= 3 && G * pl.bn <= 256))
+                   ? 2
+                   : 1;
     if (runs == 2 && 2 * 2 * (int)box_a + 3 * (int)box_b > budget) runs = 1;  // two-run A stages must fit twice
     int cps = (pl.cin_p / 32) % 2 == 0 ? 2 : 1;
     if (cps == 2 && 2 * 2 * runs * (int)box_a + 4 * 2 * (int)box_b > budget) cps = 1;
@@ -542,7 +545,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     PTB_REQUIRE(sa >= 2, "hconv: shared memory too small for the rings");
     p.sa = sa;
     p.sb = sb;
-    p.nacc = 4 * runs * G * pl.bn <= 512 ? 4 : 2;
+    p.nacc = 4 * runs * G * pl.bn <= 512 ? 4 : 2 * runs * G * pl.bn <= 512 ? 2 : 1;
     p.tmem_cols = 32;
     while ((int)p.tmem_cols < p.nacc * runs * G * pl.bn) p.tmem_cols <<= 1;
     PTB_REQUIRE(p.tmem_cols <= 512, "hconv: accumulators exceed TMEM");
@@ -569,7 +572,8 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         for (auto fn : {umma_hconv_kernel<1, 1, 1>, umma_hconv_kernel<1, 2, 1>, umma_hconv_kernel<1, 3, 1>,
                         umma_hconv_kernel<1, 4, 1>, umma_hconv_kernel<2, 1, 1>, umma_hconv_kernel<2, 2, 1>,
                         umma_hconv_kernel<2, 3, 1>, umma_hconv_kernel<2, 4, 1>, umma_hconv_kernel<1, 1, 2>,
-                        umma_hconv_kernel<1, 2, 2>, umma_hconv_kernel<2, 1, 2>, umma_hconv_kernel<2, 2, 2>})
+                        umma_hconv_kernel<1, 2, 2>, umma_hconv_kernel<2, 1, 2>, umma_hconv_kernel<2, 2, 2>,
+                        umma_hconv_kernel<1, 3, 2>, umma_hconv_kernel<2, 3, 2>})
             PTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
         attr = true;
     }
@@ -590,10 +594,12 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     if (runs == 2) {
         if (cps == 2) {
             if (G == 1) PTB_HCONV_LAUNCH(2, 1, 2);
-            else PTB_HCONV_LAUNCH(2, 2, 2);
+            else if (G == 2) PTB_HCONV_LAUNCH(2, 2, 2);
+            else PTB_HCONV_LAUNCH(2, 3, 2);
         } else {
             if (G == 1) PTB_HCONV_LAUNCH(1, 1, 2);
-            else PTB_HCONV_LAUNCH(1, 2, 2);
+            else if (G == 2) PTB_HCONV_LAUNCH(1, 2, 2);
+            else PTB_HCONV_LAUNCH(1, 3, 2);
         }
     } else if (cps == 2) {
         if (G == 1) PTB_HCONV_LAUNCH(2, 1, 1);
