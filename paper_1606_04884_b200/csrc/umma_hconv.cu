@@ -43,7 +43,7 @@ namespace {
 
 using namespace umma;
 
-constexpr int kThreadsH = 320;
+constexpr int kThreadsH = 352;  // + warp 10: the weight (B) producer
 constexpr int kSmemLimitH = 232448;
 // epilogue neighbour exchange: [tile parity][bn/16 chunks][3 warps][G-1 deltas][G-1 lanes][16]
 // floats (two tile buffers: a warp may write tile t+1's slot while its neighbour still
@@ -148,9 +148,13 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     const int cid = blockIdx.x / (2 * PPC), ncl = gridDim.x / (2 * PPC);
     constexpr int kCtaSpan = 129 - G;  // positions a CTA advances per tile
 
-    if (warp == 0) {
+    if (warp == 0 || warp == 10) {
+        // ===== TMA producers (both CTAs; bytes complete on the leader's barriers): warp 0
+        // the pixel runs (A), warp 10 the weights (B), each walking the same stage sequence
+        // on its own ring — one thread issuing both let a full B ring stall the A prefetch
+        // (the B ring holds only ~2 A stages' worth of taps) =====
+        const bool doA = warp == 0, doB = warp == 10;
         if (lane == 0) {
-            // ===== TMA producer (both CTAs; bytes complete on the leader's barriers) =====
             int as = 0, bs = 0;
             uint32_t aph = 0, bph = 0;
             const uint32_t btx = 2 * p.stage_b;
@@ -180,6 +184,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 const int brow = G > 1 ? 0 : nt * p.bn + (int)rank * (p.bn / 2);
                 for (int r = 0; r < p.kH; ++r) {
                     for (int cc = 0; cc < p.chunks; cc += CPS) {
+                        if (doA) {
                         mbar_wait(&aempty[as], aph ^ 1);
                         if (leader) mbar_arrive_expect_tx(&afull[as], atx_t);
                         // NR full padded rows from the dense NHWC tensor (out-of-bounds = the zero
@@ -210,7 +215,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             as = 0;
                             aph ^= 1;
                         }
-                        for (int s = 0; s < p.kW; s += G) {
+                        }  // doA
+                        for (int s = 0; doB && s < p.kW; s += G) {
                             mbar_wait(&bempty[bs], bph ^ 1);
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
                             uint8_t* bdst = sB + (size_t)bs * p.stage_b;
@@ -310,7 +316,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 mma_commit_cg2_warp_mask(&tfull[acc], pair_mask);
             }
         }
-    } else {
+    } else if (warp < 10) {
         // ===== epilogue: TMEM -> registers -> (+bias) -> NCHW, border columns dropped =====
         const uint32_t q = warp & 3;            // TMEM lane quarter
         const int half = (int)(warp - 2) >> 2;  // column chunks half, 2*k + half
