@@ -545,6 +545,11 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.stage_b = cps * p.box_b;
     // B ring: enough stages to cover two filter rows' worth of taps; A ring: the rest
     int sb = std::min(16, std::max(4, pair ? 2 * (int)ceil_div(kW, G) : 2 * kW));
+    static const int sb_env = [] {
+        const char* e = std::getenv("PT_B200_HCONV_SB");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (sb_env >= 2) sb = sb_env;
     while (sb > 3 && budget - sb * (int)p.stage_b < 2 * (int)p.stage_a) --sb;
     int sa = (budget - sb * (int)p.stage_b) / (int)p.stage_a;
     sa = std::min(sa, 8);

@@ -320,3 +320,23 @@ def test_hankel_two_runs_forced_edge_geometries():
     errs = json.loads(r.stdout.strip().splitlines()[-1])
     for g, e in zip(HANKEL_EDGE, errs):
         assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
+
+
+def test_fdgrad_opt_in_small_c():
+    """PT_B200_FDGRAD=1: the gcol GEMM + fused col2im fold dgrad for C <= 4 stride-1
+    layers (opt-in engine), TF32 tolerance vs oracle on the small-C geometries."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    geoms = [g for g in SMALLC_GEOMS if g.kW <= 12]
+    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW] for g in geoms]
+    env = dict(os.environ, PT_B200_FDGRAD="1")
+    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
+                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    errs = json.loads(r.stdout.strip().splitlines()[-1])
+    for g, e in zip(geoms, errs):
+        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
