@@ -294,9 +294,12 @@ bool hwgrad_ok(const Geo& g) {
     if (env == 0) return false;
     if (g.sH != 1 || g.sW != 1 || g.C < 32) return false;
     // quads of taps: kW = 9 computes 12 tap slots (75%), worth it against the im2col
-    // engine's L2->SM bound; 3x3 layers (75%) already run near that on the im2col engine
-    if (env != 2 && g.kW < 7) return false;
+    // engine's L2->SM bound; 3x3 layers (75%) with >= 128 channels already run near that on
+    // the im2col engine, but with <= 64 channels (one chunk pair: VGG-A conv2, the
+    // space-to-depth conv1s) the quads win (VGG-A conv2 wgrad 0.27 -> 0.20 ms, AlexNet
+    // conv1 0.113 -> 0.064)
     const HWPlan w = hwplan(g);
+    if (env != 2 && g.kW < 7 && w.Cp > 64) return false;
     // useful fraction of the MMA work: tap slots x pixel columns x pixel rows computed
     // (convnet L2 0.75, L3 0.72 -> faster than the im2col engine; L4, 10x10 outputs in
     // 16-column stages: 0.55 -> slower, 0.046 -> 0.052 ms)
