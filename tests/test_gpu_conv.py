@@ -340,3 +340,24 @@ def test_fdgrad_opt_in_small_c():
     errs = json.loads(r.stdout.strip().splitlines()[-1])
     for g, e in zip(geoms, errs):
         assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
+
+
+# default-engine parity for shapes that select the newer paths: two position tiles per
+# weight stage (short reduction), tap-quad wgrad at <= 64 channels, flat tiling with
+# border filter-row skipping (large padding)
+DEFAULT_PATHS = [
+    po.geom(2, 64, 30, 30, 128, 3, 3, 1, 1, 1, 1),     # VGG conv2-like: RUNS = 2 fwd, quad wgrad
+    po.geom(3, 64, 18, 21, 64, 3, 3, 1, 1, 1, 1),      # 64 -> 64, odd sizes
+    po.geom(2, 64, 24, 24, 128, 9, 9, 0, 0, 1, 1),     # L2-like: flat dgrad (8-row zero border)
+    po.geom(2, 32, 17, 23, 48, 7, 7, 3, 3, 1, 1),      # padded 7x7
+]
+
+
+@pytest.mark.parametrize("g", DEFAULT_PATHS, ids=gstr)
+def test_default_engine_paths(g):
+    (x, w, b, gy), (y, gx, gw, gb) = run_all(g, "tf32", seed=57)
+    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
+    check_tf32(y, ry, "fwd")
+    check_tf32(gx, rgx, "dgrad")
+    check_tf32(gw, rgw, "wgrad")
+    np.testing.assert_allclose(gb, rgb, rtol=1e-5, atol=1e-4)
