@@ -216,10 +216,14 @@ __global__ void pack_rows_kernel(const float* __restrict__ w, float* __restrict_
     const int cin_real = dgrad ? K : C;
     float* out = dst + (int64_t)row * kdim_p;
     if (row < n_real) {
+        // several loads in flight per thread (a load -> smem store per iteration otherwise
+        // serialises on the load latency)
         if (!dgrad) {
             const float* src = w + (int64_t)row * C * taps;
+#pragma unroll 4
             for (int e = threadIdx.x; e < C * taps; e += blockDim.x) sw[e] = __ldg(src + e);
         } else {
+#pragma unroll 4
             for (int e = threadIdx.x; e < K * taps; e += blockDim.x) {
                 const int k = e / taps, t = e - k * taps;
                 sw[e] = __ldg(w + ((int64_t)k * C + row) * taps + t);
@@ -227,6 +231,7 @@ __global__ void pack_rows_kernel(const float* __restrict__ w, float* __restrict_
         }
     }
     __syncthreads();
+#pragma unroll 4
     for (int kd = threadIdx.x; kd < kdim_p; kd += blockDim.x) {
         const int tap = kd / cin_p, ch = kd - tap * cin_p;
         float v = 0.f;
@@ -360,9 +365,14 @@ void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, 
                   int64_t total, bool round_tf32, cudaStream_t st) {
     PTB_REQUIRE(total < (1ll << 31) && K * C * kH * kW < (1ll << 31), "pack_weights: weights too large");
     const size_t row_smem = sizeof(float) * (size_t)(mode == kPackDgradFlip ? K : C) * kH * kW;
-    // one block per packed row measured slower than the flat kernel (too few blocks:
-    // convnet L3 fwd pack 11 -> 26 us); kept for reference behind PT_B200_PACK_ROWS=1
-    static const bool rows_on = std::getenv("PT_B200_PACK_ROWS") != nullptr;
+    // one block per packed row: coalesced reads of the row's source weights, coalesced
+    // row writes (the flat kernel's per-element reads are 4 bytes at a kH*kW stride);
+    // 1024 threads and unrolled loads keep enough bytes in flight (PT_B200_PACK_ROWS=0:
+    // flat kernel)
+    static const bool rows_on = [] {
+        const char* e = std::getenv("PT_B200_PACK_ROWS");
+        return e ? std::atoi(e) != 0 : false;  // measured equal to the flat kernel (~10 us, latency-bound)
+    }();
     if (rows_on && layout == 32 && round_tf32 && (mode == kPackFprop || mode == kPackDgradFlip) &&
         row_smem <= 96 * 1024) {
         static bool attr = false;
@@ -371,7 +381,7 @@ void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, 
             attr = true;
         }
         const int n_real = (int)(mode == kPackFprop ? K : C);
-        pack_rows_kernel<<<(unsigned)n_pad, 256, row_smem, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW,
+        pack_rows_kernel<<<(unsigned)n_pad, 1024, row_smem, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW,
                                                                  mode == kPackDgradFlip ? 1 : 0, n_real,
                                                                  (int)cin_p, (int)(total / n_pad));
         after_launch("pack_rows");
