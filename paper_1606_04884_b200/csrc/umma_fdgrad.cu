@@ -210,27 +210,38 @@ __global__ void __launch_bounds__(kThreadsF, 1) umma_fdgrad_kernel(const __grid_
                         }
                         tmem_ld_wait();
                         }
+                        // the four groups' folds interleaved (independent shuffle chains)
+                        float own[4], spl[4];
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            own[b] = __uint_as_float(v[b][0]);
+                            spl[b] = 0.f;
+                        }
+#pragma unroll
+                        for (int s = 1; s < 12; ++s) {
+                            if (s < p.kW) {
+                                float x[4];
+#pragma unroll
+                                for (int b = 0; b < 4; ++b)
+                                    x[b] = (p.exp & 4) ? __uint_as_float(v[b][s])
+                                                       : __shfl_sync(0xffffffffu, __uint_as_float(v[b][s]), (lane - s) & 31);
+#pragma unroll
+                                for (int b = 0; b < 4; ++b) {
+                                    if ((int)lane >= s) own[b] += x[b];
+                                    else spl[b] += x[b];
+                                }
+                            }
+                        }
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             const int g = gb + 2 * b;
-                            if (g >= g_end) break;
-                            // own[x = px] = sum_s D[px - s][s] (lanes >= s of this warp); the
-                            // lanes below s take lane + 32 - s's value: the next quarter's cell
-                            float own = __uint_as_float(v[b][0]), spl = 0.f;
-#pragma unroll
-                            for (int s = 1; s < 12; ++s) {
-                                if (s < p.kW) {
-                                    const float x = (p.exp & 4) ? __uint_as_float(v[b][s]) : __shfl_sync(0xffffffffu, __uint_as_float(v[b][s]), (lane - s) & 31);
-                                    if ((int)lane >= s) own += x;
-                                    else spl += x;
-                                }
+                            if (g < g_end && !(p.exp & 16)) {
+                                const int r = g / p.C, c = g - r * p.C;
+                                int slot = slot0 + r;
+                                if (slot >= p.kH) slot -= p.kH;
+                                ring[(c * p.kH + slot) * p.ring_w + px] += own[b];
+                                if ((int)lane < p.kW - 1) spill[((c * p.kH + slot) * 5 + q + 1) * 32 + lane] += spl[b];
                             }
-                            const int r = g / p.C, c = g - r * p.C;
-                            int slot = slot0 + r;
-                            if (slot >= p.kH) slot -= p.kH;
-                            if (p.exp & 16) { if (own == 1234.5f && spl == 1.f) ring[0] = 0.f; continue; }
-                            ring[(c * p.kH + slot) * p.ring_w + px] += own;
-                            if ((int)lane < p.kW - 1) spill[((c * p.kH + slot) * 5 + q + 1) * 32 + lane] += spl;
                         }
                     }
                     if (!(p.exp & 32)) {
