@@ -256,31 +256,31 @@ void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, flo
               bool inner_gw_plain, const float* finput = nullptr) {
     int64_t fph = 0, fpw = 0;
     if (finput && !finput_layout(g, math, &fph, &fpw)) finput = nullptr;
-        char* base = ws;
-        if (gx && gw && bwd_shared(g, math)) {
-            // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
-            float* gyh = reinterpret_cast<float*>(base);
-            float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
-            char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
-            char* wws = dws + align_up(bwd_data_ws(g, math), 256);
-            {
-                PassScope pass("bwd");
-                ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
-                nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate, part,
-                                  st);
-            }
-            bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
-            if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, st, finput, fph, fpw);
-            else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st, finput, fph, fpw);
-            return;
+    char* base = ws;
+    if (gx && gw && bwd_shared(g, math)) {
+        // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
+        float* gyh = reinterpret_cast<float*>(base);
+        float* part = reinterpret_cast<float*>(base + gyh_bytes(g));
+        char* dws = base + gyh_bytes(g) + bias_part_bytes(g);
+        char* wws = dws + align_up(bwd_data_ws(g, math), 256);
+        {
+            PassScope pass("bwd");
+            ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
+            nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate, part,
+                              st);
         }
-        if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
-        if (gw) {
-            if (inner_gw_plain)
-                bwd_filter_impl(g, x, gy, gw, gb, 1.f, 0, math, base, st, scale, accumulate, finput);
-            else
-                bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st, scale, accumulate, finput);
-        }
+        bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
+        if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, st, finput, fph, fpw);
+        else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, st, finput, fph, fpw);
+        return;
+    }
+    if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
+    if (gw) {
+        if (inner_gw_plain)
+            bwd_filter_impl(g, x, gy, gw, gb, 1.f, 0, math, base, st, scale, accumulate, finput);
+        else
+            bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, base, st, scale, accumulate, finput);
+    }
 }
 
 
