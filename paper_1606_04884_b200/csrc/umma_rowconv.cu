@@ -200,27 +200,31 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
 // x NCHW -> zero-bordered NHWC with 4 channels: xp[n][Hp][Wa][4], TF32-rounded.
 __global__ void pad_nhwc4_kernel(const float* __restrict__ x, float4* __restrict__ xp, int64_t N, int C,
                                  int H, int W, int pH, int pW, int Hp, int Wa) {
-    const int64_t total = N * Hp * Wa;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t n = e / ((int64_t)Hp * Wa);
-        const int rem = (int)(e - n * Hp * Wa);
-        const int h = rem / Wa - pH, w = rem % Wa - pW;
+    // one block per padded row (n, hp): no 64-bit division per element (it made this
+    // 58 MB pass take 21 us)
+    const int64_t row = blockIdx.x;
+    const int n = (int)(row / Hp), hp = (int)(row - (int64_t)n * Hp);
+    const int h = hp - pH;
+    const bool hin = h >= 0 && h < H;
+    const float* src = x + ((int64_t)n * C * H + (hin ? h : 0)) * W;
+    float4* dst = xp + row * Wa;
+    for (int wa = threadIdx.x; wa < Wa; wa += blockDim.x) {
+        const int w = wa - pW;
         float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (h >= 0 && h < H && w >= 0 && w < W) {
-            for (int c = 0; c < C; ++c) {
-                uint32_t r;
-                const float f = __ldg(x + ((n * C + c) * H + h) * W + w);
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
-                v[c] = __uint_as_float(r);
+        if (hin && w >= 0 && w < W) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (c < C) {
+                    uint32_t r;
+                    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(__ldg(src + (int64_t)c * H * W + w)));
+                    v[c] = __uint_as_float(r);
+                }
             }
         }
-        xp[e] = make_float4(v[0], v[1], v[2], v[3]);
+        dst[wa] = make_float4(v[0], v[1], v[2], v[3]);
     }
 }
 
-// W KCRS -> Bw[half][r][s][n'][4] with n = half*Np/2 + n' (s padded to S2, n to Np,
-// channels to 4), TF32-rounded; each half is one contiguous block of w_half floats.
 __global__ void pack_rowconv_w_kernel(const float* __restrict__ w, float* __restrict__ bw, int K, int C,
                                       int kH, int kW, int S2, int Np, int64_t w_half) {
     const int Nh = Np / 2;
@@ -269,9 +273,9 @@ RowPlan rplan(const Geo& g) {
 
 void pad_nhwc4(const float* x, float* xp, const Geo& g, int Hp, int Wa, cudaStream_t st) {
     const int64_t total = g.N * Hp * Wa;
-    pad_nhwc4_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count()), 256, 0,
-                       st>>>(x, reinterpret_cast<float4*>(xp), g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.pH,
-                             (int)g.pW, Hp, Wa);
+    (void)total;
+    pad_nhwc4_kernel<<<(unsigned)(g.N * Hp), Wa >= 256 ? 256 : 128, 0, st>>>(
+        x, reinterpret_cast<float4*>(xp), g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.pH, (int)g.pW, Hp, Wa);
     after_launch("pad_nhwc4");
 }
 
@@ -296,9 +300,9 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + g.N * rp.Hp * rp.Wa * 4));
         const int64_t total = g.N * rp.Hp * rp.Wa;
-        pad_nhwc4_kernel<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 16 * (int64_t)sm_count()), 256, 0,
-                           st>>>(x, reinterpret_cast<float4*>(xp), g.N, (int)g.C, (int)g.H, (int)g.W,
-                                 (int)g.pH, (int)g.pW, rp.Hp, rp.Wa);
+        (void)total;
+        pad_nhwc4_kernel<<<(unsigned)(g.N * rp.Hp), rp.Wa >= 256 ? 256 : 128, 0, st>>>(
+            x, reinterpret_cast<float4*>(xp), g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.pH, (int)g.pW, rp.Hp, rp.Wa);
         after_launch("pad_nhwc4");
     }
     pack_rowconv_w_kernel<<<(unsigned)ceil_div(2 * rp.w_half, 256), 256, 0, st>>>(

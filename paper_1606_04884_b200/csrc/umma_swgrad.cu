@@ -215,24 +215,39 @@ __global__ void expand_planes_kernel(const float* __restrict__ x, float4* __rest
     }
 }
 
-// gw[k][c][r][s] = (acc ? gw : 0) + scale * sum_cta part[cta][k][r*P + s*C + c]  (cta order).
-// One thread per partial column (k, col): consecutive threads read consecutive columns.
+// gw[k][c][r][s] = (acc ? gw : 0) + scale * sum_cta part[cta][k][r*P + s*C + c]. Four
+// threads per partial column (k, col) each sum a quarter of the slabs in order, then the
+// quarters are added in order (fixed tree: deterministic); consecutive threads read
+// consecutive columns. (One thread per column over ~148 slabs was latency-bound: 24 us.)
 __global__ void swgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ gw, int K, int C,
                                      int kH, int kW, int npad, int ctas, float scale, int accumulate) {
+    __shared__ float red[4][64];
     const int P = kW * C;
     const int total = K * npad;
     const int64_t slab = (int64_t)K * npad;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const int k = i / npad, col = i - k * npad;
-        const int r = col / P, pl = col - r * P;
-        if (r >= kH) continue;
-        const int s = pl / C, c = pl - s * C;
-        const float* src = part + i;
+    const int qtr = threadIdx.x >> 6, li = threadIdx.x & 63;
+    const int per = (ctas + 3) / 4, b0 = qtr * per, b1 = min(ctas, b0 + per);
+    for (int base = blockIdx.x * 64; base < total; base += gridDim.x * 64) {
+        const int i = base + li;
         float acc = 0.f;
+        if (i < total) {
+            const float* src = part + i;
 #pragma unroll 8
-        for (int b = 0; b < ctas; ++b) acc += __ldg(src + b * slab);
-        const int64_t o = (((int64_t)k * C + c) * kH + r) * kW + s;
-        gw[o] = (accumulate ? gw[o] : 0.f) + scale * acc;
+            for (int b = b0; b < b1; ++b) acc += __ldg(src + b * slab);
+        }
+        red[qtr][li] = acc;
+        __syncthreads();
+        if (qtr == 0 && i < total) {
+            const float sum = ((red[0][li] + red[1][li]) + red[2][li]) + red[3][li];
+            const int k = i / npad, col = i - k * npad;
+            const int r = col / P, pl = col - r * P;
+            if (r < kH) {
+                const int s = pl / C, c = pl - s * C;
+                const int64_t o = (((int64_t)k * C + c) * kH + r) * kW + s;
+                gw[o] = (accumulate ? gw[o] : 0.f) + scale * sum;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -374,7 +389,7 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
         after_launch("umma_swgrad");
     }
     const int64_t n = g.K * w.npad;
-    swgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256, 0, st>>>(
+    swgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 64), 16 * (int64_t)sm_count()), 256, 0, st>>>(
         part, gw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, w.npad, w.ctas, scale, accumulate);
     after_launch("swgrad_reduce");
 }
