@@ -499,7 +499,12 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
         const int bn8 = (int)((pl.n_rows + 7) / 8 * 8), bn16 = (int)((pl.n_rows + 15) / 16 * 16);
         int best_g = 2, best_bn = bn8;
         double best_cost = 1e30;
-        for (int G = 2; G <= hconv_group_max(); ++G) {
+        // a short reduction per tap (filter rows x 32-channel chunks <= 9) leaves the tile
+        // epilogue-paced, and the epilogue grows with G: pairs only (L1 dgrad 0.38 -> 0.32 ms,
+        // VGG-A conv1 dgrad 0.246 -> 0.206, Overfeat conv1 dgrad 0.112 -> 0.093; L2 dgrad,
+        // 36 per tap, keeps G = 3: 0.79 vs 0.87 ms with pairs)
+        const int g_max = (pl.taps / kW) * (pl.cin_p / 32) <= 9 ? 2 : hconv_group_max();
+        for (int G = 2; G <= g_max; ++G) {
             const int bn = (G % 2 == 1) ? bn16 : bn8;
             if (G * bn > 256 || (G * bn) % 16 != 0) continue;
             const double cost = (double)ceil_div(kW, G) * std::max(64.0, G * bn / 2.0);
