@@ -346,16 +346,23 @@ __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar) {
 // output pixel) and store them to NCHW: out[ch * chan_stride] for ch = ch0 .. ch0+ncols-1
 // (`out` already points at the pixel of channel ch0), adding bias[ch] when given.
 // Channels >= n_valid are skipped. tcgen05.ld is warp-collective: every lane calls this.
+// sbias: when non-null, the bias staged in shared memory (whole channel range, zero past
+// n_valid) replaces the global bias loads (an L2 round trip per 16 columns per tile sat on
+// the store path of short-reduction kernels).
 __device__ __forceinline__ void store_tmem_columns_nchw(uint32_t taddr, int ncols, float* out,
                                                         int64_t chan_stride, const float* bias,
-                                                        int ch0, int n_valid, bool valid) {
+                                                        int ch0, int n_valid, bool valid,
+                                                        const float* sbias = nullptr) {
     for (int c0 = 0; c0 < ncols; c0 += 16) {
         uint32_t v[16];
         tmem_ld_32x32b_x16(taddr + c0, v);
         float bv[16];
         const int chb = ch0 + c0;
         const bool full16 = chb + 16 <= n_valid;
-        if (bias && full16) {
+        if (sbias) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) bv[q] = sbias[chb + q];
+        } else if (bias && full16) {
             const float4* b4 = reinterpret_cast<const float4*>(bias + chb);
             if ((reinterpret_cast<uintptr_t>(b4) & 15) == 0) {
 #pragma unroll

@@ -63,6 +63,7 @@ struct UConvParams {
     uint32_t tmem_cols;
     float* out;
     const float* bias;
+    int sbias_n;  // > 0: bias staged in smem (this many floats, zero past n_rows)
     int64_t out_hw;
 };
 
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
     uint64_t* tfull = empty + S;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* sbias = reinterpret_cast<float*>(tmem_holder + 4);  // [sbias_n] staged bias (epilogue)
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = CG == 2 ? cluster_rank() : 0;
@@ -254,6 +256,11 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
         // ===== epilogue: TMEM -> registers -> (+bias) -> NCHW =====
         const uint32_t q = warp & 3;            // TMEM lane quarter
         const int half = (int)(warp - 2) >> 2;  // this warp drains column chunks 2*k + half
+        if (p.sbias_n > 0) {  // the bias once per CTA (an L2 round trip per chunk per tile otherwise)
+            for (int e = (int)((warp - 2) * 32 + lane); e < p.sbias_n; e += 256)
+                sbias[e] = e < p.n_rows ? __ldg(p.bias + e) : 0.f;
+            asm volatile("bar.sync 3, 256;" ::: "memory");
+        }
         int it = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
             const uint32_t acc = it & 1;
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
             for (int c0 = half * 16; c0 < p.bn; c0 += 32)
                 store_tmem_columns_nchw(taddr + c0, 16,
                                         p.out + (valid ? base + (int64_t)(ch0 + c0) * p.out_hw : 0), p.out_hw,
-                                        p.bias, ch0 + c0, nv, valid);
+                                        p.bias, ch0 + c0, nv, valid, p.sbias_n > 0 ? sbias : nullptr);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -390,14 +397,15 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
     p.m_tiles = (int)ceil_div(M, (int64_t)kTileM * pl.cg);
     p.stage_a = pl.cb == 32 ? kBoxA * slots_per_stage : kBoxA;  // CG=2: sps 32-deep boxes per stage
     p.stage_b = pl.cb == 32 ? (uint32_t)(pl.bn / pl.cg) * 128u * slots_per_stage : (uint32_t)pl.bn * 128u;
-    int s = (kSmemLimit - 1024 - 256) / (int)(p.stage_a + p.stage_b);
+    p.sbias_n = (bias && pl.n_rows <= 4096) ? (int)((pl.n_rows + 15) / 16 * 16 + 16) : 0;
+    int s = (kSmemLimit - 1024 - 256 - p.sbias_n * 4) / (int)(p.stage_a + p.stage_b);
     p.stages = s > 8 ? 8 : s;
     p.tmem_cols = tmem_cols_for(pl.bn);
     p.out = out;
     p.bias = bias;
     p.out_hw = oH * oW;
     const size_t smem =
-        1024 + (size_t)p.stages * (p.stage_a + p.stage_b) + (2 * p.stages + 4) * 8 + 16;
+        1024 + (size_t)p.stages * (p.stage_a + p.stage_b) + (2 * p.stages + 4) * 8 + 16 + (size_t)p.sbias_n * 4;
     const int num_tiles = p.m_tiles * p.n_tiles;
     const int clusters = std::min(num_tiles, sm_count() / pl.cg);
     ProfScope prof("umma_conv", st, alg_flops, 0.0);

@@ -79,6 +79,8 @@ struct HConvParams {
                          // = two consecutive CTA tiles), filter rows whose input rows lie entirely in
                          // the zero border are skipped
     int tpc, ctiles, aH; // flat: CTA tiles per image, in total; input rows
+    int sbias_n;         // > 0: bias staged in smem (this many floats, zero past n_rows)
+    uint32_t xch_bytes_; // bytes of the G > 1 exchange region (the staged bias follows it)
     CUtensorMap tmap_run;  // im2col over the dense NHWC act: {32 ch, run_px positions}, virtual kW = 1
     float* out;
     const float* bias;
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     uint64_t* tempty = tfull + 4;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 4);
     float* xch = reinterpret_cast<float*>(tmem_holder + 4);  // G > 1: [8 chunks][3 warps][G-1][G-1][16]
+    float* sbias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xch) + p.xch_bytes_);
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t crank = cluster_rank();
@@ -372,6 +375,12 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         const uint32_t q = warp & 3;            // TMEM lane quarter
         const int half = (int)(warp - 2) >> 2;  // column chunks half, 2*k + half
         const int64_t ohw = (int64_t)p.oH * p.oW;
+        if (p.sbias_n > 0) {  // the bias once per CTA (an L2 round trip per chunk per tile otherwise)
+            for (int e = (int)((warp - 2) * 32 + lane); e < p.sbias_n; e += 256)
+                sbias[e] = e < p.n_rows ? __ldg(p.bias + e) : 0.f;
+            asm volatile("bar.sync 3, 256;" ::: "memory");
+        }
+        const float* sb = p.sbias_n > 0 ? sbias : nullptr;
         int it = 0;
         for (int uu = cid; uu * PPC < num_units; uu += ncl, ++it) {
             const int u0 = uu * PPC + (int)pr;
@@ -409,7 +418,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                 for (int c0 = half * 16; c0 < p.bn; c0 += 32)
                     store_tmem_columns_nchw(lane_base + (acc * RUNS + run) * p.bn + c0, 16,
                                             p.out + (valid ? base + (int64_t)c0 * ohw : 0), ohw, p.bias,
-                                            ch0 + c0, p.n_rows, valid);
+                                            ch0 + c0, p.n_rows, valid, sb);
             } else {
                 const uint32_t taddr = lane_base + (acc * RUNS + run) * G * p.bn;
                 for (int c0 = half * 16; c0 < p.bn; c0 += 32) {
@@ -421,7 +430,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                     const bool full16 = chb + 16 <= p.n_rows;
                     float bv[16];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) bv[e] = (p.bias && chb + e < p.n_rows) ? __ldg(p.bias + chb + e) : 0.f;
+                    for (int e = 0; e < 16; ++e)
+                        bv[e] = sb ? sb[chb + e] : (p.bias && chb + e < p.n_rows) ? __ldg(p.bias + chb + e) : 0.f;
                     tmem_ld_wait();
 #pragma unroll
                     for (int e = 0; e < 16; ++e) acc_v[e] = __uint_as_float(vd[0][e]);
@@ -529,7 +539,8 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     const uint32_t box_a = p.a_run ? (uint32_t)align_up((size_t)p.run_px * 128, 1024) : (uint32_t)(NR * Wp) * 128u;
     // B per CTA: G*bn/2 rows of the (delta, c) stack (G > 1), else bn/2 rows of one tap
     const uint32_t box_b = (uint32_t)align_up((size_t)(pair ? G * pl.bn / 2 : pl.bn / 2), 8) * 128u;
-    const int budget = kSmemLimitH - 1024 - 512 - xch_bytes(G, pl.bn);
+    const int sbias_n = (bias && pl.n_rows <= 4096) ? (int)((pl.n_rows + 15) / 16 * 16 + 16) : 0;
+    const int budget = kSmemLimitH - 1024 - 512 - xch_bytes(G, pl.bn) - sbias_n * 4;
     // RUNS = 2 (two position tiles per weight stage) for tiles with a short reduction (their
     // per-tile fixed costs dominate: VGG-A conv2 fwd, 72 MMAs per tile, 0.289 -> 0.200 ms;
     // convnet L2 fwd, 648 per tile, unchanged), when both accumulators of a unit still leave
@@ -630,7 +641,9 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         p.exp = e ? std::atoi(e) : 0;
     }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
-                        (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn);
+                        (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn) + (size_t)sbias_n * 4;
+    p.sbias_n = sbias_n;
+    p.xch_bytes_ = (uint32_t)xch_bytes(G, pl.bn);
     // flat tiling (run mode, no multicast clusters): consecutive CTA tiles over whole images
     // only where border filter rows are worth skipping (>= 5% of the (row, filter row)
     // pairs: convnet L2 dgrad, 8-row zero border, 0.82 -> 0.78 ms); elsewhere the image-halves

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
     uint64_t* tempty = tfull + 2;
     uint64_t* wbar = tempty + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wbar + 1);
+    float* sbias = reinterpret_cast<float*>(tmem_holder + 4);  // [Np] bias staged once (epilogue)
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
@@ -168,6 +169,11 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
         const uint32_t q = warp & 3;
         int it = 0;
         const int64_t ohw = (int64_t)p.oH * p.oW;
+        if (p.bias) {
+            for (int e = (int)((warp - 2) * 32 + lane); e < p.Np; e += 128)
+                sbias[e] = e < p.n_rows ? __ldg(p.bias + e) : 0.f;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         for (int u = cid; u < pairs; u += ncl, ++it) {
             const uint32_t acc = it & 1;
             mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
             const int64_t base = (int64_t)n * p.n_rows * ohw + (int64_t)i * p.oW + j;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.Np;
             if ((p.exp & 1) == 0) store_tmem_columns_nchw(taddr, p.Np, p.out + (valid ? base : 0), ohw, p.bias, 0,
-                                    p.n_rows, valid);
+                                    p.n_rows, valid, p.bias ? sbias : nullptr);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -346,7 +352,7 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     p.tiles = (int)(g.N * g.oH * rp.segs);
     p.stage_a = (uint32_t)align_up((size_t)p.stage_bytes, 1024);
     p.w_bytes = (uint32_t)(rp.w_half * 4);
-    const int avail = kSmemLimit - 1024 - 512 - (int)align_up(p.w_bytes, 1024);
+    const int avail = kSmemLimit - 1024 - 512 - (int)align_up(p.w_bytes, 1024) - rp.Np * 4;
     int s = avail / (int)p.stage_a;
     p.stages = s > kMaxStagesR ? kMaxStagesR : s;
     uint32_t cols = 32;
@@ -354,8 +360,8 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     p.tmem_cols = cols;
     p.out = y;
     p.bias = b;
-    const size_t smem =
-        1024 + align_up(p.w_bytes, 1024) + (size_t)p.stages * p.stage_a + (2 * p.stages + 5) * 8 + 16;
+    const size_t smem = 1024 + align_up(p.w_bytes, 1024) + (size_t)p.stages * p.stage_a + (2 * p.stages + 5) * 8 +
+                        16 + (size_t)rp.Np * 4;  // + the staged bias
     const int pairs = (p.tiles + 1) / 2;
     const int ncl = std::min(pairs, sm_count() / 2);
     static bool attr = false;
