@@ -29,7 +29,7 @@ namespace {
 
 using namespace umma;
 
-constexpr int kThreadsR = 192;
+constexpr int kThreadsR = 320;  // warps 2..9: epilogue (4 or 8 used, p.epi)
 // A-ring depth: each stage is one ~2.5 KB row-segment TMA load feeding only kW/2 MMAs,
 // so many loads must be in flight to cover L2 latency
 static int kMaxStagesR = [] {
@@ -43,6 +43,7 @@ struct RowConvParams {
     uint32_t stage_bytes; // bytes one CTA's stage TMA delivers
     uint32_t row16;       // bytes between consecutive rows in a stage, >> 4
     int exp;  // timing experiments (PT_B200_ROWCONV_EXP; wrong results if != 0)
+    int epi;  // epilogue warps: 4, or 8 (two per TMEM lane quarter, each half of the columns)
     CUtensorMap tmap_x;  // xp viewed (128 floats, Wa*4/128 chunks, N*Hp rows), box {128, seg_chunks, 1}
     CUtensorMap tmap_w;  // packed weights viewed (128 floats, w_chunks, 2 halves), box {128, w_chunks, 1}
     int oH, oW, Hp, kH, S2;  // S2 = kW rounded up to even
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 8);
+            mbar_init(&tempty[i], 2 * p.epi);
         }
         mbar_init(wbar, 2);
         fence_mbar_init();
@@ -165,14 +166,17 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
                 mma_commit_cg2_warp(&tfull[acc]);
             }
         }
-    } else {
+    } else if (warp < 2 + (uint32_t)p.epi) {
         const uint32_t q = warp & 3;
+        const int half = (int)(warp - 2) >> 2;  // p.epi == 8: this warp's column half
+        const int ncol = p.epi == 8 ? p.Np / 2 : p.Np, col0 = half * ncol;
         int it = 0;
         const int64_t ohw = (int64_t)p.oH * p.oW;
         if (p.bias) {
-            for (int e = (int)((warp - 2) * 32 + lane); e < p.Np; e += 128)
+            for (int e = (int)((warp - 2) * 32 + lane); e < p.Np; e += 32 * p.epi)
                 sbias[e] = e < p.n_rows ? __ldg(p.bias + e) : 0.f;
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (p.epi == 8) asm volatile("bar.sync 1, 256;" ::: "memory");
+            else asm volatile("bar.sync 1, 128;" ::: "memory");
         }
         for (int u = cid; u < pairs; u += ncl, ++it) {
             const uint32_t acc = it & 1;
@@ -184,9 +188,10 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
             const int j = seg * 128 + (int)(q * 32 + lane);
             const bool valid = t < p.tiles && j < p.oW;
             const int64_t base = (int64_t)n * p.n_rows * ohw + (int64_t)i * p.oW + j;
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.Np;
-            if ((p.exp & 1) == 0) store_tmem_columns_nchw(taddr, p.Np, p.out + (valid ? base : 0), ohw, p.bias, 0,
-                                    p.n_rows, valid, p.bias ? sbias : nullptr);
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.Np + col0;
+            if ((p.exp & 1) == 0)
+                store_tmem_columns_nchw(taddr, ncol, p.out + (valid ? base + (int64_t)col0 * ohw : 0), ohw, p.bias, col0,
+                                        p.n_rows, valid, p.bias ? sbias : nullptr);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -349,6 +354,13 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     p.seg_chunks = rp.seg_chunks;
     p.n_rows = (int)g.K;
     p.Np = rp.Np;
+    // 8 epilogue warps, each half of the columns (VGG-A conv1, output-write bound: 0.210 ->
+    // 0.181 ms; convnet L1 unchanged)
+    static const int epi_env = [] {
+        const char* e = std::getenv("PT_B200_ROWCONV_EPI");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.epi = epi_env == 4 || epi_env == 8 ? epi_env : (rp.Np % 32 == 0 ? 8 : 4);
     p.tiles = (int)(g.N * g.oH * rp.segs);
     p.stage_a = (uint32_t)align_up((size_t)p.stage_bytes, 1024);
     p.w_bytes = (uint32_t)(rp.w_half * 4);
@@ -372,7 +384,7 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * ncl);
-    cfg.blockDim = dim3(kThreadsR);
+    cfg.blockDim = dim3(64 + 32 * p.epi);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
