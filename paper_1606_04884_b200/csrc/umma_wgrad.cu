@@ -347,6 +347,9 @@ WPlan wplan(const Geo& g) {
     // depth halve the bytes per TMA request), so one m-tile per unit is the default
     w.mt = (wgrad_mt_env() == 2 && w.bn <= 128 && w.m_tiles >= 2) ? 2 : 1;
     w.kp = w.mt == 2 ? 32 : wgrad_kp_env();
+    // <= 64 channels (two 32-channel chunks): 64-pixel stages measured faster (AlexNet conv2
+    // wgrad 0.110 -> 0.099 ms)
+    if (w.kp == 128 && w.Cp <= 64 && std::getenv("PT_B200_WGRAD_KPIX") == nullptr) w.kp = 64;
     // a 128-pixel stage must still leave a 2-deep ring (bn = 256 would get one stage:
     // VGG-A conv4 wgrad 0.33 -> 0.60 ms)
     if (w.kp == 128 && 2 * (4 * 128 * 128 + (w.bn / 64) * 128 * 128) > kSmemLimit - 2048) w.kp = 64;
