@@ -361,3 +361,10 @@ def test_default_engine_paths(g):
     check_tf32(gx, rgx, "dgrad")
     check_tf32(gw, rgw, "wgrad")
     np.testing.assert_allclose(gb, rgb, rtol=1e-5, atol=1e-4)
+
+
+def test_randomised_channel_rich_geometries():
+    """24 random channel-rich geometries (tests/stress_tc.py) through the default engines."""
+    import stress_tc
+    worst, bad = stress_tc.run(24, 11)
+    assert not bad, f"worst {worst:.3e}: {bad[:3]}"
