@@ -326,8 +326,8 @@ def main():
 
     peaks, peak_kind = load_peaks()
     clocks = ClockSampler(local)
-    L.lib().pt_b200_profile_enable(1)
-    L.lib().pt_b200_profile_reset()
+    L.lib().pt_b200_profile_enable(0)
+    L.lib().pt_b200_set_bwd_streams(1)
     launches0 = pt.launch_count()
     if world > 1:
         dist.barrier()
@@ -345,6 +345,20 @@ def main():
     clk = clocks.stop()
     launches = pt.launch_count() - launches0
     ms = e0.elapsed_time(e1)
+    # per-launch kernel timings: a second pass of the same steps with the backward's two
+    # streams serialised — in the timed region the input- and weight-gradient kernels run
+    # concurrently, so per-launch event spans there would overlap
+    L.lib().pt_b200_set_bwd_streams(0)
+    L.lib().pt_b200_profile_enable(1)
+    L.lib().pt_b200_profile_reset()
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for _ in range(args.steps):
+        step()
+    p1.record()
+    torch.cuda.synchronize()
+    ms_serial = p0.elapsed_time(p1)
     prof = {c: L.profile_read(c) for c in ("umma_conv", "umma_wgrad", "simt_conv", "layout")}
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -372,6 +386,7 @@ def main():
                 lay[f"{s_['name']}.{ps}"] = {"ms": v[0] / args.steps, "launches": v[1] // args.steps,
                                              "gbs": v[3] / (v[0] * 1e-3) / 1e9 if v[0] > 0 else None}
     L.lib().pt_b200_profile_enable(0)
+    L.lib().pt_b200_set_bwd_streams(1)
     tf32_cublas = measure_cublas_tf32(torch) if rank == 0 else None
     tf32_derived = peaks.get("bf16_tflops", 1590.0) / 2.0
     # denominator: the measured TF32 tensor-pipe ceiling of this GPU (back-to-back MMAs,
@@ -388,7 +403,10 @@ def main():
     roof["kernel"] = dom
     roof["avg_launch_ms"] = avg_ms
     roof["flops_per_launch"] = dfl / dn
-    roof["share_of_step"] = dms / ms if ms > 0 else None
+    roof["share_of_step"] = dms / ms_serial if ms_serial > 0 else None
+    roof["timing"] = ("per-launch CUDA events in a serialised pass of the same steps right after the "
+                      f"timed region ({ms_serial / args.steps:.3f} ms/step serialised vs "
+                      f"{ms / args.steps:.3f} ms/step timed with the backward's two streams)")
     roof["peak_source"] = (f"max(measured TF32 MMA ceiling on this box = {tf32_mma:.1f} "
                            f"[pt_b200_tf32_mma_peak], cuBLAS TF32 8192^3 = {tf32_cublas}, "
                            f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})")

@@ -174,6 +174,11 @@ double pt_b200_tf32_mma_peak(void);
  * synchronises the recorded events. Kernel classes: "umma_conv" (tcgen05 fprop/dgrad),
  * "umma_wgrad" (tcgen05 wgrad), "simt_conv" (FFMA passes), "layout" (NHWC/pack passes). */
 int pt_b200_profile_enable(int on);
+/* Scheduling of the combined backward (pt_b200_conv_bwd / _finput): 1 (default) runs the
+ * weight gradient on an internal per-device stream concurrently with the input gradient
+ * (fork/join with events on the caller's stream, results unchanged); 0 serialises them on
+ * the caller's stream (per-launch event timings then measure each kernel alone). */
+int pt_b200_set_bwd_streams(int on);
 int pt_b200_profile_reset(void);
 /* Label for the launches the calling thread records next (e.g. the layer name); each
  * launch is also accumulated under "<class>@<tag>.<pass>", pass = fwd | dgrad | wgrad. */

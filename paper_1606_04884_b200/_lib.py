@@ -95,6 +95,7 @@ _SIGS = {
     "pt_b200_launch_count": (C.c_int64, []),
     "pt_b200_tf32_mma_peak": (C.c_double, []),
     "pt_b200_profile_enable": (C.c_int, [C.c_int]),
+    "pt_b200_set_bwd_streams": (C.c_int, [C.c_int]),
     "pt_b200_profile_reset": (C.c_int, []),
     "pt_b200_profile_tag": (C.c_int, [C.c_char_p]),
     "pt_b200_profile_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
