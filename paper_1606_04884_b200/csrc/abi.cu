@@ -252,30 +252,11 @@ void require_ws(size_t have, size_t need, const void* ws) {
 // Combined backward body (pt_b200_conv_bwd). inner_gw_plain: write gw with unit scale and
 // overwrite (the s2d wrapper applies the caller's scale / accumulate in its remap) while
 // gradBias still takes the caller's scale / accumulate.
-// Side stream (one per device, non-blocking) for the weight gradient of the combined
-// backward: it and the input gradient only share the transformed gy, so running them
-// concurrently lets each kernel's last partial wave overlap the other's (each is a
-// persistent kernel sized to the whole GPU). PT_B200_BWD_STREAMS=1 serialises them.
-cudaStream_t side_stream() {
-    static std::mutex mu;
-    static cudaStream_t streams[64] = {};
-    int dev = 0;
-    PTB_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(mu);
-    if (dev < 0 || dev >= 64) return nullptr;
-    if (!streams[dev]) PTB_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
-    return streams[dev];
-}
-std::atomic<int> g_bwd_streams{-1};  // -1: PT_B200_BWD_STREAMS (default 2 streams)
-bool bwd_two_streams() {
-    static const bool env_on = [] {
-        const char* e = std::getenv("PT_B200_BWD_STREAMS");
-        return e ? std::atoi(e) != 1 : true;
-    }();
-    const int v = g_bwd_streams.load(std::memory_order_relaxed);
-    return v < 0 ? env_on : v != 0;
-}
-
+// The combined backward runs the weight gradient on an internal stream (Fork slot 0)
+// concurrently with the input gradient: they only share the transformed gy, and each
+// kernel's last partial wave then overlaps the other's (each is a persistent kernel sized
+// to the whole GPU). pt_b200_set_bwd_streams(0) serialises (the bench's per-launch timing
+// pass).
 void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, float* gx, float* gw,
               float* gb, float scale, int accumulate, int math, char* ws, cudaStream_t st,
               bool inner_gw_plain, const float* finput = nullptr) {
@@ -294,25 +275,11 @@ void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, flo
             nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate, part,
                               st);
         }
-        cudaStream_t side = bwd_two_streams() ? side_stream() : nullptr;
-        cudaStream_t wst = side ? side : st;
-        if (side) {  // fork: the weight gradient waits for the gy transform only
-            cudaEvent_t fork;
-            PTB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-            PTB_CUDA(cudaEventRecord(fork, st));
-            PTB_CUDA(cudaStreamWaitEvent(side, fork, 0));
-            PTB_CUDA(cudaEventDestroy(fork));
-        }
-        if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, wst, finput, fph, fpw);
-        else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, wst, finput, fph, fpw);
+        Fork fk(st, 0);  // fork: the weight gradient waits for the gy transform only
+        if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, fk.side, finput, fph, fpw);
+        else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, fk.side, finput, fph, fpw);
         bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
-        if (side) {  // join: the caller's stream sees both gradients
-            cudaEvent_t join;
-            PTB_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-            PTB_CUDA(cudaEventRecord(join, side));
-            PTB_CUDA(cudaStreamWaitEvent(st, join, 0));
-            PTB_CUDA(cudaEventDestroy(join));
-        }
+        fk.join();  // the caller's stream sees both gradients
         return;
     }
     if (gx) bwd_data_impl(g, gy, w, gx, math, ws, st);
@@ -605,7 +572,7 @@ static int conv_bwd_entry(const pt_conv_geom* gp, const float* x, const float* g
 }
 
 int pt_b200_set_bwd_streams(int on) {
-    g_bwd_streams.store(on ? 1 : 0, std::memory_order_relaxed);
+    set_concurrency(on);
     return PT_OK;
 }
 

@@ -84,6 +84,19 @@ struct ProfScope {
     ProfScope(const char* c, cudaStream_t s, double f, double b);
     ~ProfScope();
 };
+// Concurrency of independent work inside one API call (pt_b200_set_bwd_streams): internal
+// per-device non-blocking streams (slot 0: the backward's weight gradient, slot 1: weight
+// packs next to layout passes) joined back to the caller's stream with events.
+bool concurrency_on();
+void set_concurrency(int on);
+cudaStream_t aux_stream(int slot);
+// fork(st, slot): work submitted to .side after this waits for everything already on st;
+// join(): st waits for everything submitted to .side. side == st when concurrency is off.
+struct Fork {
+    cudaStream_t st, side;
+    Fork(cudaStream_t s, int slot);
+    void join();
+};
 // Labels the launches recorded while alive with the conv pass ("fwd", "dgrad", "wgrad").
 struct PassScope {
     const char* prev;

@@ -1,5 +1,7 @@
 // profile.cu — CUDA-event timing of the library's hot kernels on their own
 // launching stream (bench.py reads it for the roofline's per-launch duration).
+#include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -67,6 +69,52 @@ ProfScope::~ProfScope() {
     // per-launch key "class@tag.pass" (e.g. umma_conv@L2.dgrad) beside the class total
     std::string key = g_tag.empty() && !*g_pass ? std::string() : std::string(cls) + "@" + g_tag + "." + g_pass;
     g_pending.push_back({cls, std::move(key), e0, e1, flops, bytes});
+}
+
+namespace {
+std::atomic<int> g_conc{-1};  // -1: PT_B200_BWD_STREAMS (default on)
+}  // namespace
+
+bool concurrency_on() {
+    static const bool env_on = [] {
+        const char* e = std::getenv("PT_B200_BWD_STREAMS");
+        return e ? std::atoi(e) != 1 : true;
+    }();
+    const int v = g_conc.load(std::memory_order_relaxed);
+    return v < 0 ? env_on : v != 0;
+}
+void set_concurrency(int on) { g_conc.store(on ? 1 : 0, std::memory_order_relaxed); }
+
+cudaStream_t aux_stream(int slot) {
+    static std::mutex mu;
+    static cudaStream_t streams[64][2] = {};
+    int dev = 0;
+    PTB_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64 || slot < 0 || slot > 1) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!streams[dev][slot]) PTB_CUDA(cudaStreamCreateWithFlags(&streams[dev][slot], cudaStreamNonBlocking));
+    return streams[dev][slot];
+}
+
+Fork::Fork(cudaStream_t s, int slot) : st(s), side(s) {
+    if (!concurrency_on()) return;
+    cudaStream_t a = aux_stream(slot);
+    if (!a) return;
+    cudaEvent_t e;
+    PTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    PTB_CUDA(cudaEventRecord(e, st));
+    PTB_CUDA(cudaStreamWaitEvent(a, e, 0));
+    PTB_CUDA(cudaEventDestroy(e));
+    side = a;
+}
+void Fork::join() {
+    if (side == st) return;
+    cudaEvent_t e;
+    PTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    PTB_CUDA(cudaEventRecord(e, side));
+    PTB_CUDA(cudaStreamWaitEvent(st, e, 0));
+    PTB_CUDA(cudaEventDestroy(e));
+    side = st;
 }
 
 }  // namespace ptb

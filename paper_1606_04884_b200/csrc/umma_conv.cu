@@ -608,15 +608,17 @@ void umma_conv_fwd(const Geo& g, const UmmaPlan& pl, const float* x, const float
     float* act = act_out ? act_out : reinterpret_cast<float*>(ws);
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
     PTB_REQUIRE(!act_ready || act_out, "umma_conv_fwd: act_ready without act_out");
+    Fork fk(st, 1);  // the weight pack (latency-bound, ~10 us) beside the layout pass
+    if (pl.hankel && pl.tap_group > 1)
+        pack_grouped(w, wt, g.K, g.C, g.kH, g.kW, false, pl.tap_group, pl.bn, pl.cin_p, fk.side);
+    else
+        pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackFprop, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
+                     pl.wt_elems, true, fk.side);
     if (!act_ready) {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + g.N * g.HW * pl.cin_p));
         nchw_to_nhwc(x, act, g.N, g.C, g.HW, pl.cin_p, true, st);
     }
-    if (pl.hankel && pl.tap_group > 1)
-        pack_grouped(w, wt, g.K, g.C, g.kH, g.kW, false, pl.tap_group, pl.bn, pl.cin_p, st);
-    else
-        pack_weights(w, wt, g.K, g.C, g.kH, g.kW, kPackFprop, pl.cb, pl.n_pad, pl.cin_p, pl.slots_p,
-                     pl.wt_elems, true, st);
+    fk.join();
     if (pl.hankel) {
         run_hconv(pl, act, wt, g.N, g.H, g.W, g.pH, g.pW, (int)g.kH, (int)g.kW, g.oH, g.oW, y, b,
                   2.0 * g.M * g.K * g.CRS, st);

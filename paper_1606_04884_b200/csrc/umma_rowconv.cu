@@ -308,6 +308,10 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
     const RowPlan rp = rplan(g);
     float* xp = reinterpret_cast<float*>(ws);
     float* bw = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(rp.xp_elems * 4, 256));
+    Fork fk(st, 1);  // the filter pack beside the layout pass
+    pack_rowconv_w_kernel<<<(unsigned)ceil_div(2 * rp.w_half, 256), 256, 0, fk.side>>>(
+        w, bw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, rp.S2, rp.Np, rp.w_half);
+    after_launch("pack_rowconv_w");
     {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW + g.N * rp.Hp * rp.Wa * 4));
         const int64_t total = g.N * rp.Hp * rp.Wa;
@@ -316,9 +320,7 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
             x, reinterpret_cast<float4*>(xp), g.N, (int)g.C, (int)g.H, (int)g.W, (int)g.pH, (int)g.pW, rp.Hp, rp.Wa);
         after_launch("pad_nhwc4");
     }
-    pack_rowconv_w_kernel<<<(unsigned)ceil_div(2 * rp.w_half, 256), 256, 0, st>>>(
-        w, bw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, rp.S2, rp.Np, rp.w_half);
-    after_launch("pack_rowconv_w");
+    fk.join();
 
     RowConvParams p;
     memset(&p, 0, sizeof p);
