@@ -95,6 +95,11 @@ cudaStream_t aux_stream(int slot);
 struct Fork {
     cudaStream_t st, side;
     Fork(cudaStream_t s, int slot);
+    Fork(const Fork&) = delete;
+    Fork& operator=(const Fork&) = delete;
+    // An error thrown between fork and join still leaves st ordered after the side work,
+    // so the caller never frees or reuses buffers the side stream is still reading.
+    ~Fork();
     void join();
 };
 // Labels the launches recorded while alive with the conv pass ("fwd", "dgrad", "wgrad").

@@ -107,6 +107,13 @@ Fork::Fork(cudaStream_t s, int slot) : st(s), side(s) {
     PTB_CUDA(cudaEventDestroy(e));
     side = a;
 }
+Fork::~Fork() {
+    if (side == st) return;
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+    if (cudaEventRecord(e, side) == cudaSuccess) cudaStreamWaitEvent(st, e, 0);
+    cudaEventDestroy(e);
+}
 void Fork::join() {
     if (side == st) return;
     cudaEvent_t e;
