@@ -84,6 +84,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-finput", action="store_true", help="re-lay x out in the weight gradient")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the step eagerly instead of replaying its CUDA graph (N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -328,6 +330,28 @@ def main():
     clocks = ClockSampler(local)
     L.lib().pt_b200_profile_enable(0)
     L.lib().pt_b200_set_bwd_streams(1)
+    # N=1: the step (every layer's forward + combined backward, internal streams included)
+    # is captured once as a CUDA graph and replayed, so the GPU never waits on the host's
+    # per-launch work (~0.5 ms of ctypes + tensor-map encoding per step). N>1 launches
+    # eagerly: the gradient allreduce is not captured.
+    run, graph, graph_launches = step, None, 0
+    if world == 1 and not args.no_graph:
+        cur = torch.cuda.current_stream()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):  # the capture stream's workspace, allocated outside
+            step()
+        cur.wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        c0 = pt.launch_count()
+        with torch.cuda.graph(graph):
+            step()
+        graph_launches = pt.launch_count() - c0
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+        run = graph.replay
     launches0 = pt.launch_count()
     if world > 1:
         dist.barrier()
@@ -337,13 +361,13 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        step()
+        run()
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    launches = pt.launch_count() - launches0
+    launches = pt.launch_count() - launches0 + graph_launches * args.steps * (graph is not None)
     ms = e0.elapsed_time(e1)
     # per-launch kernel timings: a second pass of the same steps with the backward's two
     # streams serialised — in the timed region the input- and weight-gradient kernels run
@@ -423,6 +447,7 @@ def main():
         "config": {"workload": args.workload, "layers": [l[0] for l in layers],
                    "global_batch": layers[0][1] * world, "per_gpu_batch": layers[0][1],
                    "parallelism": f"dp{world}", "math": args.math,
+                   "launch": "one CUDA-graph replay per step" if graph is not None else "eager",
                    "l2": "no flush: per-step working set "
                          f"{sum(4*(s['x'].numel()+s['y'].numel()+s['gy'].numel()+s['gx'].numel()) for s in st)/1e9:.2f} GB > 126 MB L2"},
         "clocks": clk, "gpu_launches": launches, "roofline": roof,
