@@ -49,7 +49,6 @@ struct FDParams {
     int sa;               // A ring depth
     uint32_t stage_a, b_bytes, b_off, tmem_cols;
     float* slab;          // [bands][C][kBand + kH - 1][W]
-    int exp;              // timing experiments (PT_B200_FDGRAD_EXP, wrong results if != 0)
 };
 
 __global__ void __launch_bounds__(kThreadsF, 1) umma_fdgrad_kernel(const __grid_constant__ FDParams p) {
@@ -183,24 +182,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) umma_fdgrad_kernel(const __grid_
                     tc_fence_after();
                     const uint32_t taddr = tmem_base + ((q * 32u) << 16) + (uint32_t)(h * p.nhalf);
                     const int g0 = h * p.gpr, g_end = min(p.ngroups, g0 + p.gpr);
-                    if (p.exp & 32) {  // timing: release the region before folding it
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (leader) mbar_arrive(&tempty[h]);
-                            else mbar_arrive_cluster(&tempty[h], 0);
-                        }
-                    }
                     // batches of 4 of this warp's groups: 12 TMEM loads under one wait, then
                     // four independent shuffle folds
-                    for (int gb = g0 + half; gb < g_end && !(p.exp & 1); gb += 8) {
+                    for (int gb = g0 + half; gb < g_end; gb += 8) {
                         uint32_t v[4][12];
-                        if (p.exp & 8) {
-#pragma unroll
-                            for (int b = 0; b < 4; ++b)
-#pragma unroll
-                                for (int k = 0; k < 12; ++k) v[b][k] = lane + k + b;
-                        } else {
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             const int gl = min(gb + 2 * b, g_end - 1) - g0;
@@ -209,7 +194,6 @@ __global__ void __launch_bounds__(kThreadsF, 1) umma_fdgrad_kernel(const __grid_
                                 tmem_ld_32x32b_x4(taddr + gl * 12 + 4 * k, *reinterpret_cast<uint32_t(*)[4]>(&v[b][4 * k]));
                         }
                         tmem_ld_wait();
-                        }
                         // the four groups' folds interleaved (independent shuffle chains)
                         float own[4], spl[4];
 #pragma unroll
@@ -223,8 +207,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) umma_fdgrad_kernel(const __grid_
                                 float x[4];
 #pragma unroll
                                 for (int b = 0; b < 4; ++b)
-                                    x[b] = (p.exp & 4) ? __uint_as_float(v[b][s])
-                                                       : __shfl_sync(0xffffffffu, __uint_as_float(v[b][s]), (lane - s) & 31);
+                                    x[b] = __shfl_sync(0xffffffffu, __uint_as_float(v[b][s]), (lane - s) & 31);
 #pragma unroll
                                 for (int b = 0; b < 4; ++b) {
                                     if ((int)lane >= s) own[b] += x[b];
@@ -235,7 +218,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) umma_fdgrad_kernel(const __grid_
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             const int g = gb + 2 * b;
-                            if (g < g_end && !(p.exp & 16)) {
+                            if (g < g_end) {
                                 const int r = g / p.C, c = g - r * p.C;
                                 int slot = slot0 + r;
                                 if (slot >= p.kH) slot -= p.kH;
@@ -244,16 +227,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) umma_fdgrad_kernel(const __grid_
                             }
                         }
                     }
-                    if (!(p.exp & 32)) {
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (leader) mbar_arrive(&tempty[h]);
-                            else mbar_arrive_cluster(&tempty[h], 0);
-                        }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (leader) mbar_arrive(&tempty[h]);
+                        else mbar_arrive_cluster(&tempty[h], 0);
                     }
                 }
-                if (p.exp & 2) continue;
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 // gx row (band row0 + t - pH) is complete for this band: slab row t
                 for (int e = tid; e < p.C * p.W; e += ept) {
@@ -464,10 +444,6 @@ void fdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, 
     p.b_off = (uint32_t)align_up(f.b_bytes, 1024);
     p.tmem_cols = f.tmem_cols;
     p.slab = slab;
-    {
-        const char* e = std::getenv("PT_B200_FDGRAD_EXP");
-        p.exp = e ? std::atoi(e) : 0;
-    }
     static bool attr = false;
     if (!attr) {
         PTB_CUDA(cudaFuncSetAttribute(umma_fdgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitF));

@@ -69,7 +69,6 @@ struct HConvParams {
     int sa, sb;          // ring depths
     uint32_t stage_a, stage_b;  // bytes per stage (CPS boxes)
     uint32_t box_a, box_b;      // bytes per 32-channel box
-    int exp;                    // timing experiments (PT_B200_HCONV_EXP; wrong results if != 0)
     uint32_t tmem_cols;
     int nacc;            // TMEM accumulator buffers (2 or 4)
     int mc;              // 1: clusters of two CTA pairs sharing each weight stage by TMA multicast
@@ -636,10 +635,6 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     PTB_REQUIRE(p.tmem_cols <= 512, "hconv: accumulators exceed TMEM");
     p.out = out;
     p.bias = bias;
-    {
-        const char* e = std::getenv("PT_B200_HCONV_EXP");
-        p.exp = e ? std::atoi(e) : 0;
-    }
     const size_t smem = 1024 + (size_t)sa * p.stage_a + (size_t)sb * p.stage_b +
                         (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn) + (size_t)sbias_n * 4;
     p.sbias_n = sbias_n;

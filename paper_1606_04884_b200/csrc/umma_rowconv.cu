@@ -42,7 +42,6 @@ struct RowConvParams {
     int rps;              // padded input rows per pipeline stage
     uint32_t stage_bytes; // bytes one CTA's stage TMA delivers
     uint32_t row16;       // bytes between consecutive rows in a stage, >> 4
-    int exp;  // timing experiments (PT_B200_ROWCONV_EXP; wrong results if != 0)
     int epi;  // epilogue warps: 4, or 8 (two per TMEM lane quarter, each half of the columns)
     CUtensorMap tmap_x;  // xp viewed (128 floats, Wa*4/128 chunks, N*Hp rows), box {128, seg_chunks, 1}
     CUtensorMap tmap_w;  // packed weights viewed (128 floats, w_chunks, 2 halves), box {128, w_chunks, 1}
@@ -142,7 +141,7 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
                 const int npair = p.S2 / 2;
                 constexpr uint32_t kHi = desc_hi(128, kSwizzleNone);
                 for (int r0 = 0; r0 < p.kH; r0 += p.rps) {
-                    if ((p.exp & 2) == 0 || it == 0) mbar_wait(&full[stage], phase);
+                    mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t abase = desc_lo(smem_u32(sA + (size_t)stage * p.stage_a), 16);
                     const int rn = p.kH - r0 < p.rps ? p.kH - r0 : p.rps;
@@ -153,9 +152,8 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
                         const uint32_t alo = abase + (uint32_t)rr * p.row16;
                         uint32_t blo = desc_lo(wbase + (uint32_t)(r * p.S2) * lbo_b, lbo_b);
                         for (int k = 0; k < npair; ++k, blo += bstep)
-                            if ((p.exp & 4) == 0)
-                                mma_tf32_cg2_warp(d, desc_make(alo + 2u * k, kHi), desc_make(blo, kHi), idesc,
-                                                  (r | k) != 0);
+                            mma_tf32_cg2_warp(d, desc_make(alo + 2u * k, kHi), desc_make(blo, kHi), idesc,
+                                              (r | k) != 0);
                     }
                     mma_commit_cg2_warp(&empty[stage]);
                     if (++stage == S) {
@@ -189,9 +187,8 @@ __global__ void __launch_bounds__(kThreadsR, 1) umma_rowconv_kernel(const __grid
             const bool valid = t < p.tiles && j < p.oW;
             const int64_t base = (int64_t)n * p.n_rows * ohw + (int64_t)i * p.oW + j;
             const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * p.Np + col0;
-            if ((p.exp & 1) == 0)
-                store_tmem_columns_nchw(taddr, ncol, p.out + (valid ? base + (int64_t)col0 * ohw : 0), ohw, p.bias, col0,
-                                        p.n_rows, valid, p.bias ? sbias : nullptr);
+            store_tmem_columns_nchw(taddr, ncol, p.out + (valid ? base + (int64_t)col0 * ohw : 0), ohw, p.bias, col0,
+                                    p.n_rows, valid, p.bias ? sbias : nullptr);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -342,10 +339,6 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
         const uint64_t strides[2] = {512, (uint64_t)rp.w_half * 4};
         const uint32_t box[3] = {128, (uint32_t)rp.w_chunks, 1};
         tmap_tiled(&p.tmap_w, bw, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
-    }
-    {
-        const char* e = std::getenv("PT_B200_ROWCONV_EXP");
-        p.exp = e ? std::atoi(e) : 0;
     }
     p.oH = (int)g.oH;
     p.oW = (int)g.oW;
