@@ -428,9 +428,10 @@ def main():
     roof["avg_launch_ms"] = avg_ms
     roof["flops_per_launch"] = dfl / dn
     roof["share_of_step"] = dms / ms_serial if ms_serial > 0 else None
-    roof["timing"] = ("per-launch CUDA events in a serialised pass of the same steps right after the "
-                      f"timed region ({ms_serial / args.steps:.3f} ms/step serialised vs "
-                      f"{ms / args.steps:.3f} ms/step timed with the backward's two streams)")
+    roof["timing"] = ("per-launch CUDA events in a serialised, eagerly launched pass of the same steps "
+                      f"right after the timed region ({ms_serial / args.steps:.3f} ms/step serialised vs "
+                      f"{ms / args.steps:.3f} ms/step timed: backward's two streams, "
+                      + ("CUDA-graph replay)" if graph is not None else "eager launches)"))
     roof["peak_source"] = (f"max(measured TF32 MMA ceiling on this box = {tf32_mma:.1f} "
                            f"[pt_b200_tf32_mma_peak], cuBLAS TF32 8192^3 = {tf32_cublas}, "
                            f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})")
