@@ -633,6 +633,10 @@ void umma_conv_bwd_data(const Geo& g, const UmmaPlan& pl, const float* gy, const
     if (alg_flops < 0) alg_flops = 2.0 * g.M * g.K * g.CRS;
     float* act = reinterpret_cast<float*>(ws);
     float* wt = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + align_up(pl.act_elems * 4, 256));
+    // a shared gy copy (the combined backward's NHWC transform, channels padded to 32) is only
+    // this plan's operand when the plan reads 32-channel chunks of exactly that padding (a
+    // small-K plan packs gy to 8/16 channels: relay it itself)
+    if (gyh_pre && !(pl.cb == 32 && pl.cin_p == (g.K + 31) / 32 * 32)) gyh_pre = nullptr;
     if (gyh_pre) {
         act = const_cast<float*>(gyh_pre);
     } else {

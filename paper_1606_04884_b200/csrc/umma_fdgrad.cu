@@ -395,6 +395,7 @@ void fdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, 
     float* wt = reinterpret_cast<float*>(base);
     float* gyh = reinterpret_cast<float*>(base + f.wt_bytes);
     float* slab = reinterpret_cast<float*>(base + f.wt_bytes + f.gyh_bytes);
+    if (gyh_pre && f.Kp != (g.K + 31) / 32 * 32) gyh_pre = nullptr;  // not the shared padding
     if (!gyh_pre) {
         ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * f.Kp));
         nchw_to_nhwc(gy, gyh, g.N, g.K, g.oHW, f.Kp, true, st);

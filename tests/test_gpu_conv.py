@@ -133,6 +133,45 @@ def test_fused_backward_matches_separate_passes(g, math):
     np.testing.assert_allclose(_h(agb), gb0 + 0.5 * rgb, rtol=1e-5, atol=1e-4)
 
 
+# Small-C layers with fewer than 32 (or a non-multiple of 32) output channels: the combined
+# backward's shared gy copy is padded to 32 channels, which a small-K dgrad plan must not
+# read as its own 8/16-channel layout (found by tests/stress_tc.py).
+SMALLK_COMBINED = [
+    po.geom(3, 3, 32, 10, 16, 7, 7, 3, 3, 1, 1),
+    po.geom(1, 3, 32, 21, 16, 11, 11, 2, 2, 1, 1),
+    po.geom(1, 3, 18, 50, 16, 7, 7, 3, 3, 1, 1),
+    po.geom(2, 3, 20, 24, 8, 5, 5, 2, 2, 1, 1),
+    po.geom(2, 3, 20, 24, 48, 7, 7, 3, 3, 1, 1),
+    po.geom(2, 4, 16, 30, 24, 3, 3, 1, 1, 1, 1),
+    po.geom(2, 3, 35, 35, 16, 11, 11, 2, 2, 4, 4),
+    po.geom(2, 16, 20, 20, 16, 5, 5, 2, 2, 1, 1),
+]
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("g", SMALLK_COMBINED, ids=gstr)
+def test_combined_backward_small_k(g, math):
+    pt = _pt()
+    x, w, b, gy = conv_inputs(g, 41)
+    G = _g(g)
+    nb = pt.finput_bytes(G, math)
+    fin = torch.empty(max(nb, 1), dtype=torch.uint8, device="cuda") if nb else None
+    pt.conv_forward(G, _d(x), _d(w), _d(b), math=math, finput=fin)
+    gx, gw, gb = pt.conv_backward(G, _d(x), _d(gy), _d(w), math=math, finput=fin)
+    sgx = pt.conv_backward_input(G, _d(gy), _d(w), math=math)
+    np.testing.assert_array_equal(_h(gx), _h(sgx))
+    rgx = po.conv_backward_input(g, gy, w)
+    rgw, rgb = po.conv_backward_weight(g, x, gy)
+    oh, ow = po.out_hw(g)
+    if math == "fp32":
+        check_fp32(_h(gx), rgx, g.K * g.kH * g.kW, 1.0, np.abs(w).max(), "dgrad")
+        check_fp32(_h(gw), rgw, g.N * oh * ow, 1.0, 1.0, "wgrad")
+    else:
+        check_tf32(_h(gx), rgx, "dgrad")
+        check_tf32(_h(gw), rgw, "wgrad")
+    np.testing.assert_allclose(_h(gb), rgb, rtol=1e-5, atol=1e-5 * g.N * oh * ow)
+
+
 @pytest.mark.parametrize("name", list(LAYERS))
 def test_convnet_layers_batch_slice(name):
     """L1-L5 at the real per-image shape on a 2-image slice (fwd/dgrad are per-image
