@@ -85,7 +85,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-finput", action="store_true", help="re-lay x out in the weight gradient")
     ap.add_argument("--no-graph", action="store_true",
-                    help="launch the step eagerly instead of replaying its CUDA graph (N=1)")
+                    help="launch the step eagerly instead of replaying each layer's CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
 
@@ -305,16 +305,22 @@ def main():
                        gw=bucket.views[0], gb=bucket.views[1]))
     comm = torch.cuda.Stream(device=dev) if world > 1 else None
 
-    def step():
+    def layer(s):
+        g = s["g"]
+        L.lib().pt_b200_profile_tag(s["name"].encode())
+        # Torch's finput: the forward's relaid input is reused by accGradParameters
+        pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math, finput=s["finput"])
+        pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math,
+                         finput=s["finput"])
+
+    def step(graphs=None):
         cur = torch.cuda.current_stream()
         done = []
-        for s in st:
-            g = s["g"]
-            L.lib().pt_b200_profile_tag(s["name"].encode())
-            # Torch's finput: the forward's relaid input is reused by accGradParameters
-            pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math, finput=s["finput"])
-            pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math,
-                             finput=s["finput"])
+        for i, s in enumerate(st):
+            if graphs is None:
+                layer(s)
+            else:
+                graphs[i].replay()
             # batch-sharded DP: one allreduce(sum) of this layer's gradW||gradB bucket on the
             # comm stream, overlapping the next layer's kernels
             done.append(allreduce_async(s["bucket"], comm))
@@ -330,28 +336,38 @@ def main():
     clocks = ClockSampler(local)
     L.lib().pt_b200_profile_enable(0)
     L.lib().pt_b200_set_bwd_streams(1)
-    # N=1: the step (every layer's forward + combined backward, internal streams included)
-    # is captured once as a CUDA graph and replayed, so the GPU never waits on the host's
-    # per-launch work (~0.5 ms of ctypes + tensor-map encoding per step). N>1 launches
-    # eagerly: the gradient allreduce is not captured.
+    # Each layer's forward + combined backward (internal streams included) is captured once
+    # as a CUDA graph and replayed, so the GPU never waits on the host's per-launch work
+    # (~0.5 ms of ctypes + tensor-map encoding per step). The gradient allreduce stays an
+    # eager NCCL call between the replays, so N=1 and N>1 run the same kernels the same way.
     run, graph, graph_launches = step, None, 0
-    if world == 1 and not args.no_graph:
-        cur = torch.cuda.current_stream()
-        side = torch.cuda.Stream(device=dev)
-        side.wait_stream(cur)
-        with torch.cuda.stream(side):  # the capture stream's workspace, allocated outside
-            step()
-        cur.wait_stream(side)
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        c0 = pt.launch_count()
-        with torch.cuda.graph(graph):
-            step()
-        graph_launches = pt.launch_count() - c0
-        for _ in range(2):
-            graph.replay()
-        torch.cuda.synchronize()
-        run = graph.replay
+    if not args.no_graph:
+        try:
+            cur = torch.cuda.current_stream()
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):  # the capture stream's workspace, allocated outside
+                for s in st:
+                    layer(s)
+            cur.wait_stream(side)
+            torch.cuda.synchronize()
+            graphs = []
+            c0 = pt.launch_count()
+            for s in st:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, capture_error_mode="thread_local"):
+                    layer(s)
+                graphs.append(gr)
+            graph_launches = pt.launch_count() - c0
+            for _ in range(2):
+                step(graphs)
+            torch.cuda.synchronize()
+            graph = graphs
+            run = lambda: step(graphs)  # noqa: E731
+        except Exception as ex:  # pragma: no cover - eager launches instead
+            print(f"bench: CUDA-graph capture failed ({ex}); timing eager launches", file=sys.stderr)
+            torch.cuda.synchronize()
+            run, graph, graph_launches = step, None, 0
     launches0 = pt.launch_count()
     if world > 1:
         dist.barrier()
@@ -448,7 +464,7 @@ def main():
         "config": {"workload": args.workload, "layers": [l[0] for l in layers],
                    "global_batch": layers[0][1] * world, "per_gpu_batch": layers[0][1],
                    "parallelism": f"dp{world}", "math": args.math,
-                   "launch": "one CUDA-graph replay per step" if graph is not None else "eager",
+                   "launch": "one CUDA-graph replay per layer (fwd + bwd), allreduce eager" if graph is not None else "eager",
                    "l2": "no flush: per-step working set "
                          f"{sum(4*(s['x'].numel()+s['y'].numel()+s['gy'].numel()+s['gx'].numel()) for s in st)/1e9:.2f} GB > 126 MB L2"},
         "clocks": clk, "gpu_launches": launches, "roofline": roof,
