@@ -24,6 +24,9 @@ GEOMS = [
     (4, 64, 20, 20, 64, 5, 5, 2, 2, 1, 1),    # Hankel engines, channel-rich wgrad
     (4, 3, 24, 24, 32, 5, 5, 0, 0, 1, 1),     # small-C row kernels
     (2, 32, 17, 19, 48, 3, 3, 1, 1, 2, 2),    # strided, ragged
+    (2, 3, 35, 35, 64, 11, 11, 2, 2, 4, 4),   # space-to-depth (AlexNet conv1-like)
+    (2, 3, 24, 24, 64, 3, 3, 1, 1, 1, 1),     # small-C row forward + plane wgrad (VGG conv1-like)
+    (2, 3, 30, 30, 96, 11, 11, 0, 0, 1, 1),   # convnet L1-like
 ]
 
 
