@@ -14,7 +14,7 @@ METRICS = {
     "gpu__time_duration.sum": "time",
     "dram__bytes_read.sum": "dram_rd",
     "dram__bytes_write.sum": "dram_wr",
-    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_%",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_%",
     "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum": "tma_ld_bytes",
     "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum.per_second": "tma_ld_rate",
     "lts__t_sectors_srcunit_tex.avg.pct_of_peak_sustained_elapsed": "l2_tex_%",
