@@ -7,8 +7,9 @@ import numpy as np
 import pytest
 
 import pyoracle as po
-from helpers import (CFG1, LAYERS, TC_GEOMS, check_fp32, check_tf32, conv_inputs, gstr,
-                     spec_random_geometries, with_batch)
+from engine_check import check_geometry
+from helpers import (CFG1, EPS32, TC_GEOMS, check_fp32, check_tf32, conv_inputs, gstr,
+                     spec_random_geometries, tf32_bounds)
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -51,6 +52,15 @@ def oracle_all(g, x, w, b, gy):
     return y, gx, gw, gb
 
 
+def check_all_tf32(g, inputs, outs, refs=None):
+    """fwd / dgrad / wgrad / gradBias against the oracle with elementwise TF32 bounds."""
+    x, w, b, gy = inputs
+    refs = refs or oracle_all(g, x, w, b, gy)
+    tol = tf32_bounds(g, x, w, b, gy)
+    for o, r, k in zip(outs, refs, ("fwd", "dgrad", "wgrad", "gradBias")):
+        check_tf32(o, r, f"{gstr(g)} {k}", tol[k])
+
+
 @pytest.mark.parametrize("math", ["fp32", "tf32"])
 @pytest.mark.parametrize("g", spec_random_geometries(50), ids=gstr)
 def test_spec_random_geometries(g, math):
@@ -64,9 +74,7 @@ def test_spec_random_geometries(g, math):
         check_fp32(gx, rgx, g.K * g.kH * g.kW, 1.0, np.abs(w).max(), "dgrad")
         check_fp32(gw, rgw, g.N * oh * ow, 1.0, 1.0, "wgrad")
     else:
-        check_tf32(y, ry, "fwd")
-        check_tf32(gx, rgx, "dgrad")
-        check_tf32(gw, rgw, "wgrad")
+        check_all_tf32(g, (x, w, b, gy), (y, gx, gw, gb), (ry, rgx, rgw, rgb))
     np.testing.assert_allclose(gb, rgb, rtol=1e-5, atol=1e-5 * g.N * oh * ow)
 
 
@@ -74,10 +82,15 @@ def test_spec_random_geometries(g, math):
 def test_tensor_core_tiles(g):
     """tcgen05 tile variants (SW128 / small-C, bn 64..256, ragged tiles) in TF32 mode."""
     (x, w, b, gy), (y, gx, gw, gb) = run_all(g, "tf32", seed=77)
-    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
-    check_tf32(y, ry, "fwd")
-    check_tf32(gx, rgx, "dgrad")
-    check_tf32(gw, rgw, "wgrad")
+    check_all_tf32(g, (x, w, b, gy), (y, gx, gw, gb))
+
+
+@pytest.mark.parametrize("g", TC_GEOMS, ids=gstr)
+def test_tensor_core_tiles_exact(g):
+    """TF32-exact integer inputs: bitwise equal to the oracle through the default engines
+    (finput + combined backward and the separate passes)."""
+    fails, _ = check_geometry(g, seed=79, exact=True, real=False)
+    assert not fails, "\n".join(fails[:4])
 
 
 @pytest.mark.parametrize("g", TC_GEOMS[:4], ids=gstr)
@@ -96,8 +109,7 @@ def test_cfg1_full(math):
     (x, w, b, gy), (y, gx, gw, gb) = run_all(CFG1, math)
     ry, rgx, rgw, rgb = oracle_all(CFG1, x, w, b, gy)
     if math == "tf32":
-        for o, r, n in ((y, ry, "fwd"), (gx, rgx, "dgrad"), (gw, rgw, "wgrad")):
-            check_tf32(o, r, n)
+        check_all_tf32(CFG1, (x, w, b, gy), (y, gx, gw, gb), (ry, rgx, rgw, rgb))
     else:
         check_fp32(y, ry, 27, 1.0, np.abs(w).max(), "fwd")
         check_fp32(gx, rgx, 64 * 9, 1.0, np.abs(w).max(), "dgrad")
@@ -129,7 +141,8 @@ def test_fused_backward_matches_separate_passes(g, math):
     if math == "fp32":
         check_fp32(_h(agw), gw0 + 0.5 * rgw, g.N * oh * ow, 1.0, 1.0, "acc wgrad")
     else:
-        check_tf32(_h(agw) - gw0, 0.5 * rgw, "acc wgrad")
+        tol = tf32_bounds(g, x, w, b, gy)["wgrad"]
+        check_tf32(_h(agw), gw0 + 0.5 * rgw, "acc wgrad", 0.5 * tol + 2 * EPS32 * np.abs(gw0))
     np.testing.assert_allclose(_h(agb), gb0 + 0.5 * rgb, rtol=1e-5, atol=1e-4)
 
 
@@ -167,21 +180,10 @@ def test_combined_backward_small_k(g, math):
         check_fp32(_h(gx), rgx, g.K * g.kH * g.kW, 1.0, np.abs(w).max(), "dgrad")
         check_fp32(_h(gw), rgw, g.N * oh * ow, 1.0, 1.0, "wgrad")
     else:
-        check_tf32(_h(gx), rgx, "dgrad")
-        check_tf32(_h(gw), rgw, "wgrad")
+        tol = tf32_bounds(g, x, w, b, gy)
+        check_tf32(_h(gx), rgx, "dgrad", tol["dgrad"])
+        check_tf32(_h(gw), rgw, "wgrad", tol["wgrad"])
     np.testing.assert_allclose(_h(gb), rgb, rtol=1e-5, atol=1e-5 * g.N * oh * ow)
-
-
-@pytest.mark.parametrize("name", list(LAYERS))
-def test_convnet_layers_batch_slice(name):
-    """L1-L5 at the real per-image shape on a 2-image slice (fwd/dgrad are per-image
-    independent; the full-batch runs are covered by property tests)."""
-    g = with_batch(LAYERS[name], 2)
-    (x, w, b, gy), (y, gx, gw, gb) = run_all(g, "tf32", seed=99)
-    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
-    check_tf32(y, ry, f"{name} fwd")
-    check_tf32(gx, rgx, f"{name} dgrad")
-    check_tf32(gw, rgw, f"{name} wgrad")
 
 
 FINPUT_GEOMS = [g for g in TC_GEOMS] + [
@@ -219,50 +221,6 @@ HANKEL_EDGE = [
     po.geom(1, 32, 40, 61, 32, 11, 11, 5, 5, 1, 1),
 ]
 
-_HANKEL_SCRIPT = r"""
-import sys, json
-sys.path[:0] = sys.argv[1:4]
-import numpy as np, torch
-import paper_1606_04884_b200 as pt, pyoracle as po
-from helpers import conv_inputs
-out = []
-for spec in json.loads(sys.argv[4]):
-    g = po.geom(*spec)
-    x, w, b, gy = conv_inputs(g, 91)
-    G = pt.ConvGeometry(*spec)
-    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    y = pt.conv_forward(G, d(x), d(w), d(b))
-    gx, gw, gb = pt.conv_backward(G, d(x), d(gy), d(w))
-    torch.cuda.synchronize()
-    rel = lambda a, r: float(np.linalg.norm(a.cpu().numpy().astype(np.float64) - r) /
-                             max(np.linalg.norm(r), 1e-30))
-    out.append([rel(y, po.conv_direct(g, x, w, b, f64=True)),
-                rel(gx, po.conv_backward_input(g, gy, w)),
-                rel(gw, po.conv_backward_weight(g, x, gy)[0])])
-print(json.dumps(out))
-"""
-
-
-def test_hankel_engine_forced_edge_geometries():
-    """PT_B200_HCONV=1 forces the Hankel engine for every eligible pass (the engine
-    choice is read once per process, hence the subprocess); TF32 tolerance vs oracle."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW]
-             for g in HANKEL_EDGE]
-    env = dict(os.environ, PT_B200_HCONV="1")
-    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
-                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    errs = json.loads(r.stdout.strip().splitlines()[-1])
-    for g, e in zip(HANKEL_EDGE, errs):
-        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
-
-
 @pytest.mark.parametrize("g", HANKEL_EDGE, ids=gstr)
 def test_hankel_edge_default_engines(g):
     """The same edge geometries through whatever engines the default plan picks."""
@@ -271,11 +229,13 @@ def test_hankel_edge_default_engines(g):
     G = _g(g)
     y = pt.conv_forward(G, _d(x), _d(w), _d(b))
     gx, gw, gb = pt.conv_backward(G, _d(x), _d(gy), _d(w))
-    check_tf32(_h(y), po.conv_direct(g, x, w, b, f64=True), "fwd")
-    check_tf32(_h(gx), po.conv_backward_input(g, gy, w), "dgrad")
-    rgw, rgb = po.conv_backward_weight(g, x, gy)
-    check_tf32(_h(gw), rgw, "wgrad")
-    np.testing.assert_allclose(_h(gb), rgb, rtol=1e-5, atol=1e-4)
+    check_all_tf32(g, (x, w, b, gy), (_h(y), _h(gx), _h(gw), _h(gb)))
+
+
+@pytest.mark.parametrize("g", HANKEL_EDGE, ids=gstr)
+def test_hankel_edge_exact(g):
+    fails, _ = check_geometry(g, seed=93, exact=True, real=False)
+    assert not fails, "\n".join(fails[:4])
 
 
 # small-C stride-1 layers: the planes-of-taps weight gradient (umma_swgrad.cu) — odd
@@ -298,15 +258,16 @@ def test_small_c_weight_gradient(g):
     G = _g(g)
     gw, gb = pt.conv_backward_weight(G, _d(x), _d(gy), math="tf32")
     rgw, rgb = po.conv_backward_weight(g, x, gy)
-    check_tf32(_h(gw), rgw, "wgrad")
+    tol = tf32_bounds(g, x, w, b, gy)
+    check_tf32(_h(gw), rgw, "wgrad", tol["wgrad"])
     np.testing.assert_allclose(_h(gb), rgb, rtol=1e-5, atol=1e-4)
     # fused backward with Torch's accumulate / scale: gw = gw0 + 0.5 * dW
     gw0 = po.uniform((g.K, g.C, g.kH, g.kW), 9)
     gb0 = po.uniform((g.K,), 10)
     gx, agw, agb = pt.conv_backward(G, _d(x), _d(gy), _d(w), gw=_d(gw0), gb=_d(gb0), scale=0.5,
                                     accumulate=True, math="tf32")
-    check_tf32(_h(agw) - gw0, 0.5 * rgw, "acc wgrad")
-    check_tf32(_h(gx), po.conv_backward_input(g, gy, w), "dgrad")
+    check_tf32(_h(agw), gw0 + 0.5 * rgw, "acc wgrad", 0.5 * tol["wgrad"] + 2 * EPS32 * np.abs(gw0))
+    check_tf32(_h(gx), po.conv_backward_input(g, gy, w), "dgrad", tol["dgrad"])
 
 
 # Hankel tap-quad weight gradient (umma_hwgrad.cu) forced on: odd chunk counts (C = 96 ->
@@ -319,66 +280,6 @@ HWGRAD_EDGE = [
     po.geom(3, 64, 12, 12, 96, 3, 3, 1, 1, 1, 1),
     po.geom(1, 128, 7, 9, 256, 7, 7, 3, 3, 1, 1),
 ]
-
-
-def test_hwgrad_forced_edge_geometries():
-    """PT_B200_HWGRAD=2 routes every stride-1 C >= 32 weight gradient through the tap-quad
-    kernel (read once per process, hence the subprocess); TF32 tolerance vs oracle."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW]
-             for g in HWGRAD_EDGE]
-    env = dict(os.environ, PT_B200_HWGRAD="2")
-    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
-                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    errs = json.loads(r.stdout.strip().splitlines()[-1])
-    for g, e in zip(HWGRAD_EDGE, errs):
-        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
-
-
-def test_hankel_two_runs_forced_edge_geometries():
-    """PT_B200_HCONV=1 + PT_B200_HCONV_RUNS=2: the Hankel engine with two position tiles
-    per weight stage (odd tile counts -> a dummy second run) on the edge geometries."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW]
-             for g in HANKEL_EDGE]
-    env = dict(os.environ, PT_B200_HCONV="1", PT_B200_HCONV_RUNS="2")
-    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
-                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    errs = json.loads(r.stdout.strip().splitlines()[-1])
-    for g, e in zip(HANKEL_EDGE, errs):
-        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
-
-
-def test_fdgrad_opt_in_small_c():
-    """PT_B200_FDGRAD=1: the gcol GEMM + fused col2im fold dgrad for C <= 4 stride-1
-    layers (opt-in engine), TF32 tolerance vs oracle on the small-C geometries."""
-    import json
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    geoms = [g for g in SMALLC_GEOMS if g.kW <= 12]
-    specs = [[g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.padH, g.padW, g.strideH, g.strideW] for g in geoms]
-    env = dict(os.environ, PT_B200_FDGRAD="1")
-    r = subprocess.run([sys.executable, "-c", _HANKEL_SCRIPT, root, os.path.join(root, "oracle"),
-                        os.path.join(root, "tests"), json.dumps(specs)], env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    errs = json.loads(r.stdout.strip().splitlines()[-1])
-    for g, e in zip(geoms, errs):
-        assert max(e) < 5e-3, f"{gstr(g)}: fwd/dgrad/wgrad rel errors {e}"
 
 
 # default-engine parity for shapes that select the newer paths: two position tiles per
@@ -395,11 +296,7 @@ DEFAULT_PATHS = [
 @pytest.mark.parametrize("g", DEFAULT_PATHS, ids=gstr)
 def test_default_engine_paths(g):
     (x, w, b, gy), (y, gx, gw, gb) = run_all(g, "tf32", seed=57)
-    ry, rgx, rgw, rgb = oracle_all(g, x, w, b, gy)
-    check_tf32(y, ry, "fwd")
-    check_tf32(gx, rgx, "dgrad")
-    check_tf32(gw, rgw, "wgrad")
-    np.testing.assert_allclose(gb, rgb, rtol=1e-5, atol=1e-4)
+    check_all_tf32(g, (x, w, b, gy), (y, gx, gw, gb))
 
 
 def test_randomised_channel_rich_geometries():
