@@ -86,6 +86,7 @@ const char* pt_b200_last_error(void);
 int pt_b200_device_count(void);
 int pt_b200_device_info(int device, pt_device_desc* out);
 int pt_b200_set_device(int device);
+int pt_b200_get_device(int* device);
 int pt_b200_malloc(void** ptr, size_t bytes);
 int pt_b200_free(void* ptr);
 /* device_upload / device_download (proj/src/backend.cpp:163-181): contiguous staging copies. */

@@ -60,6 +60,7 @@ _SIGS = {
     "pt_b200_device_count": (C.c_int, []),
     "pt_b200_device_info": (C.c_int, [C.c_int, C.POINTER(PtDeviceDesc)]),
     "pt_b200_set_device": (C.c_int, [C.c_int]),
+    "pt_b200_get_device": (C.c_int, [C.POINTER(C.c_int)]),
     "pt_b200_malloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_size_t]),
     "pt_b200_free": (C.c_int, [_P]),
     "pt_b200_memcpy_h2d": (C.c_int, [_P, _P, C.c_size_t, _P]),

@@ -104,6 +104,10 @@ def _math(math) -> int:
 def _dev(t: torch.Tensor, shape, what: str) -> int:
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValidationError(f"{what}: expected a CUDA tensor")
+    if t.device.index != torch.cuda.current_device():
+        # the workspace, the stream and the library's device are the current device's
+        raise ValidationError(f"{what}: on {t.device}, but the current device is "
+                              f"cuda:{torch.cuda.current_device()}")
     if t.dtype != torch.float32:
         raise ValidationError(f"{what}: expected float32, got {t.dtype}")
     if shape is not None and tuple(t.shape) != tuple(shape):

@@ -363,6 +363,12 @@ int pt_b200_device_info(int device, pt_device_desc* out) {
 }
 
 int pt_b200_set_device(int device) { return guarded([&] { PTB_CUDA(cudaSetDevice(device)); }); }
+int pt_b200_get_device(int* device) {
+    return guarded([&] {
+        PTB_REQUIRE(device != nullptr, "get_device: null output");
+        PTB_CUDA(cudaGetDevice(device));
+    });
+}
 
 int pt_b200_malloc(void** ptr, size_t bytes) {
     return guarded([&] {

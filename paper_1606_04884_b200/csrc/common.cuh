@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <functional>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -85,11 +86,14 @@ struct ProfScope {
     ~ProfScope();
 };
 // Concurrency of independent work inside one API call (pt_b200_set_bwd_streams): internal
-// per-device non-blocking streams (slot 0: the backward's weight gradient, slot 1: weight
-// packs next to layout passes) joined back to the caller's stream with events.
+// non-blocking streams per (device, caller stream) (slot 0: the backward's weight gradient,
+// slot 1: weight packs next to layout passes) joined back to the caller's stream with events.
 bool concurrency_on();
 void set_concurrency(int on);
-cudaStream_t aux_stream(int slot);
+cudaStream_t aux_stream(cudaStream_t caller, int slot);
+// Runs `set` once per (current device, key) and makes concurrent callers wait until it has
+// run: kernel attributes such as the dynamic shared-memory limit are per device.
+void once_per_device(const void* key, const std::function<void()>& set);
 // fork(st, slot): work submitted to .side after this waits for everything already on st;
 // join(): st waits for everything submitted to .side. side == st when concurrency is off.
 struct Fork {

@@ -375,11 +375,9 @@ void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, 
     }();
     if (rows_on && layout == 32 && round_tf32 && (mode == kPackFprop || mode == kPackDgradFlip) &&
         row_smem <= 96 * 1024) {
-        static bool attr = false;
-        if (!attr) {
+        once_per_device((const void*)pack_rows_kernel, [&] {  // the smem limit is a per-device attribute
             PTB_CUDA(cudaFuncSetAttribute(pack_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-            attr = true;
-        }
+        });
         const int n_real = (int)(mode == kPackFprop ? K : C);
         pack_rows_kernel<<<(unsigned)n_pad, 1024, row_smem, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW,
                                                                  mode == kPackDgradFlip ? 1 : 0, n_real,

@@ -4,6 +4,9 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <set>
+#include <tuple>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -85,20 +88,35 @@ bool concurrency_on() {
 }
 void set_concurrency(int on) { g_conc.store(on ? 1 : 0, std::memory_order_relaxed); }
 
-cudaStream_t aux_stream(int slot) {
+// One internal stream per (device, caller stream, slot): calls on different caller streams
+// (other threads, other CUDA-graph captures) never share an aux stream, so a fork/join on
+// one caller stream neither waits on nor joins another caller's work.
+cudaStream_t aux_stream(cudaStream_t caller, int slot) {
     static std::mutex mu;
-    static cudaStream_t streams[64][2] = {};
+    static std::map<std::tuple<int, cudaStream_t, int>, cudaStream_t> streams;
     int dev = 0;
     PTB_CUDA(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64 || slot < 0 || slot > 1) return nullptr;
+    if (slot < 0 || slot > 1) return nullptr;
     std::lock_guard<std::mutex> lock(mu);
-    if (!streams[dev][slot]) PTB_CUDA(cudaStreamCreateWithFlags(&streams[dev][slot], cudaStreamNonBlocking));
-    return streams[dev][slot];
+    cudaStream_t& s = streams[{dev, caller, slot}];
+    if (!s) PTB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+void once_per_device(const void* key, const std::function<void()>& set) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void*>> done;
+    int dev = 0;
+    PTB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);  // held across set(): no launch before it is done
+    if (done.count({dev, key})) return;
+    set();
+    done.insert({dev, key});
 }
 
 Fork::Fork(cudaStream_t s, int slot) : st(s), side(s) {
     if (!concurrency_on()) return;
-    cudaStream_t a = aux_stream(slot);
+    cudaStream_t a = aux_stream(st, slot);
     if (!a) return;
     cudaEvent_t e;
     PTB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

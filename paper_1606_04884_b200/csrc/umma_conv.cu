@@ -319,12 +319,10 @@ uint32_t tmem_cols_for(int bn) {
 
 template <int CB, int CG, int SPS = 2>
 void launch_k(const UConvParams& p, int grid, size_t smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)umma_conv_kernel<CB, CG, SPS>, [&] {  // the smem limit is a per-device attribute
         PTB_CUDA(cudaFuncSetAttribute(umma_conv_kernel<CB, CG, SPS>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-        attr = true;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreadsU);

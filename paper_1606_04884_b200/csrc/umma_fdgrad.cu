@@ -445,11 +445,9 @@ void fdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, 
     p.b_off = (uint32_t)align_up(f.b_bytes, 1024);
     p.tmem_cols = f.tmem_cols;
     p.slab = slab;
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)umma_fdgrad_kernel, [&] {  // the smem limit is a per-device attribute
         PTB_CUDA(cudaFuncSetAttribute(umma_fdgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitF));
-        attr = true;
-    }
+    });
     const int units = (f.bands + 1) / 2;
     const int pairs = std::min(units, sm_count() / 2);
     cudaLaunchConfig_t cfg = {};

@@ -664,16 +664,14 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     }
     const int cl_ctas = p.mc ? 4 : 2;
     const int ncl = std::min(p.mc ? (units + 1) / 2 : units, sm_count() / cl_ctas);
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)umma_hconv_kernel<1, 1, 1>, [&] {  // the smem limit is a per-device attribute
         for (auto fn : {umma_hconv_kernel<1, 1, 1>, umma_hconv_kernel<1, 2, 1>, umma_hconv_kernel<1, 3, 1>,
                         umma_hconv_kernel<1, 4, 1>, umma_hconv_kernel<2, 1, 1>, umma_hconv_kernel<2, 2, 1>,
                         umma_hconv_kernel<2, 3, 1>, umma_hconv_kernel<2, 4, 1>, umma_hconv_kernel<1, 1, 2>,
                         umma_hconv_kernel<1, 2, 2>, umma_hconv_kernel<2, 1, 2>, umma_hconv_kernel<2, 2, 2>,
                         umma_hconv_kernel<1, 3, 2>, umma_hconv_kernel<2, 3, 2>})
             PTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitH));
-        attr = true;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl_ctas * ncl);
     cfg.blockDim = dim3(kThreadsH);

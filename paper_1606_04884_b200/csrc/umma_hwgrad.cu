@@ -363,8 +363,7 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
     const size_t smem = 1024 + (size_t)w.stages * (w.stage_a + w.stage_b) + (2 * w.stages + 4) * 8 + 16;
     const int units = (int)(g.kH * w.cps * w.n_tiles * w.splits);
     const int pairs = std::min(units, sm_count() / 2);
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)umma_hwgrad_kernel<1>, [&] {  // the smem limit is a per-device attribute
         PTB_CUDA(cudaFuncSetAttribute(umma_hwgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimitHW));
         PTB_CUDA(cudaFuncSetAttribute(umma_hwgrad_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -373,8 +372,7 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
                                       kSmemLimitHW));
         PTB_CUDA(cudaFuncSetAttribute(umma_hwgrad_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimitHW));
-        attr = true;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreadsHW);

@@ -371,12 +371,10 @@ void rowconv_fwd(const Geo& g, const float* x, const float* w, const float* b, f
                         16 + (size_t)rp.Np * 4;  // + the staged bias
     const int pairs = (p.tiles + 1) / 2;
     const int ncl = std::min(pairs, sm_count() / 2);
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)umma_rowconv_kernel, [&] {  // the smem limit is a per-device attribute
         PTB_CUDA(cudaFuncSetAttribute(umma_rowconv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
-        attr = true;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * ncl);
     cfg.blockDim = dim3(64 + 32 * p.epi);

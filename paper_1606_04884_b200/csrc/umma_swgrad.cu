@@ -375,12 +375,10 @@ void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float sca
     p.part = part;
     p.pad = w.pad;
     const size_t smem = 1024 + (size_t)w.stages * (w.stage_a + w.stage_b) + w.pad + (2 * w.stages + 2) * 8 + 16;
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)umma_swgrad_kernel<2>, [&] {  // the smem limit is a per-device attribute
         for (auto fn : {umma_swgrad_kernel<2>, umma_swgrad_kernel<4>, umma_swgrad_kernel<8>})
             PTB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimitS));
-        attr = true;
-    }
+    });
     {
         ProfScope prof("umma_wgrad", st, 2.0 * g.M * g.K * g.CRS, 0.0);
         if (w.R == 8) umma_swgrad_kernel<8><<<(unsigned)w.ctas, kThreadsS, smem, st>>>(p);

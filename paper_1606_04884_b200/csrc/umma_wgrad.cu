@@ -454,16 +454,14 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
                         (2 * p.stages + 4) * 8 + 16;
     const int units = w.m_groups * w.n_tiles * w.splits;
     const int pairs = std::min(units, sm_count() / 2);
-    static bool attr = false;
-    if (!attr) {
+    once_per_device((const void*)umma_wgrad_kernel<1, 64>, [&] {  // the smem limit is a per-device attribute
         PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
         PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
         PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
-        attr = true;
-    }
+    });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreadsW);

@@ -11,22 +11,33 @@ namespace portten::conv {
 
 namespace {
 
-// Grow-only device scratch per thread (conv passes on one stream are ordered).
+// Grow-only device scratch per (device, stream): the conv passes on one stream are ordered,
+// so one buffer per stream is never in use by two passes at once, while calls on different
+// streams (or devices) get different buffers. A buffer is replaced only after its stream has
+// drained, since queued work may still read the old one.
 struct Scratch {
     std::shared_ptr<void> buf;
     std::size_t bytes = 0;
-    void* get(std::size_t need) {
-        if (need == 0) return nullptr;
-        if (need > bytes) {
-            void* p = nullptr;
-            throw_if_error(pt_b200_malloc(&p, need));
-            buf = std::shared_ptr<void>(p, [](void* q) { pt_b200_free(q); });
-            bytes = need;
-        }
-        return buf.get();
-    }
 };
-thread_local Scratch t_scratch;
+
+void* scratch(void* stream, std::size_t need) {
+    if (need == 0) return nullptr;
+    static std::mutex mu;
+    static std::map<std::pair<int, void*>, Scratch> pool;
+    int dev = 0;
+    throw_if_error(pt_b200_get_device(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    Scratch& s = pool[{dev, stream}];
+    if (need > s.bytes) {
+        if (s.buf) throw_if_error(pt_b200_stream_sync(stream));
+        s.buf.reset();
+        void* p = nullptr;
+        throw_if_error(pt_b200_malloc(&p, need));
+        s.buf = std::shared_ptr<void>(p, [](void* q) { pt_b200_free(q); });
+        s.bytes = need;
+    }
+    return s.buf.get();
+}
 
 std::size_t ws_bytes(const ConvGeometry& g, int op, Math m) {
     const pt_conv_geom a = g.abi();
@@ -62,7 +73,7 @@ DeviceTensor conv_forward(const ConvGeometry& g, const DeviceTensor& x, const De
     const pt_conv_geom a = g.abi();
     const std::size_t n = ws_bytes(g, PT_CONV_FWD, math);
     throw_if_error(pt_b200_conv_fwd(&a, x.data(), w.data(), b ? b->data() : nullptr, y.data(),
-                                    static_cast<int>(math), t_scratch.get(n), n, stream));
+                                    static_cast<int>(math), scratch(stream, n), n, stream));
     return y;
 }
 
@@ -75,7 +86,7 @@ DeviceTensor conv_backward_input(const ConvGeometry& g, const DeviceTensor& gy, 
     const pt_conv_geom a = g.abi();
     const std::size_t n = ws_bytes(g, PT_CONV_BWD_DATA, math);
     throw_if_error(pt_b200_conv_bwd_data(&a, gy.data(), w.data(), gx.data(), static_cast<int>(math),
-                                         t_scratch.get(n), n, stream));
+                                         scratch(stream, n), n, stream));
     return gx;
 }
 
@@ -92,7 +103,7 @@ void conv_backward_weight(const ConvGeometry& g, const DeviceTensor& x, const De
     const std::size_t n = ws_bytes(g, PT_CONV_BWD_FILTER, math);
     throw_if_error(pt_b200_conv_bwd_filter(&a, x.data(), gy.data(), gw.data(), gb ? gb->data() : nullptr,
                                            scale, accumulate ? 1 : 0, static_cast<int>(math),
-                                           t_scratch.get(n), n, stream));
+                                           scratch(stream, n), n, stream));
 }
 
 // ---- host-Tensor SPEC ops ----
@@ -270,7 +281,7 @@ const DeviceTensor& SpatialConvolutionMM::updateOutput(const DeviceTensor& input
     output = DeviceTensor::empty({g.batch, g.outChannels, g.outHeight(), g.outWidth()});
     const std::size_t n = ws_bytes(g, PT_CONV_FWD, math);
     throw_if_error(pt_b200_conv_fwd_finput(&a, input.data(), weight.data(), bias.data(), output.data(),
-                                           static_cast<int>(math), t_scratch.get(n), n, finput.data(),
+                                           static_cast<int>(math), scratch(nullptr, n), n, finput.data(),
                                            nullptr));
     finputFor_ = input.data();
     return output;
@@ -297,7 +308,7 @@ const DeviceTensor& SpatialConvolutionMM::backward(const DeviceTensor& input, co
     const float* fin = finputFor_ == input.data() ? finput.data() : nullptr;
     throw_if_error(pt_b200_conv_bwd_finput(&a, input.data(), gradOutput.data(), weight.data(),
                                            gradInput.data(), gradWeight.data(), gradBias.data(), scale, 1,
-                                           static_cast<int>(math), t_scratch.get(n), n, fin, nullptr));
+                                           static_cast<int>(math), scratch(nullptr, n), n, fin, nullptr));
     return gradInput;
 }
 
