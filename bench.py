@@ -9,9 +9,12 @@ per layer (fprop + dgrad + wgrad; bias work excluded).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload convnet|alexnet|...]
   python bench.py --impl reference ...   # the CPU reference path (oracle port), same metric
 
-Multi-GPU (torchrun, one rank per GPU): each rank runs the same per-GPU batch (weak
-scaling, batch-sharded data parallelism) and gradWeight/gradBias are all-reduced with
-NCCL per layer on a communication stream overlapping the next layer's backward.
+Multi-GPU (torchrun, one rank per GPU): strong scaling — the workload's fixed global batch
+is sharded over the ranks (dp.shard_range; e.g. AlexNet 128 -> 16 images per GPU at 8),
+and gradWeight/gradBias are all-reduced with NCCL per layer on a communication stream
+overlapping the next layer's kernels; `value` = the global batch's FLOPs / the max-over-
+ranks step time. The line also carries `alexnet.ms_per_batch` (the metric's second half:
+AlexNet conv stack fwd+bwd per global batch of 128 at this N).
 """
 from __future__ import annotations
 
@@ -83,6 +86,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alexnet", action="store_true",
+                    help="skip the AlexNet ms/batch leg (the metric's second half)")
     ap.add_argument("--no-finput", action="store_true", help="re-lay x out in the weight gradient")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch the step eagerly instead of replaying each layer's CUDA graph")
@@ -266,6 +271,122 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------- GPU arm
+def local_layers(layers, rank, world):
+    """Strong scaling (north_star): the workload's FIXED global batch is
+    sharded over the ranks (dp.shard_range: AlexNet 128 -> 64/32/16 per GPU, VGG-A 64 ->
+    32/16/8); every rank holds the full weights; the gradients are all-reduced."""
+    from paper_1606_04884_b200.dp import shard_range
+    out = []
+    for l in layers:
+        lo, hi = shard_range(l[1], rank, world)
+        out.append((l[0], hi - lo) + tuple(l[2:]))
+    return out
+
+
+class Workload:
+    """One rank's share of a workload: per layer the device buffers, Torch's finput, the
+    gradient bucket, and (after capture()) one CUDA graph of the layer's fwd + bwd."""
+
+    def __init__(self, pt, torch, layers, dev, rank, math, use_finput=True):
+        from paper_1606_04884_b200.dp import GradBucket
+        self.pt, self.torch, self.math, self.dev = pt, torch, math, dev
+        self.layers = layers
+        self.st = []
+        for i, l in enumerate(layers):
+            name, N, C, H, W, K, kH, kW, pH, pW, sH, sW = l
+            g = pt.ConvGeometry(N, C, H, W, K, kH, kW, pH, pW, sH, sW)
+            seed = 0x5EED + 101 * i + 7919 * rank
+            x = pt.fill_uniform(torch.empty(g.input_shape(), device=dev), seed + 1)
+            s = 1.0 / (C * kH * kW) ** 0.5
+            w = pt.fill_uniform(torch.empty(g.weight_shape(), device=dev), seed + 2, -s, s)
+            b = pt.fill_uniform(torch.empty((K,), device=dev), seed + 3, -0.1, 0.1)
+            gy = pt.fill_uniform(torch.empty(g.output_shape(), device=dev), seed + 4)
+            bucket = GradBucket([torch.Size(g.weight_shape()), torch.Size((K,))], dev)
+            fb = pt.finput_bytes(g, math) if use_finput else 0
+            finput = torch.empty(fb, dtype=torch.uint8, device=dev) if fb else None
+            self.st.append(dict(name=name, finput=finput, g=g, x=x, w=w, b=b, gy=gy,
+                                y=torch.empty(g.output_shape(), device=dev),
+                                gx=torch.empty(g.input_shape(), device=dev), bucket=bucket,
+                                gw=bucket.views[0], gb=bucket.views[1]))
+        self.graphs = None
+        self.graph_launches = 0
+
+    def layer(self, s):
+        from paper_1606_04884_b200 import _lib as L
+        pt, g = self.pt, s["g"]
+        L.lib().pt_b200_profile_tag(s["name"].encode())
+        # Torch's finput: the forward's relaid input is reused by accGradParameters
+        pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=self.math, finput=s["finput"])
+        pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=self.math,
+                         finput=s["finput"])
+
+    def step(self, comm=None, eager=False):
+        from paper_1606_04884_b200.dp import allreduce_async
+        cur = self.torch.cuda.current_stream()
+        done = []
+        for i, s in enumerate(self.st):
+            if self.graphs is None or eager:
+                self.layer(s)
+            else:
+                self.graphs[i].replay()
+            # batch-sharded DP: one allreduce(sum) of this layer's gradW||gradB bucket on the
+            # comm stream, overlapping the next layer's kernels
+            done.append(allreduce_async(s["bucket"], comm))
+        for ev in done:
+            if ev is not None:
+                cur.wait_event(ev)
+
+    def capture(self):
+        """Each layer's forward + combined backward (internal streams included) captured
+        once as a CUDA graph on a side stream whose workspace is warmed (allocated) first,
+        so nothing allocates during capture; the allreduce stays an eager NCCL call between
+        the replays, so every N runs the same kernels the same way."""
+        torch, pt = self.torch, self.pt
+        cur = torch.cuda.current_stream()
+        side = torch.cuda.Stream(device=self.dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            for s in self.st:
+                self.layer(s)
+        side.synchronize()
+        graphs = []
+        c0 = pt.launch_count()
+        for s in self.st:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=side, capture_error_mode="thread_local"):
+                self.layer(s)
+            graphs.append(gr)
+        self.graph_launches = pt.launch_count() - c0
+        self.graphs = graphs
+        torch.cuda.synchronize()
+
+    def bytes_working_set(self):
+        return sum(4 * (s["x"].numel() + s["y"].numel() + s["gy"].numel() + s["gx"].numel())
+                   for s in self.st)
+
+
+def timed(torch, dist, world, run, steps):
+    """Device time of `steps` calls of run(): barrier + synchronize on both sides, CUDA
+    events on the current stream, max over ranks."""
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -283,108 +404,40 @@ def main():
 
     import paper_1606_04884_b200 as pt
     from paper_1606_04884_b200 import _lib as L
-    from paper_1606_04884_b200.dp import GradBucket, allreduce_async
 
-    layers = WORKLOADS[args.workload]
+    glayers = WORKLOADS[args.workload]
+    layers = local_layers(glayers, rank, world)
     dev = torch.device("cuda", local)
-    st = []
-    for i, l in enumerate(layers):
-        name, N, C, H, W, K, kH, kW, pH, pW, sH, sW = l
-        g = pt.ConvGeometry(N, C, H, W, K, kH, kW, pH, pW, sH, sW)
-        seed = 0x5EED + 101 * i + 7919 * rank
-        x = pt.fill_uniform(torch.empty(g.input_shape(), device=dev), seed + 1)
-        s = 1.0 / (C * kH * kW) ** 0.5
-        w = pt.fill_uniform(torch.empty(g.weight_shape(), device=dev), seed + 2, -s, s)
-        b = pt.fill_uniform(torch.empty((K,), device=dev), seed + 3, -0.1, 0.1)
-        gy = pt.fill_uniform(torch.empty(g.output_shape(), device=dev), seed + 4)
-        bucket = GradBucket([torch.Size(g.weight_shape()), torch.Size((K,))], dev)
-        fb = 0 if args.no_finput else pt.finput_bytes(g, args.math)
-        finput = torch.empty(fb, dtype=torch.uint8, device=dev) if fb else None
-        st.append(dict(name=name, finput=finput, g=g, x=x, w=w, b=b, gy=gy, y=torch.empty(g.output_shape(), device=dev),
-                       gx=torch.empty(g.input_shape(), device=dev), bucket=bucket,
-                       gw=bucket.views[0], gb=bucket.views[1]))
+    wl = Workload(pt, torch, layers, dev, rank, args.math, use_finput=not args.no_finput)
+    st = wl.st
     comm = torch.cuda.Stream(device=dev) if world > 1 else None
 
-    def layer(s):
-        g = s["g"]
-        L.lib().pt_b200_profile_tag(s["name"].encode())
-        # Torch's finput: the forward's relaid input is reused by accGradParameters
-        pt.conv_forward(g, s["x"], s["w"], s["b"], s["y"], math=args.math, finput=s["finput"])
-        pt.conv_backward(g, s["x"], s["gy"], s["w"], s["gx"], s["gw"], s["gb"], math=args.math,
-                         finput=s["finput"])
-
-    def step(graphs=None):
-        cur = torch.cuda.current_stream()
-        done = []
-        for i, s in enumerate(st):
-            if graphs is None:
-                layer(s)
-            else:
-                graphs[i].replay()
-            # batch-sharded DP: one allreduce(sum) of this layer's gradW||gradB bucket on the
-            # comm stream, overlapping the next layer's kernels
-            done.append(allreduce_async(s["bucket"], comm))
-        for ev in done:
-            if ev is not None:
-                cur.wait_event(ev)
-
     for _ in range(max(3, args.warmup)):
-        step()
+        wl.step(comm)
     torch.cuda.synchronize()
 
     peaks, peak_kind = load_peaks()
     clocks = ClockSampler(local)
     L.lib().pt_b200_profile_enable(0)
     L.lib().pt_b200_set_bwd_streams(1)
-    # Each layer's forward + combined backward (internal streams included) is captured once
-    # as a CUDA graph and replayed, so the GPU never waits on the host's per-launch work
-    # (~0.5 ms of ctypes + tensor-map encoding per step). The gradient allreduce stays an
-    # eager NCCL call between the replays, so N=1 and N>1 run the same kernels the same way.
-    run, graph, graph_launches = step, None, 0
+    graph = None
     if not args.no_graph:
         try:
-            cur = torch.cuda.current_stream()
-            side = torch.cuda.Stream(device=dev)
-            side.wait_stream(cur)
-            with torch.cuda.stream(side):  # the capture stream's workspace, allocated outside
-                for s in st:
-                    layer(s)
-            cur.wait_stream(side)
-            torch.cuda.synchronize()
-            graphs = []
-            c0 = pt.launch_count()
-            for s in st:
-                gr = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(gr, capture_error_mode="thread_local"):
-                    layer(s)
-                graphs.append(gr)
-            graph_launches = pt.launch_count() - c0
+            wl.capture()
             for _ in range(2):
-                step(graphs)
+                wl.step(comm)
             torch.cuda.synchronize()
-            graph = graphs
-            run = lambda: step(graphs)  # noqa: E731
+            graph = wl.graphs
         except Exception as ex:  # pragma: no cover - eager launches instead
             print(f"bench: CUDA-graph capture failed ({ex}); timing eager launches", file=sys.stderr)
             torch.cuda.synchronize()
-            run, graph, graph_launches = step, None, 0
+            wl.graphs = None
     launches0 = pt.launch_count()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        run()
-    e1.record()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ms = timed(torch, dist, world, lambda: wl.step(comm), args.steps)
     clk = clocks.stop()
-    launches = pt.launch_count() - launches0 + graph_launches * args.steps * (graph is not None)
-    ms = e0.elapsed_time(e1)
+    launches = pt.launch_count() - launches0 + wl.graph_launches * args.steps * (graph is not None)
     # per-launch kernel timings: a second pass of the same steps with the backward's two
     # streams serialised — in the timed region the input- and weight-gradient kernels run
     # concurrently, so per-launch event spans there would overlap
@@ -395,18 +448,14 @@ def main():
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record()
     for _ in range(args.steps):
-        step()
+        wl.step(comm, eager=True)
     p1.record()
     torch.cuda.synchronize()
     ms_serial = p0.elapsed_time(p1)
     prof = {c: L.profile_read(c) for c in ("umma_conv", "umma_wgrad", "simt_conv", "layout")}
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
     ms_step = ms / args.steps
-    flops_step = sum(layer_flops(l) for l in layers)
-    value = flops_step * world / (ms_step * 1e-3) / 1e9
+    flops_step = sum(layer_flops(l) for l in glayers)  # the global batch's work
+    value = flops_step / (ms_step * 1e-3) / 1e9
 
     # roofline of the dominant kernel: the (layer, pass) tensor-core launch with the
     # largest device time inside the timed region (CUDA events on its own stream)
@@ -444,6 +493,7 @@ def main():
     roof["avg_launch_ms"] = avg_ms
     roof["flops_per_launch"] = dfl / dn
     roof["share_of_step"] = dms / ms_serial if ms_serial > 0 else None
+    roof["step_frac"] = value / 1e3 / peak_tf
     roof["timing"] = ("per-launch CUDA events in a serialised, eagerly launched pass of the same steps "
                       f"right after the timed region ({ms_serial / args.steps:.3f} ms/step serialised vs "
                       f"{ms / args.steps:.3f} ms/step timed: backward's two streams, "
@@ -458,15 +508,17 @@ def main():
     result = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "tf32" if args.math == "tf32" else "fp32",
         "data": "synthetic (counter-based uniform, device-generated)",
         "config": {"workload": args.workload, "layers": [l[0] for l in layers],
-                   "global_batch": layers[0][1] * world, "per_gpu_batch": layers[0][1],
+                   "global_batch": glayers[0][1], "per_gpu_batch": layers[0][1],
                    "parallelism": f"dp{world}", "math": args.math,
+                   "sharding": "fixed global batch split over the ranks (dp.shard_range); "
+                               "gradWeight||gradBias all-reduced per layer (NCCL)",
                    "launch": "one CUDA-graph replay per layer (fwd + bwd), allreduce eager" if graph is not None else "eager",
                    "l2": "no flush: per-step working set "
-                         f"{sum(4*(s['x'].numel()+s['y'].numel()+s['gy'].numel()+s['gx'].numel()) for s in st)/1e9:.2f} GB > 126 MB L2"},
+                         f"{wl.bytes_working_set() / 1e9:.2f} GB > 126 MB L2"},
         "clocks": clk, "gpu_launches": launches, "roofline": roof,
         "kernels": {c: {"ms": v[0], "launches": v[1], "tflops": (v[2] / (v[0] * 1e-3) / 1e12)
                         if v[0] > 0 and v[2] > 0 else None,
@@ -474,13 +526,21 @@ def main():
                     for c, v in prof.items()},
         "layout_per_pass": lay,
     }
+    del wl, st
+
+    # the metric's second half: AlexNet conv stack ms per (global) batch of 128 at this N
+    if args.workload != "alexnet" and not args.no_alexnet:
+        result["alexnet"] = alexnet_ms_per_batch(args, pt, torch, dist, dev, rank, world)
+    elif args.workload == "alexnet":
+        result["alexnet"] = {"ms_per_batch": ms_step, "global_batch": glayers[0][1],
+                             "per_gpu_batch": layers[0][1], "n_gpus": world}
 
     # e2e through the public API with HOST buffers (pinned), copies inside the timed region
     if not args.no_e2e:
-        result["e2e"] = e2e(args, pt, torch, layers, dev, world, rank, dist)
+        result["e2e"] = e2e(args, pt, torch, layers, glayers, dev, world, rank, dist)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            result["cpu_baseline"] = cpu_baseline(layers, args.cpu_seconds)
+            result["cpu_baseline"] = cpu_baseline(glayers, args.cpu_seconds)
         except Exception as ex:  # pragma: no cover
             result["cpu_baseline"] = {"value": None, "error": str(ex)}
     if rank == 0:
@@ -489,7 +549,27 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e(args, pt, torch, layers, dev, world, rank, dist):
+def alexnet_ms_per_batch(args, pt, torch, dist, dev, rank, world):
+    """AlexNet conv stack fwd+bwd, global batch 128 sharded over the ranks, CUDA-graph
+    replay per layer, allreduce per layer: device ms per global batch (max over ranks)."""
+    glayers = WORKLOADS["alexnet"]
+    layers = local_layers(glayers, rank, world)
+    wl = Workload(pt, torch, layers, dev, rank, args.math)
+    comm = torch.cuda.Stream(device=dev) if world > 1 else None
+    for _ in range(3):
+        wl.step(comm)
+    wl.capture()
+    for _ in range(2):
+        wl.step(comm)
+    steps = max(args.steps, 10)
+    ms = timed(torch, dist, world, lambda: wl.step(comm), steps) / steps
+    flops = sum(layer_flops(l) for l in glayers)
+    return {"ms_per_batch": ms, "global_batch": glayers[0][1], "per_gpu_batch": layers[0][1],
+            "n_gpus": world, "steps": steps, "gflops": flops / (ms * 1e-3) / 1e9,
+            "timing": "CUDA events around `steps` CUDA-graph-replayed steps, max over ranks"}
+
+
+def e2e(args, pt, torch, layers, glayers, dev, world, rank, dist):
     host = []
     for i, l in enumerate(layers):
         name, N, C, H, W, K, kH, kW, pH, pW, sH, sW = l
@@ -578,7 +658,7 @@ def e2e(args, pt, torch, layers, dev, world, rank, dist):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    flops_step = sum(layer_flops(l) for l in layers) * world
+    flops_step = sum(layer_flops(l) for l in glayers)  # global batch (strong scaling)
     return {"value": flops_step / (ms / args.e2e_steps * 1e-3) / 1e9, "unit": "GFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
             "path": "paper_1606_04884_b200.conv_* (C ABI) on pinned host tensors, H2D inputs + "

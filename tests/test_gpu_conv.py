@@ -299,8 +299,11 @@ def test_default_engine_paths(g):
     check_all_tf32(g, (x, w, b, gy), (y, gx, gw, gb))
 
 
-def test_randomised_channel_rich_geometries():
-    """24 random channel-rich geometries (tests/stress_tc.py) through the default engines."""
+@pytest.mark.parametrize("wide", [False, True])
+def test_randomised_geometries(wide):
+    """64 random channel-rich (or odd-channel / strided / rectangular: wide) geometries
+    (tests/stress_tc.py) through the default engines: bitwise on TF32-exact inputs,
+    elementwise TF32 bounds on real-valued ones."""
     import stress_tc
-    worst, bad = stress_tc.run(24, 11)
+    worst, bad = stress_tc.run(64, 11 + wide, wide)
     assert not bad, f"worst {worst:.3e}: {bad[:3]}"

@@ -56,6 +56,7 @@ CONFIGS = {
     "rowdgrad-horizontal": {"PT_B200_ROWDGRAD": "0"},
     "rowconv-epi4": {"PT_B200_ROWCONV_EPI": "4"},
     "serial-bwd": {"PT_B200_BWD_STREAMS": "0"},
+    "fdgrad": {"PT_B200_FDGRAD": "1"},
 }
 
 
@@ -66,7 +67,7 @@ def _extra(cfg):
         return HANKEL_EDGE
     if cfg.startswith("hwgrad"):
         return HWGRAD_EDGE
-    if cfg in ("swgrad-off", "no-rowconv", "rowdgrad-horizontal", "rowconv-epi4"):
+    if cfg in ("swgrad-off", "no-rowconv", "rowdgrad-horizontal", "rowconv-epi4", "fdgrad"):
         return SMALLC_GEOMS
     return []
 
