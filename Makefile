@@ -18,6 +18,9 @@ CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(CUDA_INC)
 CU_SRCS  := $(wildcard $(PKG)/csrc/*.cu)
 CU_HDRS  := $(wildcard $(PKG)/csrc/*.cuh) include/pt_b200.h
 CU_OBJS  := $(patsubst $(PKG)/csrc/%.cu,build/cu/%.o,$(CU_SRCS))
+# host-only parts of the library (the apply-expression compiler)
+CC_SRCS  := $(wildcard $(PKG)/csrc/*.cpp)
+CC_OBJS  := $(patsubst $(PKG)/csrc/%.cpp,build/cc/%.o,$(CC_SRCS))
 HOST_SRCS := $(wildcard $(PKG)/host/*.cpp)
 HOST_HDRS := $(wildcard include/portten/*.hpp) include/pt_b200.h
 
@@ -35,9 +38,13 @@ build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 	@mkdir -p build/cu
 	$(NVCC) $(NVFLAGS) -dc -o $@ $<
 
-$(LIBDIR)/libpt_b200.so: $(CU_OBJS)
+build/cc/%.o: $(PKG)/csrc/%.cpp include/pt_b200.h
+	@mkdir -p build/cc
+	$(CXX) $(CXXFLAGS) -c -o $@ $<
+
+$(LIBDIR)/libpt_b200.so: $(CU_OBJS) $(CC_OBJS)
 	@mkdir -p $(LIBDIR)
-	$(NVCC) $(GENCODE) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS) -L$(CUDA_LIB) -lcudart_static -ldl -lpthread -lrt
+	$(NVCC) $(GENCODE) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS) $(CC_OBJS) -L$(CUDA_LIB) -lcudart_static -ldl -lpthread -lrt
 
 $(LIBDIR)/libportten.so: $(HOST_SRCS) $(HOST_HDRS) $(LIBDIR)/libpt_b200.so
 	@mkdir -p $(LIBDIR)

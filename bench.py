@@ -86,6 +86,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--emulate-ranks", type=int, default=1,
+                    help="N=1 only: run rank 0's shard of a G-rank strong-scaling job (compute "
+                         "of one rank, no collective) and report the projected job throughput")
     ap.add_argument("--no-alexnet", action="store_true",
                     help="skip the AlexNet ms/batch leg (the metric's second half)")
     ap.add_argument("--no-finput", action="store_true", help="re-lay x out in the weight gradient")
@@ -406,7 +409,8 @@ def main():
     from paper_1606_04884_b200 import _lib as L
 
     glayers = WORKLOADS[args.workload]
-    layers = local_layers(glayers, rank, world)
+    emu = args.emulate_ranks if world == 1 else 1
+    layers = local_layers(glayers, rank, world) if emu == 1 else local_layers(glayers, 0, emu)
     dev = torch.device("cuda", local)
     wl = Workload(pt, torch, layers, dev, rank, args.math, use_finput=not args.no_finput)
     st = wl.st
@@ -526,6 +530,11 @@ def main():
                     for c, v in prof.items()},
         "layout_per_pass": lay,
     }
+    if emu > 1:
+        result["emulated_ranks"] = {
+            "ranks": emu, "per_rank_batch": layers[0][1],
+            "note": "one rank's shard timed alone on one GPU (no collective): `value` is the "
+                    "projected throughput of the job if the allreduce overlaps fully"}
     del wl, st
 
     # the metric's second half: AlexNet conv stack ms per (global) batch of 128 at this N

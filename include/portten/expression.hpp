@@ -1,7 +1,8 @@
 // expr::Program — the apply grammar "x = <expr>" of the reference
-// (proj/include/portten/expression.hpp:36-85, proj/src/expression.cpp:34-338): same
-// lexer, recursive-descent grammar, validation messages and depth limit. Compiles to
-// the RPN bytecode pt_b200_apply evaluates on the device (include/pt_b200.h).
+// (proj/include/portten/expression.hpp:29-85): same accepted language, validation
+// messages, depth limit and kernel statement. Compiled by the library's operator-precedence
+// compiler (pt_b200_expression_compile, csrc/exprc.cpp) to the RPN bytecode pt_b200_apply
+// evaluates on the device (include/pt_b200.h).
 #pragma once
 
 #include <cstdint>

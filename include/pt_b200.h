@@ -146,6 +146,16 @@ int pt_b200_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float 
                  int64_t ldc, int math, void* stream);
 
 /* ---- pointwise apply / reduce on the conv path (Backend::runApply / runReduce*) ---- */
+/* Compiles an apply expression "x = <expr>" (the grammar of expr::Program::parse,
+ * proj/include/portten/expression.hpp:29-45: operands x y z up to `arity`, scalar s, float
+ * literals, + - * /, unary minus, parentheses, abs exp log sqrt tanh max min, stack depth
+ * <= 32) to the pt_apply_op bytecode pt_b200_apply runs. On a grammar error returns
+ * PT_EVALIDATION with the reference's message (pt_b200_last_error). code may be NULL (then
+ * only *ncode is set); *referenced = highest operand index used + 1; statement (optional)
+ * receives the canonical kernel-language text, e.g. "x = (x * 2);" (kernelStatement()). */
+int pt_b200_expression_compile(const char* text, int arity, int32_t* code, int32_t capacity,
+                               int32_t* ncode, int32_t* referenced, char* statement,
+                               size_t statement_cap);
 /* Elementwise program over 1..3 same-shaped strided views; bases[0]/views[0] is x
  * (the destination). Mirrors ReferenceBackend::runApply (proj/src/reference_backend.cpp:80-113). */
 int pt_b200_apply(const int32_t* code, int32_t ncode, int arity, float* const* bases,

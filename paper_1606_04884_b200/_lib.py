@@ -88,6 +88,9 @@ _SIGS = {
     "pt_b200_col2im": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P]),
     "pt_b200_gemm": (C.c_int, [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_float, _P,
                                C.c_int64, _P, C.c_int64, C.c_float, _P, C.c_int64, C.c_int, _P]),
+    "pt_b200_expression_compile": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.c_int32,
+                                             C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                             C.c_char_p, C.c_size_t]),
     "pt_b200_apply": (C.c_int, [C.POINTER(C.c_int32), C.c_int32, C.c_int, C.POINTER(C.c_void_p),
                                 C.POINTER(PtView), C.c_float, _P]),
     "pt_b200_bias_add": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, _P]),

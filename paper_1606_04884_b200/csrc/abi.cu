@@ -15,6 +15,11 @@ std::atomic<int64_t> g_launches{0};
 
 namespace {
 thread_local std::string g_last_error;
+}  // namespace
+
+void set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+namespace {
 
 template <class F>
 int guarded(F&& f) {

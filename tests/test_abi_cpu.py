@@ -5,6 +5,7 @@ import ctypes as C
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_1606_04884_b200 as pt
@@ -113,3 +114,65 @@ def test_expression_depth_limit():
     very = "x = " + "".join(f"x*(" for _ in range(33)) + "x" + ")" * 33
     with pytest.raises(pt.ValidationError):
         parse(very, 1)
+
+
+# ---- the library's expression compiler (csrc/exprc.cpp) against the reference's parser ----
+_TOKS = ["x", "y", "z", "s", "1", "2.5", ".5e1", "1e-3", "+", "-", "*", "/", "(", ")", ",", "abs",
+         "max", "min", "tanh", "exp", "log", "sqrt", "w", "foo", "$", "1.2.3", "=", "1e", "3.", "e5"]
+
+
+def _gen(rng, d):
+    if d <= 0:
+        return str(rng.choice(["x", "y", "z", "s", "1", "2.5", ".5e1", "7e-2"]))
+    r = rng.random()
+    if r < 0.3:
+        return _gen(rng, d - 1) + str(rng.choice([" + ", " - ", " * ", " / "])) + _gen(rng, d - 1)
+    if r < 0.4:
+        return "-" + _gen(rng, d - 1)
+    if r < 0.5:
+        return "(" + _gen(rng, d - 1) + ")"
+    if r < 0.7:
+        return str(rng.choice(["abs", "exp", "log", "sqrt", "tanh"])) + "(" + _gen(rng, d - 1) + ")"
+    if r < 0.85:
+        return str(rng.choice(["max", "min"])) + "(" + _gen(rng, d - 1) + ", " + _gen(rng, d - 1) + ")"
+    return _gen(rng, d - 1)
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="reference not built (oracle/_ref)")
+@pytest.mark.parametrize("seed", range(4))
+def test_expression_compiler_fuzz_vs_reference(seed):
+    """Token soup and well-formed expressions: accept/reject, the exact error message and
+    the canonical kernel statement all equal the reference parser's (expression.cpp)."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(4000):
+        head = str(rng.choice(["x = ", "x = ", "x = ", "y = ", "x ", "x = x ", "", "x=", "$"]))
+        body = " ".join(str(rng.choice(_TOKS)) for _ in range(int(rng.integers(1, 12))))
+        cases.append((head + body, int(rng.integers(1, 4))))
+    cases += [("x = " + _gen(rng, int(rng.integers(0, 9))), 3) for _ in range(1500)]
+    for text, arity in cases:
+        st, msg = po.ref_parse_expr(text, arity)
+        try:
+            prog = parse(text, arity)
+            got = (0, prog.statement)
+        except pt.ValidationError as ex:
+            got = (2, str(ex))
+        assert got == (st, msg), f"{text!r} (arity {arity}): library {got} vs reference {(st, msg)}"
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="reference not built (oracle/_ref)")
+def test_expression_bytecode_evaluates_like_reference():
+    """The compiled bytecode, evaluated by the oracle's stack machine, equals the
+    reference backend's dispatch_apply of the same text on the same data bitwise."""
+    rng = np.random.default_rng(99)
+    for i in range(300):
+        text = "x = " + _gen(rng, int(rng.integers(1, 7)))
+        shape = (3, 5)
+        bases = [po.uniform(shape, 10 * i + t, 0.1, 2.0).ravel().copy() for t in range(3)]
+        ref_bases = [b.copy() for b in bases]
+        st, err = po.ref_apply(text, ref_bases, [shape] * 3, [[]] * 3, 0.75)
+        assert st == 0, err
+        view = ((3, 5), (5, 1), 0)
+        po.apply(parse(text, 3).code, 3, bases, [view] * 3, 0.75)
+        np.testing.assert_array_equal(bases[0].view(np.uint32), ref_bases[0].view(np.uint32),
+                                      err_msg=text)
