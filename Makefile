@@ -4,6 +4,8 @@
 #   paper_1606_04884_b200/lib/libportten.so   C++ operator API (include/portten/*.hpp)
 #   tests/cpp/portten_tests                   C++ test driver (host logic; --gpu parity)
 #   oracle/liboracle.so, oracle/_ref/...      TEST-ONLY checkers (oracle/Makefile)
+#   integration/_ref/libportten_refdev.so     TEST-ONLY: the reference's backend layer with
+#                                             the B200 plug-in in its device slot
 NVCC     ?= /usr/local/cuda/bin/nvcc
 CXX      := g++
 PKG      := paper_1606_04884_b200
@@ -30,9 +32,10 @@ all: lib oracle $(if $(HOST_SRCS),host tests)
 lib: $(LIBDIR)/libpt_b200.so
 host: $(LIBDIR)/libportten.so
 tests: tests/cpp/portten_tests
-oracle:
+oracle: lib
 	$(MAKE) -C oracle oracle
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; else echo "oracle: /root/reference absent, keeping prebuilt _ref"; fi
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C integration; else echo "integration: /root/reference absent, keeping prebuilt _ref"; fi
 
 build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 	@mkdir -p build/cu
@@ -58,3 +61,4 @@ tests/cpp/portten_tests: tests/cpp/portten_tests.cpp $(LIBDIR)/libportten.so ora
 clean:
 	rm -rf build $(LIBDIR) tests/cpp/portten_tests
 	$(MAKE) -C oracle clean
+	$(MAKE) -C integration clean

@@ -79,6 +79,45 @@ def ref():
     return _r
 
 
+REFDEV_SO = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration",
+                         "_ref", "libportten_refdev.so")
+_rd = None
+
+
+def refdev_available() -> bool:
+    return os.path.exists(REFDEV_SO)
+
+
+def refdev():
+    """The reference's backend layer with the B200 plug-in in its device slot
+    (integration/Makefile): the same ref_* entry points, run on select_backend("device")."""
+    global _rd
+    if _rd is None:
+        if not refdev_available():
+            raise RuntimeError(f"{REFDEV_SO} not built (needs /root/reference; make -C integration)")
+        _rd = C.CDLL(REFDEV_SO)
+    return _rd
+
+
+def ref_backend_info(lib=None):
+    buf = C.create_string_buffer(1024)
+    st = (lib or ref()).ref_backend_info(buf, len(buf))
+    return st, buf.value.decode()
+
+
+def ref_roundtrip(base, base_shape, view_ops, out_elems, lib=None):
+    ops = _ops_array([(0, o[1], o[2], o[3]) if o[0] == "narrow" else (1, o[1], o[2], 0)
+                      for o in view_ops])
+    sizes = (C.c_int64 * 8)(*base_shape)
+    out = np.empty(out_elems, np.float32)
+    err = C.create_string_buffer(1024)
+    st = (lib or ref()).ref_roundtrip(base.ctypes.data_as(C.POINTER(C.c_float)), sizes,
+                                      len(base_shape), ops, len(view_ops),
+                                      out.ctypes.data_as(C.POINTER(C.c_float)), out_elems, err,
+                                      len(err))
+    return st, out, err.value.decode()
+
+
 def geom(N, C_, H, W, K, kH, kW, padH=0, padW=0, strideH=1, strideW=1) -> Geom:
     return Geom(N, C_, H, W, K, kH, kW, padH, padW, strideH, strideW)
 
@@ -223,7 +262,7 @@ def _ops_array(ops):
     return arr
 
 
-def ref_apply(expr: str, bases, base_shapes, view_ops, scalar: float):
+def ref_apply(expr: str, bases, base_shapes, view_ops, scalar: float, lib=None):
     """bases: float32 arrays (contiguous, modified in place), view_ops per operand:
     list of ("narrow", dim, start, len) / ("select", dim, idx)."""
     arity = len(bases)
@@ -241,29 +280,29 @@ def ref_apply(expr: str, bases, base_shapes, view_ops, scalar: float):
             ops[64 * t + 4 * i:64 * t + 4 * i + 4] = list(enc)
         nops[t] = len(view_ops[t])
     err = C.create_string_buffer(1024)
-    st = ref().ref_apply(expr.encode(), arity, data, sizes, ndim, ops, nops, C.c_float(scalar),
+    st = (lib or ref()).ref_apply(expr.encode(), arity, data, sizes, ndim, ops, nops, C.c_float(scalar),
                          err, len(err))
     return st, err.value.decode()
 
 
-def ref_reduce_all(op, base, base_shape, view_ops):
+def ref_reduce_all(op, base, base_shape, view_ops, lib=None):
     ops = _ops_array([(0, o[1], o[2], o[3]) if o[0] == "narrow" else (1, o[1], o[2], 0)
                       for o in view_ops])
     sizes = (C.c_int64 * 8)(*base_shape)
     out = C.c_float()
     err = C.create_string_buffer(1024)
-    st = ref().ref_reduce_all(op, base.ctypes.data_as(C.POINTER(C.c_float)), sizes,
+    st = (lib or ref()).ref_reduce_all(op, base.ctypes.data_as(C.POINTER(C.c_float)), sizes,
                               len(base_shape), ops, len(view_ops), C.byref(out), err, len(err))
     return st, out.value, err.value.decode()
 
 
-def ref_reduce_dim(op, base, base_shape, view_ops, dim, out_elems):
+def ref_reduce_dim(op, base, base_shape, view_ops, dim, out_elems, lib=None):
     ops = _ops_array([(0, o[1], o[2], o[3]) if o[0] == "narrow" else (1, o[1], o[2], 0)
                       for o in view_ops])
     sizes = (C.c_int64 * 8)(*base_shape)
     out = np.empty(out_elems, np.float32)
     err = C.create_string_buffer(1024)
-    st = ref().ref_reduce_dim(op, base.ctypes.data_as(C.POINTER(C.c_float)), sizes,
+    st = (lib or ref()).ref_reduce_dim(op, base.ctypes.data_as(C.POINTER(C.c_float)), sizes,
                               len(base_shape), ops, len(view_ops), dim,
                               out.ctypes.data_as(C.POINTER(C.c_float)), out_elems, err, len(err))
     return st, out, err.value.decode()

@@ -22,6 +22,13 @@
 
 using namespace portten;
 
+// The backend the dispatch entry points run on: the reference's host interpreter here;
+// integration/Makefile recompiles this file with SHIM_BACKEND=select_backend("device") to
+// drive the reference's dispatch through the B200 plug-in (integration/b200_backend.cpp).
+#ifndef SHIM_BACKEND
+#define SHIM_BACKEND reference_backend()
+#endif
+
 namespace {
 
 struct GeomC {
@@ -144,7 +151,7 @@ int ref_apply(const char* expr, int arity, float** data, const int64_t* sizes /*
             views.push_back(makeView(bases.back(), ops + 64 * t, nops[t]));
         }
         dispatch_apply(expr, std::span<Tensor>(views.data(), views.size()), scalar,
-                       reference_backend());
+                       SHIM_BACKEND);
         for (int t = 0; t < arity; ++t)
             std::memcpy(data[t], bases[t].data(), sizeof(float) * bases[t].numel());
     });
@@ -155,7 +162,7 @@ int ref_reduce_all(int op, const float* data, const int64_t* sizes, int ndim, co
     return guarded(err, cap, [&] {
         Tensor base = makeBase(data, sizes, ndim);
         *out = dispatch_reduce_all(static_cast<ReduceOp>(op), makeView(base, ops, nops),
-                                   reference_backend());
+                                   SHIM_BACKEND);
     });
 }
 
@@ -164,10 +171,36 @@ int ref_reduce_dim(int op, const float* data, const int64_t* sizes, int ndim, co
     return guarded(err, cap, [&] {
         Tensor base = makeBase(data, sizes, ndim);
         Tensor r = dispatch_reduce_dim(static_cast<ReduceOp>(op), makeView(base, ops, nops), dim,
-                                       reference_backend());
+                                       SHIM_BACKEND);
         if (r.numel() > out_cap) throw BackendError("reduce_dim output buffer too small");
         Tensor c = r.contiguous();
         std::memcpy(out, c.data(), sizeof(float) * c.numel());
+    });
+}
+
+// device_upload of a view, then device_download into a fresh contiguous tensor
+// (proj/src/backend.cpp:163-181): the round trip the reference promises is bitwise identity.
+int ref_roundtrip(const float* data, const int64_t* sizes, int ndim, const int64_t* ops, int nops,
+                  float* out, int64_t out_cap, char* err, int cap) {
+    return guarded(err, cap, [&] {
+        Tensor base = makeBase(data, sizes, ndim);
+        Tensor v = makeView(base, ops, nops);
+        Backend& b = SHIM_BACKEND;
+        const DeviceBuffer buf = device_upload(v, b);
+        Tensor back = Tensor::create(v.sizes());
+        device_download(buf, back, b);
+        if (back.numel() > out_cap) throw BackendError("roundtrip output buffer too small");
+        std::memcpy(out, back.data(), sizeof(float) * back.numel());
+    });
+}
+
+// Name / isDevice of the backend SHIM_BACKEND resolves to, and of every backend_enumerate() entry.
+int ref_backend_info(char* out, int cap) {
+    return guarded(out, cap, [&] {
+        std::string s = SHIM_BACKEND.descriptor().name;
+        s += SHIM_BACKEND.descriptor().isDevice ? " device" : " host";
+        for (Backend* b : backend_enumerate()) s += ";" + b->descriptor().name;
+        fail(out, cap, s, 0);
     });
 }
 

@@ -176,3 +176,15 @@ def test_expression_bytecode_evaluates_like_reference():
         po.apply(parse(text, 3).code, 3, bases, [view] * 3, 0.75)
         np.testing.assert_array_equal(bases[0].view(np.uint32), ref_bases[0].view(np.uint32),
                                       err_msg=text)
+
+
+@pytest.mark.skipif(not po.refdev_available(), reason="integration/_ref not built")
+def test_reference_device_slot_loads_without_gpu():
+    """The reference's backend layer with the B200 plug-in in its device slot loads on a
+    host without a GPU: the plug-in probes zero devices (not an error), so the reference's
+    own select_backend("device") raises its own BackendError (backend.cpp:93-96)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by tests/test_gpu_integration.py")
+    st, msg = po.ref_backend_info(po.refdev())
+    assert st == 3 and msg.startswith("no device backend available"), (st, msg)
