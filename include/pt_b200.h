@@ -170,6 +170,21 @@ int pt_b200_reduce_all(int op, const float* base, const pt_view* view, float* ou
 int pt_b200_reduce_dim(int op, const float* base, const pt_view* view, int dim, float* out,
                        void* stream);
 
+/* ---- the other layers of the model-stack bench (ModelSpec layers
+ * conv / pool-max / relu; bench_model :484-492). NCHW float32, device pointers. ---- */
+/* y = max(x, 0) (in place allowed); backward gx = y > 0 ? gy : 0 (Torch threshold). */
+int pt_b200_relu_fwd(const float* x, float* y, int64_t n, void* stream);
+int pt_b200_relu_bwd(const float* y, const float* gy, float* gx, int64_t n, void* stream);
+/* Max pooling, window kH x kW, stride sH x sW, zero-or-more padding (never selected);
+ * oH = (H + 2pH - kH)/sH + 1 (floor, Torch's default). argmax (int32 index into the input
+ * plane, may be NULL in inference) feeds the backward, a deterministic gather that sums the
+ * gradients of every window whose arg-max a pixel is. */
+int pt_b200_maxpool_fwd(const float* x, float* y, int32_t* argmax, int64_t N, int64_t C, int64_t H,
+                        int64_t W, int kH, int kW, int sH, int sW, int pH, int pW, void* stream);
+int pt_b200_maxpool_bwd(const float* gy, const int32_t* argmax, float* gx, int64_t N, int64_t C,
+                        int64_t H, int64_t W, int kH, int kW, int sH, int sW, int pH, int pW,
+                        void* stream);
+
 /* ---- data-parallel helpers (batch sharding) ---- */
 /* Number of kernels this library launched on the calling process (bench gpu_launches). */
 int64_t pt_b200_launch_count(void);

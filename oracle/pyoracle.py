@@ -319,3 +319,43 @@ def ref_geom_validate(g):
     err = C.create_string_buffer(512)
     st = ref().ref_geom_validate(C.byref(g), err, len(err))
     return st, err.value.decode()
+
+
+# ---- the model-stack layers (SPEC.md:470 pool-max / relu; Torch nn.ReLU /
+# nn.SpatialMaxPooling semantics, floor output rule), numpy restatement, TEST-ONLY ----
+def relu_fwd(x):
+    return np.maximum(x, np.float32(0)).astype(np.float32)
+
+
+def relu_bwd(y, gy):
+    return np.where(y > 0, gy, np.float32(0)).astype(np.float32)
+
+
+def maxpool_fwd(x, kH, kW, sH, sW, pH=0, pW=0):
+    """Returns (y, argmax): argmax = h*W + w of the first maximum in row-major window order
+    (padding never selected)."""
+    N, Cc, H, W = x.shape
+    oH, oW = (H + 2 * pH - kH) // sH + 1, (W + 2 * pW - kW) // sW + 1
+    y = np.full((N, Cc, oH, oW), -np.inf, np.float32)
+    arg = np.full((N, Cc, oH, oW), -1, np.int32)
+    for r in range(kH):
+        for s in range(kW):
+            hs = np.arange(oH) * sH - pH + r
+            ws = np.arange(oW) * sW - pW + s
+            vh, vw = (hs >= 0) & (hs < H), (ws >= 0) & (ws < W)
+            v = np.full((N, Cc, oH, oW), -np.inf, np.float32)
+            v[:, :, vh[:, None] & vw[None, :]] = x[:, :, hs[vh]][:, :, :, ws[vw]].reshape(N, Cc, -1)
+            idx = (hs[:, None] * W + ws[None, :]).astype(np.int32)
+            take = (v > y) | ((arg < 0) & (vh[:, None] & vw[None, :]))
+            y = np.where(take, v, y)
+            arg = np.where(take, idx[None, None], arg)
+    return y, arg
+
+
+def maxpool_bwd(gy, arg, in_shape):
+    N, Cc, H, W = in_shape
+    gx = np.zeros((N * Cc, H * W), np.float64)
+    g2, a2 = gy.reshape(N * Cc, -1), arg.reshape(N * Cc, -1)
+    for p in range(N * Cc):
+        np.add.at(gx[p], a2[p], g2[p])
+    return gx.reshape(in_shape).astype(np.float32)

@@ -96,6 +96,12 @@ _SIGS = {
     "pt_b200_bias_add": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, _P]),
     "pt_b200_reduce_all": (C.c_int, [C.c_int, _P, C.POINTER(PtView), _P, _P]),
     "pt_b200_reduce_dim": (C.c_int, [C.c_int, _P, C.POINTER(PtView), C.c_int, _P, _P]),
+    "pt_b200_relu_fwd": (C.c_int, [_P, _P, C.c_int64, _P]),
+    "pt_b200_relu_bwd": (C.c_int, [_P, _P, _P, C.c_int64, _P]),
+    "pt_b200_maxpool_fwd": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int64] +
+                            [C.c_int] * 6 + [_P]),
+    "pt_b200_maxpool_bwd": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int64] +
+                            [C.c_int] * 6 + [_P]),
     "pt_b200_launch_count": (C.c_int64, []),
     "pt_b200_tf32_mma_peak": (C.c_double, []),
     "pt_b200_profile_enable": (C.c_int, [C.c_int]),

@@ -682,6 +682,37 @@ int pt_b200_bias_add(float* y, const float* b, int64_t N, int64_t K, int64_t HW,
     });
 }
 
+int pt_b200_relu_fwd(const float* x, float* y, int64_t n, void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(x && y && n >= 1, "relu: bad arguments");
+        relu_fwd(x, y, n, as_stream(stream));
+    });
+}
+
+int pt_b200_relu_bwd(const float* y, const float* gy, float* gx, int64_t n, void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(y && gy && gx && n >= 1, "relu backward: bad arguments");
+        relu_bwd(y, gy, gx, n, as_stream(stream));
+    });
+}
+
+int pt_b200_maxpool_fwd(const float* x, float* y, int32_t* argmax, int64_t N, int64_t C, int64_t H,
+                        int64_t W, int kH, int kW, int sH, int sW, int pH, int pW, void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(x && y, "maxpool: null tensor");
+        maxpool_fwd(x, y, argmax, N, C, H, W, kH, kW, sH, sW, pH, pW, as_stream(stream));
+    });
+}
+
+int pt_b200_maxpool_bwd(const float* gy, const int32_t* argmax, float* gx, int64_t N, int64_t C,
+                        int64_t H, int64_t W, int kH, int kW, int sH, int sW, int pH, int pW,
+                        void* stream) {
+    return guarded([&] {
+        PTB_REQUIRE(gy && argmax && gx, "maxpool backward: null tensor");
+        maxpool_bwd(gy, argmax, gx, N, C, H, W, kH, kW, sH, sW, pH, pW, as_stream(stream));
+    });
+}
+
 int pt_b200_reduce_all(int op, const float* base, const pt_view* view, float* out_dev, void* stream) {
     return guarded([&] {
         PTB_REQUIRE(op >= 0 && op <= 2, "reduce: unknown op");

@@ -210,6 +210,14 @@ void reduce_all_launch(int op, const float* base, const pt_view& v, float* out, 
 void reduce_dim_launch(int op, const float* base, const pt_view& v, int dim, float* out,
                        cudaStream_t st);
 
+// ---- nnlayers.cu (model-stack bench layers) ----
+void relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st);
+void relu_bwd(const float* y, const float* gy, float* gx, int64_t n, cudaStream_t st);
+void maxpool_fwd(const float* x, float* y, int32_t* arg, int64_t N, int64_t C, int64_t H, int64_t W,
+                 int kH, int kW, int sH, int sW, int pH, int pW, cudaStream_t st);
+void maxpool_bwd(const float* gy, const int32_t* arg, float* gx, int64_t N, int64_t C, int64_t H,
+                 int64_t W, int kH, int kW, int sH, int sW, int pH, int pW, cudaStream_t st);
+
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace ptb
