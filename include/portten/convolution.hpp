@@ -45,6 +45,11 @@ Tensor conv_backward_input(const Tensor& gradOutput, const Tensor& weight, const
 /// Returns gradWeight; gradBias written to *gradBias when non-null.
 Tensor conv_backward_weight(const Tensor& input, const Tensor& gradOutput, const ConvGeometry& g,
                             Tensor* gradBias, Math math = Math::TF32);
+/// Winograd F(2x2,3x3), 3x3 stride-1 geometries only (ValidationError
+/// "unsupported geometry" otherwise); the gradInput variant needs padding <= 2.
+Tensor conv_winograd_2x2_3x3(const Tensor& input, const Tensor& weight, const Tensor* bias,
+                             const ConvGeometry& g);
+Tensor conv_backward_input_winograd(const Tensor& gradOutput, const Tensor& weight, const ConvGeometry& g);
 Tensor im2col(const Tensor& image, const ConvGeometry& g);   // one C x H x W image
 Tensor col2im(const Tensor& columns, const ConvGeometry& g);
 /// SPEC gemm: C <- alpha*op(A)*op(B) + beta*C on 2-D row-major host tensors.

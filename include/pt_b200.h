@@ -132,6 +132,17 @@ int pt_b200_conv_fwd_finput(const pt_conv_geom* g, const float* x, const float* 
 int pt_b200_conv_bwd_finput(const pt_conv_geom* g, const float* x, const float* gy, const float* w,
                             float* gx, float* gw, float* gb, float scale, int accumulate, int math,
                             void* ws, size_t ws_bytes, const float* finput, void* stream);
+/* Winograd F(2x2,3x3) registry entry (conv_winograd_2x2_3x3): 3x3 stride-1
+ * layers only (gradInput: padding <= 2), otherwise PT_EVALIDATION "unsupported geometry".
+ * Weight / input transforms, 16 transform-domain TF32 GEMMs on the tensor cores (channel
+ * sums in the transform domain), output transform + bias. Same argument meaning as
+ * pt_b200_conv_fwd / _bwd_data; scratch from pt_b200_winograd_workspace_bytes(g, op), op =
+ * PT_CONV_FWD or PT_CONV_BWD_DATA ((size_t)-1 for an unsupported geometry). */
+size_t pt_b200_winograd_workspace_bytes(const pt_conv_geom* g, int op);
+int pt_b200_conv_fwd_winograd(const pt_conv_geom* g, const float* x, const float* w, const float* b,
+                              float* y, void* ws, size_t ws_bytes, void* stream);
+int pt_b200_conv_bwd_data_winograd(const pt_conv_geom* g, const float* gy, const float* w, float* gx,
+                                   void* ws, size_t ws_bytes, void* stream);
 /* Standalone unfold of ONE image, bit-exact with proj/templates/im2col.kt.tmpl:9-21. */
 int pt_b200_im2col(const pt_conv_geom* g, const float* img, float* col, void* stream);
 /* Batched unfold: images [n0, n0+count) into (CRS) x (count*oHW). */
@@ -140,7 +151,9 @@ int pt_b200_im2col_batched(const pt_conv_geom* g, const float* x, int64_t n0, in
 /* Scatter-add inverse of im2col for ONE image. img is overwritten. */
 int pt_b200_col2im(const pt_conv_geom* g, const float* col, float* img, void* stream);
 /* SPEC gemm, row-major, device pointers:
- * C <- alpha*op(A)*op(B) + beta*C. */
+ * C <- alpha*op(A)*op(B) + beta*C (beta == 0: C is not read). math = PT_MATH_FP32: CUDA-core
+ * FFMA; PT_MATH_TF32: the tcgen05 tensor-core GEMM, which needs A, B 16-byte aligned with
+ * lda, ldb multiples of 4 (TMA), else PT_EVALIDATION. */
 int pt_b200_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float alpha,
                  const float* A, int64_t lda, const float* B, int64_t ldb, float beta, float* C,
                  int64_t ldc, int math, void* stream);

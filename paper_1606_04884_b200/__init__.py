@@ -7,11 +7,13 @@ from ._lib import (BackendError, LibraryMissing, ValidationError, PT_MATH_FP32, 
 from .conv import (ConvGeometry, conv_backward, conv_backward_input,  # noqa: F401
                    conv_backward_weight,
                    conv_forward, conv_im2col_batched, col2im, im2col, im2col_batched, gemm,
-                   bias_add, fill_uniform, launch_count, device_count, finput_bytes)
+                   bias_add, fill_uniform, launch_count, device_count, finput_bytes,
+                   conv_winograd_2x2_3x3, conv_backward_input_winograd, winograd_supported)
 from .nn import SpatialConvolutionMM  # noqa: F401
 
 __all__ = [
     "ConvGeometry", "SpatialConvolutionMM", "conv_forward", "conv_backward_input",
     "conv_backward_weight", "conv_im2col_batched", "im2col", "im2col_batched", "col2im", "gemm",
-    "bias_add", "fill_uniform", "finput_bytes", "ValidationError", "BackendError", "LibraryMissing", "lib",
+    "bias_add", "fill_uniform", "finput_bytes", "conv_winograd_2x2_3x3",
+    "conv_backward_input_winograd", "winograd_supported", "ValidationError", "BackendError", "LibraryMissing", "lib",
 ]

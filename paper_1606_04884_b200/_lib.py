@@ -82,6 +82,9 @@ _SIGS = {
                                           C.c_size_t, _P, _P]),
     "pt_b200_conv_bwd_finput": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, _P, _P,
                                           C.c_float, C.c_int, C.c_int, _P, C.c_size_t, _P, _P]),
+    "pt_b200_winograd_workspace_bytes": (C.c_size_t, [C.POINTER(PtConvGeom), C.c_int]),
+    "pt_b200_conv_fwd_winograd": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "pt_b200_conv_bwd_data_winograd": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P, _P, C.c_size_t, _P]),
     "pt_b200_im2col": (C.c_int, [C.POINTER(PtConvGeom), _P, _P, _P]),
     "pt_b200_im2col_batched": (C.c_int, [C.POINTER(PtConvGeom), _P, C.c_int64, C.c_int64, _P,
                                          _P]),

@@ -317,3 +317,49 @@ def launch_count() -> int:
 
 def device_count() -> int:
     return int(lib().pt_b200_device_count())
+
+
+# ---- Winograd F(2x2,3x3) registry entry ----
+def winograd_supported(g: ConvGeometry, op: int = _lib.PT_CONV_FWD) -> bool:
+    """3x3 stride-1 geometries (gradInput: padding <= 2)."""
+    gc = g.c()
+    return lib().pt_b200_winograd_workspace_bytes(C.byref(gc), op) != C.c_size_t(-1).value
+
+
+def _wino_ws(g: ConvGeometry, op: int):
+    gc = g.c()
+    n = lib().pt_b200_winograd_workspace_bytes(C.byref(gc), op)
+    if n == C.c_size_t(-1).value:
+        raise ValidationError(lib().pt_b200_last_error().decode())
+    return WORKSPACE.get(n)
+
+
+def conv_winograd_2x2_3x3(g: ConvGeometry, x, w, b=None, y=None):
+    """conv_winograd_2x2_3x3: weight / input transforms, 16 tensor-core
+    GEMMs with the channel sums in the transform domain, output transform + bias. Equals
+    conv_direct within 1e-3 relative (SPEC); ValidationError for unsupported geometries."""
+    gc = g.c()
+    check(lib().pt_b200_conv_validate(C.byref(gc)))
+    ws, wsn = _wino_ws(g, _lib.PT_CONV_FWD)
+    if y is None:
+        y = torch.empty(g.output_shape(), dtype=torch.float32, device=x.device)
+    pb = _dev(b, (g.outChannels,), "bias") if b is not None else None
+    check(lib().pt_b200_conv_fwd_winograd(C.byref(gc), _dev(x, g.input_shape(), "input"),
+                                          _dev(w, g.weight_shape(), "weight"), pb,
+                                          _dev(y, g.output_shape(), "output"), ws or None, wsn,
+                                          _stream()))
+    return y
+
+
+def conv_backward_input_winograd(g: ConvGeometry, gy, w, gx=None):
+    """updateGradInput through the Winograd entry (rotated, channel-swapped filter)."""
+    gc = g.c()
+    check(lib().pt_b200_conv_validate(C.byref(gc)))
+    ws, wsn = _wino_ws(g, _lib.PT_CONV_BWD_DATA)
+    if gx is None:
+        gx = torch.empty(g.input_shape(), dtype=torch.float32, device=gy.device)
+    check(lib().pt_b200_conv_bwd_data_winograd(C.byref(gc), _dev(gy, g.output_shape(), "gradOutput"),
+                                               _dev(w, g.weight_shape(), "weight"),
+                                               _dev(gx, g.input_shape(), "gradInput"), ws or None,
+                                               wsn, _stream()))
+    return gx

@@ -482,6 +482,49 @@ size_t pt_b200_conv_finput_bytes(const pt_conv_geom* gp, int math) {
     return st == PT_OK ? r : 0;
 }
 
+size_t pt_b200_winograd_workspace_bytes(const pt_conv_geom* gp, int op) {
+    size_t r = 0;
+    const int st = guarded([&] {
+        validate_geom(gp);
+        const Geo g(*gp);
+        PTB_REQUIRE(op == PT_CONV_FWD || op == PT_CONV_BWD_DATA, "winograd: op must be FWD or BWD_DATA");
+        PTB_REQUIRE(winograd_applies(g, op), "winograd: unsupported geometry " + geom_str(*gp) +
+                                                 " (3x3 stride 1; padding <= 2 for gradInput)");
+        r = winograd_workspace(g, op);
+    });
+    return st == PT_OK ? r : (size_t)-1;
+}
+
+int pt_b200_conv_fwd_winograd(const pt_conv_geom* gp, const float* x, const float* w, const float* b,
+                              float* y, void* ws, size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_ptr(x, "input");
+        require_ptr(w, "weight");
+        require_ptr(y, "output");
+        const Geo g(*gp);
+        PTB_REQUIRE(winograd_applies(g, PT_CONV_FWD),
+                    "winograd: unsupported geometry " + geom_str(*gp) + " (3x3 stride 1 only)");
+        require_ws(ws_bytes, winograd_workspace(g, PT_CONV_FWD), ws);
+        winograd_fwd(g, x, w, b, y, ws, as_stream(stream));
+    });
+}
+
+int pt_b200_conv_bwd_data_winograd(const pt_conv_geom* gp, const float* gy, const float* w, float* gx,
+                                   void* ws, size_t ws_bytes, void* stream) {
+    return guarded([&] {
+        validate_geom(gp);
+        require_ptr(gy, "gradOutput");
+        require_ptr(w, "weight");
+        require_ptr(gx, "gradInput");
+        const Geo g(*gp);
+        PTB_REQUIRE(winograd_applies(g, PT_CONV_BWD_DATA),
+                    "winograd: unsupported geometry " + geom_str(*gp) + " (3x3 stride 1, padding <= 2)");
+        require_ws(ws_bytes, winograd_workspace(g, PT_CONV_BWD_DATA), ws);
+        winograd_bwd_data(g, gy, w, gx, ws, as_stream(stream));
+    });
+}
+
 int pt_b200_conv_bwd_data(const pt_conv_geom* gp, const float* gy, const float* w, float* gx,
                           int math, void* ws, size_t ws_bytes, void* stream) {
     return guarded([&] {
@@ -641,7 +684,29 @@ int pt_b200_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float 
                     "gemm: leading dimensions smaller than the matrix extent");
         PTB_REQUIRE(A && B && C, "gemm: null matrix");
         PTB_REQUIRE(M < (1ll << 31) / 64 * 64, "gemm: M too large");
-        simt_gemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, as_stream(stream));
+        if (math == PT_MATH_FP32) {
+            simt_gemm(transA, transB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, as_stream(stream));
+            return;
+        }
+        // TF32: the tcgen05 GEMM computes C^T's columns as its rows (D[n][m] with m = C's
+        // column j, n = C's row i): its A operand is op(B) (row j, K-major iff transB), its
+        // B operand is op(A) (row i, K-major iff !transA), D = C with ldd = ldc.
+        UmmaGemm gm{};
+        gm.a = B;
+        gm.b = A;
+        gm.d = C;
+        gm.M = N;
+        gm.N = M;
+        gm.K = K;
+        gm.batch = 1;
+        gm.a_mn = !transB;
+        gm.b_mn = transA != 0;
+        gm.lda = ldb;
+        gm.ldb = lda;
+        gm.ldd = ldc;
+        gm.alpha = alpha;
+        gm.beta = beta;
+        umma_gemm(gm, as_stream(stream));
     });
 }
 

@@ -210,6 +210,26 @@ void reduce_all_launch(int op, const float* base, const pt_view& v, float* out, 
 void reduce_dim_launch(int op, const float* base, const pt_view& v, int dim, float* out,
                        cudaStream_t st);
 
+// ---- umma_gemm.cu: batched tcgen05 TF32 GEMM D[b][n][m] = alpha*sum_k A[b][m][k] B[b][n][k] (+beta*D) ----
+struct UmmaGemm {
+    const float* a;
+    const float* b;
+    float* d;
+    int64_t M, N, K, batch;
+    bool a_mn, b_mn;  // operand stored MN-major (row index contiguous) instead of K-major
+    int64_t lda, ldb, ldd, batch_a, batch_b, batch_d;
+    float alpha, beta;
+};
+bool umma_gemm_supported(const UmmaGemm& g);
+void umma_gemm(const UmmaGemm& g, cudaStream_t st);
+
+// ---- winograd.cu: F(2x2,3x3) registry entry ----
+bool winograd_applies(const Geo& g, int op);  // op: PT_CONV_FWD / PT_CONV_BWD_DATA
+size_t winograd_workspace(const Geo& g, int op);
+void winograd_fwd(const Geo& g, const float* x, const float* w, const float* b, float* y, void* ws,
+                  cudaStream_t st);
+void winograd_bwd_data(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st);
+
 // ---- nnlayers.cu (model-stack bench layers) ----
 void relu_fwd(const float* x, float* y, int64_t n, cudaStream_t st);
 void relu_bwd(const float* y, const float* gy, float* gx, int64_t n, cudaStream_t st);
