@@ -56,62 +56,71 @@ struct PoolGeo {
     int32_t H, W, oH, oW, kH, kW, sH, sW, pH, pW;
 };
 
-// one thread per output element; padding positions never win (-inf); NaN propagates
+// one block-stride loop over (plane, output row) — the only 64-bit division is per row and
+// block-uniform — with the threads along the output row; padding positions never win
+// (-inf); NaN propagates
 __global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
                                    int32_t* __restrict__ arg, const PoolGeo g) {
-    const int64_t total = g.planes * g.oH * g.oW;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int ow = (int)(i % g.oW);
-        const int oh = (int)((i / g.oW) % g.oH);
-        const int64_t plane = i / ((int64_t)g.oW * g.oH);
+    const int64_t rows = g.planes * g.oH;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int64_t plane = row / g.oH;
+        const int oh = (int)(row - plane * g.oH);
         const float* xp = x + plane * g.H * g.W;
-        const int h0 = oh * g.sH - g.pH, w0 = ow * g.sW - g.pW;
-        float best = -INFINITY;
-        int32_t bi = -1;
-        for (int r = 0; r < g.kH; ++r) {
-            const int h = h0 + r;
-            if (h < 0 || h >= g.H) continue;
-            for (int s = 0; s < g.kW; ++s) {
-                const int w = w0 + s;
-                if (w < 0 || w >= g.W) continue;
-                const float v = __ldg(xp + h * g.W + w);
-                if (v > best || bi < 0 || (v != v && best == best)) {
-                    best = v;
-                    bi = h * g.W + w;
+        const int h0 = oh * g.sH - g.pH;
+        const int64_t ob = row * g.oW;
+        for (int ow = threadIdx.x; ow < g.oW; ow += blockDim.x) {
+            const int w0 = ow * g.sW - g.pW;
+            float best = -INFINITY;
+            int32_t bi = -1;
+            for (int r = 0; r < g.kH; ++r) {
+                const int h = h0 + r;
+                if (h < 0 || h >= g.H) continue;
+                for (int s = 0; s < g.kW; ++s) {
+                    const int w = w0 + s;
+                    if (w < 0 || w >= g.W) continue;
+                    const float v = __ldg(xp + h * g.W + w);
+                    if (v > best || bi < 0 || (v != v && best == best)) {
+                        best = v;
+                        bi = h * g.W + w;
+                    }
                 }
             }
+            y[ob + ow] = best;
+            if (arg) arg[ob + ow] = bi;
         }
-        y[i] = best;
-        if (arg) arg[i] = bi;
     }
 }
 
 // gather form: input pixel (h, w) receives gy of every window (oh, ow) covering it whose
-// arg-max is (h, w), summed in ascending (oh, ow) order
+// arg-max is (h, w), summed in ascending (oh, ow) order; (plane, input row) per block step
 __global__ void maxpool_bwd_kernel(const float* __restrict__ gy, const int32_t* __restrict__ arg,
                                    float* __restrict__ gx, const PoolGeo g) {
-    const int64_t total = g.planes * g.H * g.W;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int w = (int)(i % g.W);
-        const int h = (int)((i / g.W) % g.H);
-        const int64_t plane = i / ((int64_t)g.W * g.H);
-        const int32_t me = h * g.W + w;
+    const int64_t rows = g.planes * g.H;
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int64_t plane = row / g.H;
+        const int h = (int)(row - plane * g.H);
         // windows with oh*sH - pH <= h <= oh*sH - pH + kH - 1
         const int oh_lo = max(0, (h + g.pH - g.kH + g.sH) / g.sH);
         const int oh_hi = min(g.oH - 1, (h + g.pH) / g.sH);
-        const int ow_lo = max(0, (w + g.pW - g.kW + g.sW) / g.sW);
-        const int ow_hi = min(g.oW - 1, (w + g.pW) / g.sW);
         const int64_t ob = plane * g.oH * g.oW;
-        float acc = 0.f;
-        for (int oh = oh_lo; oh <= oh_hi; ++oh)
-            for (int ow = ow_lo; ow <= ow_hi; ++ow) {
-                const int64_t o = ob + (int64_t)oh * g.oW + ow;
-                if (__ldg(arg + o) == me) acc += __ldg(gy + o);
-            }
-        gx[i] = acc;
+        for (int w = threadIdx.x; w < g.W; w += blockDim.x) {
+            const int32_t me = h * g.W + w;
+            const int ow_lo = max(0, (w + g.pW - g.kW + g.sW) / g.sW);
+            const int ow_hi = min(g.oW - 1, (w + g.pW) / g.sW);
+            float acc = 0.f;
+            for (int oh = oh_lo; oh <= oh_hi; ++oh)
+                for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+                    const int64_t o = ob + (int64_t)oh * g.oW + ow;
+                    if (__ldg(arg + o) == me) acc += __ldg(gy + o);
+                }
+            gx[row * g.W + w] = acc;
+        }
     }
+}
+
+int row_block(int64_t len) { return len >= 192 ? 256 : (len >= 96 ? 128 : 64); }
+int row_grid(int64_t rows) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(rows, 32 * (int64_t)sm_count()));
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -153,7 +162,7 @@ void maxpool_fwd(const float* x, float* y, int32_t* arg, int64_t N, int64_t C, i
     const PoolGeo g = pool_geo(N, C, H, W, kH, kW, sH, sW, pH, pW);
     const int64_t out = g.planes * g.oH * g.oW;
     ProfScope ps("layout", st, 0.0, 4.0 * (g.planes * H * W + out * (arg ? 2 : 1)));
-    maxpool_fwd_kernel<<<stream_grid(out), 256, 0, st>>>(x, y, arg, g);
+    maxpool_fwd_kernel<<<row_grid(g.planes * g.oH), row_block(g.oW), 0, st>>>(x, y, arg, g);
     after_launch("maxpool_fwd");
 }
 
@@ -162,7 +171,7 @@ void maxpool_bwd(const float* gy, const int32_t* arg, float* gx, int64_t N, int6
     const PoolGeo g = pool_geo(N, C, H, W, kH, kW, sH, sW, pH, pW);
     const int64_t in = g.planes * H * W;
     ProfScope ps("layout", st, 0.0, 4.0 * (in + 2 * g.planes * g.oH * g.oW));
-    maxpool_bwd_kernel<<<stream_grid(in), 256, 0, st>>>(gy, arg, gx, g);
+    maxpool_bwd_kernel<<<row_grid(g.planes * H), row_block(W), 0, st>>>(gy, arg, gx, g);
     after_launch("maxpool_bwd");
 }
 

@@ -333,16 +333,22 @@ def bench_model(spec: ModelSpec, scale: int = 1, batch: int = 1, backward: bool 
 
 def bench_apply(sizes: Sequence[int], reps: int = 5, expression: str = "x = x * s",
                 scalar: float = 1.0001) -> List[dict]:
-    """Per-element bandwidth sweep: one contiguous
-    apply launch per repetition on `size` floats, CUDA events around each launch, the first
-    excluded; bandwidth = size * 4 B * 2 (one read + one write) / mean time. A size whose
-    allocation fails gives a row marked skipped."""
+    """Per-element bandwidth sweep: `reps` back-to-back
+    launches of one contiguous apply on `size` floats through pt_b200_apply, after one
+    excluded warm-up launch (the "compile" iteration: the expression is compiled once, as
+    the reference's kernel cache would), timed with CUDA events; bandwidth = size * 4 B * 2
+    (one read + one write) / mean time per launch. Small sizes measure the launch overhead,
+    large ones HBM (the two regimes of the paper's Fig. 1). A size whose allocation fails
+    gives a row marked skipped."""
     import torch
-    from .backend import dispatch_apply
+    from ._lib import PtView
+    from .expr import parse
     if reps < 3:
         raise ValidationError("bench_apply: repetitions must be >= 3")
-    if list(sizes) != sorted(sizes) or min(sizes) < 1:
+    if not sizes or list(sizes) != sorted(sizes) or min(sizes) < 1:
         raise ValidationError("bench_apply: sizes must be ascending and >= 1")
+    prog = parse(expression, 1)
+    code = (C.c_int32 * len(prog.code))(*prog.code)
     rows = []
     for n in sizes:
         n = int(n)
@@ -352,16 +358,20 @@ def bench_apply(sizes: Sequence[int], reps: int = 5, expression: str = "x = x * 
             rows.append({"size": n, "reps": reps, "mean_time_s": None, "gb_per_s": None,
                          "skipped": True})
             continue
-        ts = []
-        for r in range(reps + 1):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            dispatch_apply(expression, [x], scalar)
-            e1.record()
-            e1.synchronize()
-            if r:
-                ts.append(e0.elapsed_time(e1) * 1e-3)
-        mean = sum(ts) / len(ts)
+        v = (PtView * 3)()
+        v[0].ndim, v[0].sizes[0], v[0].strides[0], v[0].offset = 1, n, 1, 0
+        bases = (C.c_void_p * 3)(x.data_ptr(), None, None)
+        st = torch.cuda.current_stream().cuda_stream
+        launch = lambda: check(lib().pt_b200_apply(code, len(prog.code), 1, bases, v,  # noqa: E731
+                                                   float(scalar), st))
+        launch()  # excluded first iteration
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            launch()
+        e1.record()
+        e1.synchronize()
+        mean = e0.elapsed_time(e1) * 1e-3 / reps
         rows.append({"size": n, "reps": reps, "mean_time_s": mean,
                      "gb_per_s": n * 4 * 2 / mean / 1e9})
         del x

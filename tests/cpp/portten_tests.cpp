@@ -127,9 +127,96 @@ static void test_registry() {
     EXPECT(conv::conv_registry_select(g, host).name == "custom");
     EXPECT(conv::conv_registry_select(g, dev).name == "implicitgemm-sm100a");
     EXPECT(throws<ValidationError>([&] { conv::conv_registry_register(e); }));
+    // the Winograd entry is registered, supports only 3x3 stride 1, and
+    // ranks below the implicit GEMM (measured slower on B200)
+    bool has_wino = false;
+    for (const auto& n : conv::conv_registry_names()) has_wino = has_wino || n == "winograd-sm100a";
+    EXPECT(has_wino);
+    conv::ConvGeometry g5{2, 8, 9, 9, 16, 5, 5, 2, 2, 1, 1};
+    EXPECT(conv::conv_registry_select(g5, dev).name == "implicitgemm-sm100a");
 }
 
 // ---------------------------------------------------------------- GPU
+// TF32-exact integer tensors: x, gy in [-8, 8], w in {-1, 0, 1}, b in [-4, 4]
+static Tensor exact(std::vector<std::int64_t> sizes, uint64_t seed, int a) {
+    Tensor t = seeded(sizes, seed, -a - 0.5f, a + 0.5f);
+    for (std::int64_t i = 0; i < t.numel(); ++i) {
+        const float v = std::nearbyint(t.data()[i]);
+        t.data()[i] = v > a ? a : (v < -a ? -a : v);
+    }
+    return t;
+}
+
+static bool same_bits(const Tensor& a, const std::vector<float>& r) {
+    return static_cast<std::size_t>(a.numel()) == r.size() &&
+           std::memcmp(a.data(), r.data(), sizeof(float) * r.size()) == 0;
+}
+
+// Every layer bench.py times, at its real per-image shape (batch 1), through the C++
+// operator API: the registry's selected entry, the Winograd entry where it applies and the
+// Torch-style SpatialConvolutionMM; TF32-exact inputs -> bitwise equal to the C oracle.
+static void test_gpu_bench_layers_exact() {
+    Backend& be = select_backend("device");
+    struct L { const char* name; conv::ConvGeometry g; };
+    const L layers[] = {
+        {"convnet/L1", {1, 3, 128, 128, 96, 11, 11, 0, 0, 1, 1}}, {"convnet/L2", {1, 64, 64, 64, 128, 9, 9, 0, 0, 1, 1}},
+        {"convnet/L3", {1, 128, 32, 32, 128, 9, 9, 0, 0, 1, 1}}, {"convnet/L4", {1, 128, 16, 16, 128, 7, 7, 0, 0, 1, 1}},
+        {"convnet/L5", {1, 384, 13, 13, 384, 3, 3, 0, 0, 1, 1}},
+        {"alexnet/c1", {1, 3, 224, 224, 64, 11, 11, 2, 2, 4, 4}}, {"alexnet/c2", {1, 64, 27, 27, 192, 5, 5, 2, 2, 1, 1}},
+        {"alexnet/c3", {1, 192, 13, 13, 384, 3, 3, 1, 1, 1, 1}}, {"alexnet/c4", {1, 384, 13, 13, 256, 3, 3, 1, 1, 1, 1}},
+        {"alexnet/c5", {1, 256, 13, 13, 256, 3, 3, 1, 1, 1, 1}},
+        {"overfeat/c1", {1, 3, 231, 231, 96, 11, 11, 0, 0, 4, 4}}, {"overfeat/c2", {1, 96, 24, 24, 256, 5, 5, 0, 0, 1, 1}},
+        {"overfeat/c3", {1, 256, 12, 12, 512, 3, 3, 1, 1, 1, 1}}, {"overfeat/c4", {1, 512, 12, 12, 1024, 3, 3, 1, 1, 1, 1}},
+        {"overfeat/c5", {1, 1024, 12, 12, 1024, 3, 3, 1, 1, 1, 1}},
+        {"vgga/c1", {1, 3, 224, 224, 64, 3, 3, 1, 1, 1, 1}}, {"vgga/c2", {1, 64, 112, 112, 128, 3, 3, 1, 1, 1, 1}},
+        {"vgga/c3", {1, 128, 56, 56, 256, 3, 3, 1, 1, 1, 1}}, {"vgga/c4", {1, 256, 56, 56, 256, 3, 3, 1, 1, 1, 1}},
+        {"vgga/c5", {1, 256, 28, 28, 512, 3, 3, 1, 1, 1, 1}}, {"vgga/c6", {1, 512, 28, 28, 512, 3, 3, 1, 1, 1, 1}},
+        {"vgga/c7", {1, 512, 14, 14, 512, 3, 3, 1, 1, 1, 1}}, {"vgga/c8", {1, 512, 14, 14, 512, 3, 3, 1, 1, 1, 1}},
+    };
+    int checked = 0;
+    for (const auto& l : layers) {
+        const auto& g = l.g;
+        or_geom og{g.batch, g.inChannels, g.inHeight, g.inWidth, g.outChannels, g.kernelH, g.kernelW,
+                   g.padH, g.padW, g.strideH, g.strideW};
+        Tensor x = exact({g.batch, g.inChannels, g.inHeight, g.inWidth}, 11, 8);
+        Tensor w = exact({g.outChannels, g.inChannels, g.kernelH, g.kernelW}, 12, 1);
+        Tensor b = exact({g.outChannels}, 13, 4);
+        Tensor gy = exact({g.batch, g.outChannels, g.outHeight(), g.outWidth()}, 14, 8);
+        std::vector<float> ry(g.batch * g.outChannels * g.outSpatial()), rgx(x.numel()), rgw(w.numel()),
+            rgb(g.outChannels);
+        or_conv_forward(&og, x.data(), w.data(), b.data(), ry.data(), 1, 0);
+        or_conv_backward_input(&og, gy.data(), w.data(), rgx.data(), 0);
+        or_conv_backward_weight(&og, x.data(), gy.data(), rgw.data(), rgb.data(), 1.0f, 0, 0);
+        const auto& impl = conv::conv_registry_select(g, be.descriptor());
+        bool ok = same_bits(impl.run(x, w, &b, g), ry);
+        ok = same_bits(impl.backward_input(gy, w, g), rgx) && ok;
+        Tensor gb;
+        ok = same_bits(impl.backward_weight(x, gy, g, &gb), rgw) && same_bits(gb, rgb) && ok;
+        // Torch-style layer over device tensors: updateOutput (keeps finput) + backward()
+        conv::SpatialConvolutionMM layer((int)g.inChannels, (int)g.outChannels, (int)g.kernelW,
+                                         (int)g.kernelH, (int)g.strideW, (int)g.strideH, (int)g.padW,
+                                         (int)g.padH);
+        layer.weight = DeviceTensor::upload(w);
+        layer.bias = DeviceTensor::upload(b);
+        layer.zeroGradParameters();
+        DeviceTensor dx = DeviceTensor::upload(x), dgy = DeviceTensor::upload(gy);
+        ok = same_bits(layer.updateOutput(dx).download(), ry) && ok;
+        ok = same_bits(layer.backward(dx, dgy).download(), rgx) && ok;
+        ok = same_bits(layer.gradWeight.download(), rgw) && same_bits(layer.gradBias.download(), rgb) && ok;
+        if (g.kernelH == 3 && g.kernelW == 3 && g.strideH == 1 && g.strideW == 1) {
+            ok = same_bits(conv::conv_winograd_2x2_3x3(x, w, &b, g), ry) && ok;
+            ok = same_bits(conv::conv_backward_input_winograd(gy, w, g), rgx) && ok;
+        }
+        if (!ok) std::fprintf(stderr, "FAIL bench layer %s: not bitwise equal to the oracle\n", l.name);
+        EXPECT(ok);
+        ++checked;
+    }
+    EXPECT(checked == 23);
+    // the Winograd entry rejects what it does not support
+    conv::ConvGeometry g5{1, 8, 9, 9, 8, 5, 5, 2, 2, 1, 1};
+    Tensor x5 = seeded({1, 8, 9, 9}, 1), w5 = seeded({8, 8, 5, 5}, 2);
+    EXPECT(throws<ValidationError>([&] { conv::conv_winograd_2x2_3x3(x5, w5, nullptr, g5); }));
+}
 static void test_gpu_conv() {
     Backend& be = select_backend("auto");
     EXPECT(be.descriptor().isDevice && be.descriptor().name.rfind("b200:", 0) == 0);
@@ -228,6 +315,7 @@ int main(int argc, char** argv) {
     if (gpu) {
         test_gpu_conv();
         test_gpu_layer_and_ops();
+        test_gpu_bench_layers_exact();
     }
     std::printf("portten_tests: %d passed, %d failed%s\n", g_pass, g_fail, gpu ? " (gpu)" : "");
     return g_fail ? 1 : 0;
