@@ -230,16 +230,23 @@ void launch_gemm(const GemmParams& p, int grid, size_t smem, cudaStream_t st) {
     PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_gemm_kernel<AMN, BMN>, p));
 }
 
+// TMA strides must be non-zero multiples of 16 bytes: a single matrix (batch 1, or a
+// broadcast operand with batch stride 0 over batch 1) gets its own extent as the stride.
+uint64_t batch_bytes(int64_t batch, int64_t batch_stride, int64_t extent) {
+    const int64_t s = (batch > 1 && batch_stride > 0) ? batch_stride : extent;
+    return (uint64_t)((s * 4 + 15) / 16 * 16);
+}
+
 void encode_operand(CUtensorMap* m, const float* base, bool mn_major, int64_t rows, int64_t K,
                     int64_t ld, int64_t batch, int64_t batch_stride, int box_rows) {
     if (mn_major) {  // element (row, k) at k*ld + row
         const uint64_t dims[3] = {(uint64_t)rows, (uint64_t)K, (uint64_t)batch};
-        const uint64_t strides[2] = {(uint64_t)ld * 4, (uint64_t)std::max<int64_t>(batch_stride, 1) * 4};
+        const uint64_t strides[2] = {(uint64_t)ld * 4, batch_bytes(batch, batch_stride, ld * K)};
         const uint32_t box[3] = {32, 32, 1};
         tmap_tiled(m, base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     } else {         // element (row, k) at row*ld + k
         const uint64_t dims[3] = {(uint64_t)K, (uint64_t)rows, (uint64_t)batch};
-        const uint64_t strides[2] = {(uint64_t)ld * 4, (uint64_t)std::max<int64_t>(batch_stride, 1) * 4};
+        const uint64_t strides[2] = {(uint64_t)ld * 4, batch_bytes(batch, batch_stride, ld * rows)};
         const uint32_t box[3] = {32, (uint32_t)box_rows, 1};
         tmap_tiled(m, base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     }
@@ -254,7 +261,8 @@ bool tma_addressable(const void* p, int64_t ld, int64_t batch_stride) {
 
 bool umma_gemm_supported(const UmmaGemm& g) {
     return tma_addressable(g.a, g.lda, g.batch_a) && tma_addressable(g.b, g.ldb, g.batch_b) &&
-           g.M >= 1 && g.N >= 1 && g.K >= 1 && g.batch >= 1 && g.M < (1ll << 31) &&
+           g.M >= 1 && g.N >= 1 && g.K >= 1 && g.batch >= 1 &&
+           (g.batch == 1 || (g.batch_a > 0 && g.batch_b > 0)) && g.M < (1ll << 31) &&
            g.N < (1ll << 31) && g.K < (1ll << 31);
 }
 
