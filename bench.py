@@ -82,7 +82,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="convnet", choices=list(WORKLOADS))
-    ap.add_argument("--math", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--math", default="tf32", choices=["tf32", "3xtf32", "fp32"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -513,7 +513,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "tf32" if args.math == "tf32" else "fp32",
+        "dtype": args.math,
         "data": "synthetic (counter-based uniform, device-generated)",
         "config": {"workload": args.workload, "layers": [l[0] for l in layers],
                    "global_batch": glayers[0][1], "per_gpu_batch": layers[0][1],

@@ -20,7 +20,8 @@
 
 namespace portten::conv {
 
-enum class Math { TF32 = PT_MATH_TF32, FP32 = PT_MATH_FP32 };
+// TF32 tensor cores / FP32 CUDA-core FFMA / FP32-accurate 3xTF32 split on the tensor cores
+enum class Math { TF32 = PT_MATH_TF32, FP32 = PT_MATH_FP32, TF32x3 = PT_MATH_3XTF32 };
 
 // ---- device-resident ops (NCHW activations, KCRS weights) ----
 DeviceTensor conv_forward(const ConvGeometry& g, const DeviceTensor& x, const DeviceTensor& w,

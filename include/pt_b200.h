@@ -42,7 +42,11 @@ typedef struct pt_conv_geom {
 /* Contraction mode. TF32: tcgen05 tensor cores, operands rounded to TF32
  * (cvt.rna), FP32 accumulate in TMEM. FP32: CUDA-core FFMA implicit GEMM,
  * the tight-tolerance mode (north_star "FP32-FFMA mode for tight checks"). */
-enum pt_math { PT_MATH_TF32 = 0, PT_MATH_FP32 = 1 };
+/* PT_MATH_3XTF32: FP32-accurate on the tensor cores. Each operand is split v = hi + lo
+ * (both TF32) and the three products hi*hi + lo*hi + hi*lo run as one TF32 convolution over
+ * a 3x reduction (SURVEY.md §5 PORTTEN_CONV_MATH=3xtf32; the reference's arithmetic is FP32
+ * SGEMM). Convolutions only; pt_b200_gemm rejects it. */
+enum pt_math { PT_MATH_TF32 = 0, PT_MATH_FP32 = 1, PT_MATH_3XTF32 = 2 };
 
 /* Which conv pass a workspace query is for. */
 enum pt_conv_op { PT_CONV_FWD = 0, PT_CONV_BWD_DATA = 1, PT_CONV_BWD_FILTER = 2, PT_CONV_BWD = 3 };
@@ -201,6 +205,11 @@ int pt_b200_maxpool_bwd(const float* gy, const int32_t* argmax, float* gx, int64
 /* ---- data-parallel helpers (batch sharding) ---- */
 /* Number of kernels this library launched on the calling process (bench gpu_launches). */
 int64_t pt_b200_launch_count(void);
+
+/* Plan cache: TMA descriptors are cached per thread, keyed by every encode argument
+ * (buffer address, extents, strides, box, swizzle), so re-running a layer on the same
+ * buffers skips the driver encodes. Counts since process start (either may be null). */
+void pt_b200_plan_cache_stats(int64_t* hits, int64_t* encodes);
 
 /* Measured TF32 tensor-pipe ceiling (TFLOP/s) of the current device at its current
  * clocks: back-to-back M=256 N=256 K=8 kind::tf32 MMAs from shared memory on every SM

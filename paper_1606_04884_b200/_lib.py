@@ -15,7 +15,7 @@ LIBDIR = os.path.join(_HERE, "lib")
 LIBPATH = os.path.join(LIBDIR, "libpt_b200.so")
 
 PT_OK, PT_EVALIDATION, PT_EBACKEND = 0, 2, 3
-PT_MATH_TF32, PT_MATH_FP32 = 0, 1
+PT_MATH_TF32, PT_MATH_FP32, PT_MATH_3XTF32 = 0, 1, 2
 PT_CONV_FWD, PT_CONV_BWD_DATA, PT_CONV_BWD_FILTER, PT_CONV_BWD = 0, 1, 2, 3
 PT_REDUCE_SUM, PT_REDUCE_MAX, PT_REDUCE_MIN = 0, 1, 2
 
@@ -106,6 +106,7 @@ _SIGS = {
     "pt_b200_maxpool_bwd": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.c_int64] +
                             [C.c_int] * 6 + [_P]),
     "pt_b200_launch_count": (C.c_int64, []),
+    "pt_b200_plan_cache_stats": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "pt_b200_tf32_mma_peak": (C.c_double, []),
     "pt_b200_profile_enable": (C.c_int, [C.c_int]),
     "pt_b200_set_bwd_streams": (C.c_int, [C.c_int]),

@@ -15,9 +15,9 @@ from typing import Optional, Tuple
 import torch
 
 from . import _lib
-from ._lib import PT_MATH_FP32, PT_MATH_TF32, ValidationError, check, lib
+from ._lib import PT_MATH_3XTF32, PT_MATH_FP32, PT_MATH_TF32, ValidationError, check, lib
 
-MATH = {"tf32": PT_MATH_TF32, "fp32": PT_MATH_FP32}
+MATH = {"tf32": PT_MATH_TF32, "fp32": PT_MATH_FP32, "3xtf32": PT_MATH_3XTF32}
 
 
 @dataclass(frozen=True)
@@ -98,7 +98,7 @@ def _math(math) -> int:
     try:
         return MATH[math]
     except KeyError:
-        raise ValidationError(f"unknown math mode {math!r} (tf32|fp32)") from None
+        raise ValidationError(f"unknown math mode {math!r} (tf32|fp32|3xtf32)") from None
 
 
 def _dev(t: torch.Tensor, shape, what: str) -> int:
@@ -313,6 +313,13 @@ def fill_uniform(t, seed: int, lo: float = -1.0, hi: float = 1.0):
 
 def launch_count() -> int:
     return int(lib().pt_b200_launch_count())
+
+
+def plan_cache_stats():
+    """(hits, encodes) of the library's TMA-descriptor cache since process start."""
+    h, e = C.c_int64(0), C.c_int64(0)
+    lib().pt_b200_plan_cache_stats(C.byref(h), C.byref(e))
+    return int(h.value), int(e.value)
 
 
 def device_count() -> int:

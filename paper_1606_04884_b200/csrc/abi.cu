@@ -8,6 +8,7 @@
 #include <string>
 
 #include "kernels.cuh"
+#include "tmap.cuh"
 
 namespace ptb {
 
@@ -45,7 +46,7 @@ std::string geom_str(const pt_conv_geom& g) {
 }
 
 void require_math(int math) {
-    PTB_REQUIRE(math == PT_MATH_TF32 || math == PT_MATH_FP32,
+    PTB_REQUIRE(math == PT_MATH_TF32 || math == PT_MATH_FP32 || math == PT_MATH_3XTF32,
                 "conv: unknown math mode " + std::to_string(math));
 }
 
@@ -327,6 +328,149 @@ int sm_count() {
     return n;
 }
 
+
+void fwd_top(const Geo& g, const float* x, const float* w, const float* b, float* y, int math, void* ws,
+             cudaStream_t st, float* finput);
+void bwd_data_top(const Geo& g, const float* gy, const float* w, float* gx, int math, void* ws, cudaStream_t st);
+void bwd_filter_top(const Geo& g, const float* x, const float* gy, float* gw, float* gb, float scale,
+                    int accumulate, int math, void* ws, cudaStream_t st);
+
+// Top-level bodies of the conv entry points (space-to-depth wrapper, then the engines).
+void fwd_top(const Geo& g, const float* x, const float* w, const float* b, float* y, int math, void* ws,
+             cudaStream_t st, float* finput) {
+    {
+        if (s2d_on(g, math)) {
+            const Geo e = s2d_geo(g);
+            char* base = reinterpret_cast<char*>(ws);
+            float* xs = reinterpret_cast<float*>(base);
+            float* wsd = reinterpret_cast<float*>(base + s2d_x_bytes(g));
+            char* inner = base + s2d_x_bytes(g) + s2d_w_bytes(g);
+            if (const int64_t cp = s2d_fwd_cp(g, math)) {
+                // x' straight into the engine's NHWC layout (into finput when shareable)
+                float* xh = finput && finput_layout(g, math) ? finput : xs;
+                s2d_input_nhwc(g, x, xh, cp, st);
+                s2d_weight(g, w, wsd, st);
+                umma_conv_fwd(e, umma_plan(e, false), nullptr, wsd, b, y, inner, st, xh, true);
+                return;
+            }
+            s2d_input(g, x, xs, st);
+            s2d_weight(g, w, wsd, st);
+            fwd_core(e, xs, wsd, b, y, math, inner, st);
+            return;
+        }
+        fwd_core(g, x, w, b, y, math, ws, st, finput);
+    }
+}
+
+void bwd_data_top(const Geo& g, const float* gy, const float* w, float* gx, int math, void* ws, cudaStream_t st) {
+    if (s2d_on(g, math)) {
+        const Geo e = s2d_geo(g);
+        char* base = reinterpret_cast<char*>(ws);
+        float* wsd = reinterpret_cast<float*>(base);
+        float* gxs = reinterpret_cast<float*>(base + s2d_w_bytes(g));
+        s2d_weight(g, w, wsd, st);
+        bwd_data_impl(e, gy, wsd, gxs, math, base + s2d_w_bytes(g) + s2d_x_bytes(g), st);
+        d2s_grad(g, gxs, gx, st);
+        return;
+    }
+    bwd_data_impl(g, gy, w, gx, math, ws, st);
+}
+
+void bwd_filter_top(const Geo& g, const float* x, const float* gy, float* gw, float* gb, float scale,
+                    int accumulate, int math, void* ws, cudaStream_t st) {
+    if (s2d_on(g, math)) {
+        const Geo e = s2d_geo(g);
+        char* base = reinterpret_cast<char*>(ws);
+        float* xs = reinterpret_cast<float*>(base);
+        float* gws = reinterpret_cast<float*>(base + s2d_x_bytes(g));
+        const int64_t cp = finput_layout(g, math) ? s2d_fwd_cp(g, math) : 0;
+        if (cp) s2d_input_nhwc(g, x, xs, cp, st);
+        else s2d_input(g, x, xs, st);
+        bwd_filter_impl(e, xs, gy, gws, gb, 1.f, 0, math, base + s2d_x_bytes(g) + s2d_w_bytes(g), st,
+                        scale, accumulate, cp ? xs : nullptr);
+        d2s_weight_grad(g, gws, gw, scale, accumulate, st);
+        return;
+    }
+    bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st, scale,
+                    accumulate);
+}
+
+// ---- 3xTF32 (split3.cu): the TF32 engines over a 3x reduction ----
+namespace {
+constexpr int kHiLoHi = 2, kHiHiLo = 4;  // split3 patterns (bit b set: block b holds lo)
+enum Axis { kAxisC, kAxisK, kAxisN };
+Geo scaled3(const Geo& g, Axis a) {
+    pt_conv_geom e{g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.pH, g.pW, g.sH, g.sW};
+    if (a == kAxisC) e.C *= 3;
+    if (a == kAxisK) e.K *= 3;
+    if (a == kAxisN) e.N *= 3;
+    validate_geom(&e);
+    return Geo(e);
+}
+size_t fbytes(int64_t n) { return align_up((size_t)n * 4, 256); }
+// [x3 | w3 | inner(C' = 3C)]
+size_t fwd_3x_ws(const Geo& g) {
+    return fbytes(3 * g.N * g.C * g.HW) + fbytes(3 * g.K * g.CRS) + fwd_ws_top(scaled3(g, kAxisC), PT_MATH_TF32);
+}
+// [gy3 | w3 | inner(K' = 3K)]
+size_t bwd_data_3x_ws(const Geo& g) {
+    return fbytes(3 * g.M * g.K) + fbytes(3 * g.K * g.CRS) + bwd_data_ws_top(scaled3(g, kAxisK), PT_MATH_TF32);
+}
+// [x3 | gy3 | gradBias scratch | inner(N' = 3N)]
+size_t bwd_filter_3x_ws(const Geo& g) {
+    return fbytes(3 * g.N * g.C * g.HW) + fbytes(3 * g.M * g.K) + align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256) +
+           bwd_filter_ws_top(scaled3(g, kAxisN), PT_MATH_TF32);
+}
+}  // namespace
+
+size_t ws_3x(const Geo& g, int op) {
+    switch (op) {
+        case PT_CONV_FWD: return fwd_3x_ws(g);
+        case PT_CONV_BWD_DATA: return bwd_data_3x_ws(g);
+        case PT_CONV_BWD_FILTER: return bwd_filter_3x_ws(g);
+        default: return std::max(bwd_data_3x_ws(g), bwd_filter_3x_ws(g));
+    }
+}
+
+// y = conv([x_hi | x_lo | x_hi], [w_hi | w_hi | w_lo]) + b over 3C input channels
+void fwd_3x(const Geo& g, const float* x, const float* w, const float* b, float* y, char* ws, cudaStream_t st) {
+    const Geo e = scaled3(g, kAxisC);
+    float* x3 = reinterpret_cast<float*>(ws);
+    float* w3 = reinterpret_cast<float*>(ws + fbytes(3 * g.N * g.C * g.HW));
+    char* inner = ws + fbytes(3 * g.N * g.C * g.HW) + fbytes(3 * g.K * g.CRS);
+    split3(x, x3, g.N, g.C * g.HW, kHiLoHi, st);
+    split3(w, w3, g.K, g.CRS, kHiHiLo, st);
+    fwd_top(e, x3, w3, b, y, PT_MATH_TF32, inner, st, nullptr);
+}
+
+// gx = tconv([gy_hi | gy_lo | gy_hi], [w_hi ; w_hi ; w_lo]) over 3K gradient channels
+void bwd_data_3x(const Geo& g, const float* gy, const float* w, float* gx, char* ws, cudaStream_t st) {
+    const Geo e = scaled3(g, kAxisK);
+    float* gy3 = reinterpret_cast<float*>(ws);
+    float* w3 = reinterpret_cast<float*>(ws + fbytes(3 * g.M * g.K));
+    char* inner = ws + fbytes(3 * g.M * g.K) + fbytes(3 * g.K * g.CRS);
+    split3(gy, gy3, g.N, g.K * g.oHW, kHiLoHi, st);
+    split3(w, w3, 1, g.K * g.CRS, kHiHiLo, st);
+    bwd_data_top(e, gy3, w3, gx, PT_MATH_TF32, inner, st);
+}
+
+// gw (+)= scale * wgrad([x_hi ; x_hi ; x_lo], [gy_hi ; gy_lo ; gy_hi]) over 3N images;
+// gradBias from gy itself (fixed-order FP32 reduction)
+void bwd_filter_3x(const Geo& g, const float* x, const float* gy, float* gw, float* gb, float scale, int accumulate,
+                   char* ws, cudaStream_t st) {
+    const Geo e = scaled3(g, kAxisN);
+    const size_t xb = fbytes(3 * g.N * g.C * g.HW), gb3 = fbytes(3 * g.M * g.K);
+    const size_t bb = align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256);
+    float* x3 = reinterpret_cast<float*>(ws);
+    float* gy3 = reinterpret_cast<float*>(ws + xb);
+    float* bws = reinterpret_cast<float*>(ws + xb + gb3);
+    char* inner = ws + xb + gb3 + bb;
+    split3(x, x3, 1, g.N * g.C * g.HW, kHiHiLo, st);
+    split3(gy, gy3, 1, g.M * g.K, kHiLoHi, st);
+    bwd_filter_top(e, x3, gy3, gw, nullptr, scale, accumulate, PT_MATH_TF32, inner, st);
+    if (gb) bias_grad(gy, gb, g.N, g.K, g.oHW, scale, accumulate, bws, bb, st);
+}
+
 }  // namespace ptb
 
 using namespace ptb;
@@ -416,12 +560,16 @@ size_t pt_b200_conv_workspace_bytes(const pt_conv_geom* gp, int op, int math) {
         validate_geom(gp);
         require_math(math);
         const Geo g(*gp);
+        if (op < PT_CONV_FWD || op > PT_CONV_BWD) fail_validation("workspace: unknown conv op " + std::to_string(op));
+        if (math == PT_MATH_3XTF32) {
+            r = ws_3x(g, op);
+            return;
+        }
         switch (op) {
             case PT_CONV_FWD: r = fwd_ws_top(g, math); break;
             case PT_CONV_BWD_DATA: r = bwd_data_ws_top(g, math); break;
             case PT_CONV_BWD_FILTER: r = bwd_filter_ws_top(g, math); break;
-            case PT_CONV_BWD: r = bwd_ws_top(g, math); break;
-            default: fail_validation("workspace: unknown conv op " + std::to_string(op));
+            default: r = bwd_ws_top(g, math); break;
         }
     });
     return st == PT_OK ? r : (size_t)-1;
@@ -438,29 +586,16 @@ static int conv_fwd_entry(const pt_conv_geom* gp, const float* x, const float* w
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
         PassScope pass("fwd");
-        require_ws(ws_bytes, fwd_ws_top(g, math), ws);
-        if (s2d_on(g, math)) {
-            const Geo e = s2d_geo(g);
-            char* base = reinterpret_cast<char*>(ws);
-            float* xs = reinterpret_cast<float*>(base);
-            float* wsd = reinterpret_cast<float*>(base + s2d_x_bytes(g));
-            char* inner = base + s2d_x_bytes(g) + s2d_w_bytes(g);
-            if (const int64_t cp = s2d_fwd_cp(g, math)) {
-                // x' straight into the engine's NHWC layout (into finput when shareable)
-                float* xh = finput && finput_layout(g, math) ? finput : xs;
-                s2d_input_nhwc(g, x, xh, cp, st);
-                s2d_weight(g, w, wsd, st);
-                umma_conv_fwd(e, umma_plan(e, false), nullptr, wsd, b, y, inner, st, xh, true);
-                return;
-            }
-            s2d_input(g, x, xs, st);
-            s2d_weight(g, w, wsd, st);
-            fwd_core(e, xs, wsd, b, y, math, inner, st);
+        if (math == PT_MATH_3XTF32) {
+            require_ws(ws_bytes, ws_3x(g, PT_CONV_FWD), ws);
+            fwd_3x(g, x, w, b, y, reinterpret_cast<char*>(ws), st);
             return;
         }
-        fwd_core(g, x, w, b, y, math, ws, st, finput);
+        require_ws(ws_bytes, fwd_ws_top(g, math), ws);
+        fwd_top(g, x, w, b, y, math, ws, st, finput);
     });
 }
+
 
 int pt_b200_conv_fwd(const pt_conv_geom* gp, const float* x, const float* w, const float* b,
                      float* y, int math, void* ws, size_t ws_bytes, void* stream) {
@@ -535,20 +670,16 @@ int pt_b200_conv_bwd_data(const pt_conv_geom* gp, const float* gy, const float* 
         require_ptr(gx, "gradInput");
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
-        require_ws(ws_bytes, bwd_data_ws_top(g, math), ws);
-        if (s2d_on(g, math)) {
-            const Geo e = s2d_geo(g);
-            char* base = reinterpret_cast<char*>(ws);
-            float* wsd = reinterpret_cast<float*>(base);
-            float* gxs = reinterpret_cast<float*>(base + s2d_w_bytes(g));
-            s2d_weight(g, w, wsd, st);
-            bwd_data_impl(e, gy, wsd, gxs, math, base + s2d_w_bytes(g) + s2d_x_bytes(g), st);
-            d2s_grad(g, gxs, gx, st);
+        if (math == PT_MATH_3XTF32) {
+            require_ws(ws_bytes, ws_3x(g, PT_CONV_BWD_DATA), ws);
+            bwd_data_3x(g, gy, w, gx, reinterpret_cast<char*>(ws), st);
             return;
         }
-        bwd_data_impl(g, gy, w, gx, math, ws, st);
+        require_ws(ws_bytes, bwd_data_ws_top(g, math), ws);
+        bwd_data_top(g, gy, w, gx, math, ws, st);
     });
 }
+
 
 int pt_b200_conv_bwd_filter(const pt_conv_geom* gp, const float* x, const float* gy, float* gw,
                             float* gb, float scale, int accumulate, int math, void* ws,
@@ -561,24 +692,16 @@ int pt_b200_conv_bwd_filter(const pt_conv_geom* gp, const float* x, const float*
         require_ptr(gw, "gradWeight");
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
-        require_ws(ws_bytes, bwd_filter_ws_top(g, math), ws);
-        if (s2d_on(g, math)) {
-            const Geo e = s2d_geo(g);
-            char* base = reinterpret_cast<char*>(ws);
-            float* xs = reinterpret_cast<float*>(base);
-            float* gws = reinterpret_cast<float*>(base + s2d_x_bytes(g));
-            const int64_t cp = finput_layout(g, math) ? s2d_fwd_cp(g, math) : 0;
-            if (cp) s2d_input_nhwc(g, x, xs, cp, st);
-            else s2d_input(g, x, xs, st);
-            bwd_filter_impl(e, xs, gy, gws, gb, 1.f, 0, math, base + s2d_x_bytes(g) + s2d_w_bytes(g), st,
-                            scale, accumulate, cp ? xs : nullptr);
-            d2s_weight_grad(g, gws, gw, scale, accumulate, st);
+        if (math == PT_MATH_3XTF32) {
+            require_ws(ws_bytes, ws_3x(g, PT_CONV_BWD_FILTER), ws);
+            bwd_filter_3x(g, x, gy, gw, gb, scale, accumulate, reinterpret_cast<char*>(ws), st);
             return;
         }
-        bwd_filter_impl(g, x, gy, gw, gb, scale, accumulate, math, reinterpret_cast<char*>(ws), st, scale,
-                        accumulate);
+        require_ws(ws_bytes, bwd_filter_ws_top(g, math), ws);
+        bwd_filter_top(g, x, gy, gw, gb, scale, accumulate, math, ws, st);
     });
 }
+
 
 static int conv_bwd_entry(const pt_conv_geom* gp, const float* x, const float* gy, const float* w,
                           float* gx, float* gw, float* gb, float scale, int accumulate, int math,
@@ -592,6 +715,13 @@ static int conv_bwd_entry(const pt_conv_geom* gp, const float* x, const float* g
         if (gw) require_ptr(x, "input");
         const Geo g(*gp);
         cudaStream_t st = as_stream(stream);
+        if (math == PT_MATH_3XTF32) {
+            require_ws(ws_bytes, ws_3x(g, PT_CONV_BWD), ws);
+            // the two products are independent 3x problems; the gradient parts run in turn
+            if (gx) bwd_data_3x(g, gy, w, gx, reinterpret_cast<char*>(ws), st);
+            if (gw) bwd_filter_3x(g, x, gy, gw, gb, scale, accumulate, reinterpret_cast<char*>(ws), st);
+            return;
+        }
         require_ws(ws_bytes, bwd_ws_top(g, math), ws);
         if (s2d_on(g, math)) {
             const Geo e = s2d_geo(g);
@@ -679,6 +809,7 @@ int pt_b200_gemm(int transA, int transB, int64_t M, int64_t N, int64_t K, float 
                  int64_t ldc, int math, void* stream) {
     return guarded([&] {
         require_math(math);
+        PTB_REQUIRE(math != PT_MATH_3XTF32, "gemm: math 3xtf32 is a convolution mode (use tf32 or fp32)");
         PTB_REQUIRE(M >= 1 && N >= 1 && K >= 1, "gemm: dims must be >= 1");
         PTB_REQUIRE(lda >= (transA ? M : K) && ldb >= (transB ? K : N) && ldc >= N,
                     "gemm: leading dimensions smaller than the matrix extent");
@@ -801,5 +932,7 @@ int pt_b200_reduce_dim(int op, const float* base, const pt_view* view, int dim, 
 }
 
 int64_t pt_b200_launch_count(void) { return g_launches.load(); }
+
+void pt_b200_plan_cache_stats(int64_t* hits, int64_t* encodes) { tmap_cache_stats(hits, encodes); }
 
 }  // extern "C"

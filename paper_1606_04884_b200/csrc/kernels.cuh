@@ -68,6 +68,9 @@ void bias_grad(const float* gy, float* gb, int64_t N, int64_t K, int64_t HW, flo
                int accumulate, float* ws, size_t ws_bytes, cudaStream_t st);
 size_t bias_grad_workspace(int64_t N, int64_t K, int64_t HW);
 
+// ---- split3.cu: 3xTF32 operand split, dst[o][b][i] = (pattern bit b ? lo : hi)(src[o][i]) ----
+void split3(const float* src, float* dst, int64_t outer, int64_t blk, int pattern, cudaStream_t st);
+
 // ---- umma_conv.cu: tcgen05 kind::tf32 implicit GEMM (fprop, stride-1 dgrad) ----
 struct UmmaPlan {
     enum Mode { kFprop = 0, kDgradTconv = 1, kDgradGcol = 2 };

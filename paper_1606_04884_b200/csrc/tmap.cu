@@ -2,8 +2,12 @@
 // through the runtime's driver-entry-point query (no link-time libcuda dependency).
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "tmap.cuh"
 
@@ -42,12 +46,68 @@ void load() {
 void small_tensor_fixup(CUtensorMap* m, size_t bytes) {
     if (g_driver_version <= 13010 && bytes < 131072) reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
 }
+
+// ---- descriptor cache ----
+// A tensor map is a pure function of its encode arguments, so repeated calls with the same
+// buffers (a training loop re-running a layer on the same activations / workspace) reuse the
+// encoded descriptor instead of calling into the driver again (the encodes were most of the
+// host time of an eager conv call). Per thread: no locking on the launch path; bounded.
+struct TmapKey {
+    uint64_t w[24];
+    bool operator==(const TmapKey& o) const { return std::memcmp(w, o.w, sizeof w) == 0; }
+};
+struct TmapKeyHash {
+    size_t operator()(const TmapKey& k) const {
+        uint64_t h = 1469598103934665603ull;
+        for (uint64_t v : k.w) h = (h ^ v) * 1099511628211ull;
+        return (size_t)h;
+    }
+};
+std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash>& tmap_cache() {
+    thread_local std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> c;
+    if (c.size() > 4096) c.clear();
+    return c;
+}
+std::atomic<int64_t> g_tmap_hits{0}, g_tmap_encodes{0};
+bool tmap_cache_on() {
+    static const bool on = std::getenv("PT_B200_NO_TMAP_CACHE") == nullptr;
+    return on;
+}
 }  // namespace
+
+void tmap_cache_stats(int64_t* hits, int64_t* encodes) {
+    if (hits) *hits = g_tmap_hits.load();
+    if (encodes) *encodes = g_tmap_encodes.load();
+}
 
 void tmap_im2col(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t W, int64_t Cp,
                  int kH, int kW, int pH, int pW, int sH, int sW, int channels, int pixels,
                  CUtensorMapSwizzle swizzle) {
+    TmapKey key{};
+    const uint64_t a[] = {1, (uint64_t)(uintptr_t)act, (uint64_t)N, (uint64_t)H, (uint64_t)W, (uint64_t)Cp,
+                          (uint64_t)kH, (uint64_t)kW, (uint64_t)pH, (uint64_t)pW, (uint64_t)sH, (uint64_t)sW,
+                          (uint64_t)channels, (uint64_t)pixels, (uint64_t)swizzle};
+    std::memcpy(key.w, a, sizeof a);
+    if (tmap_cache_on()) {
+        auto& c = tmap_cache();
+        auto it = c.find(key);
+        if (it != c.end()) {
+            *m = it->second;
+            g_tmap_hits.fetch_add(1, std::memory_order_relaxed);
+            return;
+        }
+        tmap_im2col_encode(m, act, N, H, W, Cp, kH, kW, pH, pW, sH, sW, channels, pixels, swizzle);
+        c.emplace(key, *m);
+        return;
+    }
+    tmap_im2col_encode(m, act, N, H, W, Cp, kH, kW, pH, pW, sH, sW, channels, pixels, swizzle);
+}
+
+void tmap_im2col_encode(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t W, int64_t Cp,
+                        int kH, int kW, int pH, int pW, int sH, int sW, int channels, int pixels,
+                        CUtensorMapSwizzle swizzle) {
     load();
+    g_tmap_encodes.fetch_add(1, std::memory_order_relaxed);
     cuuint64_t dims[4] = {(cuuint64_t)Cp, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)(Cp * 4), (cuuint64_t)(W * Cp * 4),
                              (cuuint64_t)(H * W * Cp * 4)};
@@ -64,7 +124,34 @@ void tmap_im2col(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t
 
 void tmap_tiled(CUtensorMap* m, const float* base, int rank, const uint64_t* dims,
                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle) {
+    if (tmap_cache_on() && rank >= 1 && rank <= 5) {
+        TmapKey key{};
+        key.w[0] = 2;
+        key.w[1] = (uint64_t)(uintptr_t)base;
+        key.w[2] = (uint64_t)rank | ((uint64_t)swizzle << 8);
+        for (int i = 0; i < rank; ++i) {
+            key.w[3 + i] = dims[i];
+            key.w[8 + i] = box[i];
+            if (i + 1 < rank) key.w[13 + i] = strides_bytes[i];
+        }
+        auto& c = tmap_cache();
+        auto it = c.find(key);
+        if (it != c.end()) {
+            *m = it->second;
+            g_tmap_hits.fetch_add(1, std::memory_order_relaxed);
+            return;
+        }
+        tmap_tiled_encode(m, base, rank, dims, strides_bytes, box, swizzle);
+        c.emplace(key, *m);
+        return;
+    }
+    tmap_tiled_encode(m, base, rank, dims, strides_bytes, box, swizzle);
+}
+
+void tmap_tiled_encode(CUtensorMap* m, const float* base, int rank, const uint64_t* dims,
+                       const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle) {
     load();
+    g_tmap_encodes.fetch_add(1, std::memory_order_relaxed);
     cuuint64_t d[5], s[4];
     cuuint32_t b[5], e[5];
     size_t bytes = 4;

@@ -18,4 +18,13 @@ void tmap_im2col(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t
 void tmap_tiled(CUtensorMap* m, const float* base, int rank, const uint64_t* dims,
                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle);
 
+// The two above go through a per-thread descriptor cache keyed by every encode argument
+// (PT_B200_NO_TMAP_CACHE=1 disables it); the *_encode forms always call the driver.
+void tmap_im2col_encode(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t W, int64_t Cp,
+                        int kH, int kW, int pH, int pW, int sH, int sW, int channels, int pixels,
+                        CUtensorMapSwizzle swizzle);
+void tmap_tiled_encode(CUtensorMap* m, const float* base, int rank, const uint64_t* dims,
+                       const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swizzle);
+void tmap_cache_stats(int64_t* hits, int64_t* encodes);
+
 }  // namespace ptb

@@ -240,6 +240,7 @@ std::vector<ConvImplEntry>& registry() {
             return e;
         };
         v.push_back(mk("implicitgemm-sm100a", 100, Math::TF32));
+        v.push_back(mk("implicitgemm-3xtf32-sm100a", 60, Math::TF32x3));
         v.push_back(mk("implicitgemm-fp32-sm100a", 50, Math::FP32));
         // Winograd F(2x2,3x3): 3x3 stride-1 only; registered BELOW the
         // implicit GEMM because it measures slower on B200 — selected by

@@ -75,7 +75,8 @@ BUNDLED = {
     """,
 }
 
-IMPLS = {"implicitgemm-sm100a": "tf32", "implicitgemm-fp32-sm100a": "fp32"}
+IMPLS = {"implicitgemm-sm100a": "tf32", "implicitgemm-3xtf32-sm100a": "3xtf32",
+         "implicitgemm-fp32-sm100a": "fp32"}
 
 
 @dataclass
