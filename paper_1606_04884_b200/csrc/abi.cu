@@ -63,6 +63,9 @@ void require_view(const pt_view& v, const char* what) {
     PTB_REQUIRE(v.offset >= 0, std::string(what) + ": negative storage offset");
 }
 
+// small-C stride-1 layers: the fused one-read backward (umma_scbwd.cu)
+bool sc_on(const Geo& g, int math) { return math == PT_MATH_TF32 && scbwd_ok(g); }
+
 bool fwd_rowconv(const Geo& g, int math) {
     static const bool off = std::getenv("PT_B200_NO_ROWCONV") != nullptr;  // A/B switch for tests
     return math == PT_MATH_TF32 && !off && rowconv_ok(g);
@@ -81,6 +84,7 @@ bool dgrad_row(const Geo& g, int math) {
     return math == PT_MATH_TF32 && !off && rowdgrad_ok(g);
 }
 size_t bwd_data_ws(const Geo& g, int math) {
+    if (sc_on(g, math)) return scbwd_workspace(g);
     if (dgrad_row(g, math)) return rowdgrad_workspace(g);
     if (math == PT_MATH_TF32) {
         const UmmaPlan pl = umma_plan(g, true);
@@ -93,6 +97,10 @@ size_t bwd_data_ws(const Geo& g, int math) {
 void bwd_data_impl(const Geo& g, const float* gy, const float* w, float* gx, int math, void* ws,
                    cudaStream_t st, const float* gyh_pre = nullptr, bool pre_padded = false) {
     PassScope pass("dgrad");
+    if (sc_on(g, math)) {
+        scbwd(g, nullptr, gy, w, gx, nullptr, nullptr, 1.f, 0, 1.f, 0, ws, st);
+        return;
+    }
     if (dgrad_row(g, math)) {
         rowdgrad(g, gy, w, gx, ws, st, gyh_pre, pre_padded);
         return;
@@ -131,6 +139,7 @@ size_t bias_part_bytes(const Geo& g) { return align_up(nhwc_bias_partials_bytes(
 // TF32 wgrad workspace: [gy NHWC + fused gradBias partials][wgrad kernel scratch]
 // FP32 wgrad workspace: [split-K partials][gradBias partials]
 size_t bwd_filter_ws(const Geo& g, int math) {
+    if (sc_on(g, math)) return scbwd_workspace(g);
     if (wgrad_tc(g, math)) return gyh_bytes(g) + bias_part_bytes(g) + wgrad_tc_ws(g, math);
     return align_up(simt_wgrad_workspace(g), 256) + align_up(bias_grad_workspace(g.N, g.K, g.oHW), 256);
 }
@@ -138,6 +147,7 @@ size_t bwd_filter_ws(const Geo& g, int math) {
 // wgrad and, when its engine reads the same layout, the dgrad.
 bool bwd_shared(const Geo& g, int math) { return wgrad_tc(g, math); }
 size_t bwd_ws(const Geo& g, int math) {
+    if (sc_on(g, math)) return scbwd_workspace(g);
     if (bwd_shared(g, math))
         return gyh_bytes(g) + bias_part_bytes(g) + align_up(bwd_data_ws(g, math), 256) + wgrad_tc_ws(g, math);
     return std::max(bwd_data_ws(g, math), bwd_filter_ws(g, math));
@@ -150,6 +160,10 @@ void bwd_filter_impl(const Geo& g, const float* x, const float* gy, float* gw, f
                      int accumulate, int math, char* ws, cudaStream_t st, float bscale, int bacc,
                      const float* xh_pre = nullptr) {
     PassScope pass("wgrad");
+    if (sc_on(g, math)) {
+        scbwd(g, x, gy, nullptr, nullptr, gw, gb, scale, accumulate, bscale, bacc, ws, st);
+        return;
+    }
     if (wgrad_tc(g, math)) {
         float* gyh = reinterpret_cast<float*>(ws);
         float* part = reinterpret_cast<float*>(ws + gyh_bytes(g));
@@ -269,6 +283,12 @@ void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, flo
     int64_t fph = 0, fpw = 0;
     if (finput && !finput_layout(g, math, &fph, &fpw)) finput = nullptr;
     char* base = ws;
+    if (gx && gw && sc_on(g, math)) {  // one gy read for gradInput, gradWeight and gradBias
+        PassScope pass("bwd");
+        if (inner_gw_plain) scbwd(g, x, gy, w, gx, gw, gb, 1.f, 0, scale, accumulate, ws, st);
+        else scbwd(g, x, gy, w, gx, gw, gb, scale, accumulate, scale, accumulate, ws, st);
+        return;
+    }
     if (gx && gw && bwd_shared(g, math)) {
         // one gy NHWC transform (+ fused gradBias) feeds both tensor-core passes
         float* gyh = reinterpret_cast<float*>(base);

@@ -185,6 +185,15 @@ size_t swgrad_workspace(const Geo& g);
 void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float scale, int accumulate, void* ws,
             cudaStream_t st);
 
+// ---- umma_scbwd.cu: fused backward of small-C stride-1 layers (C*kH*kW <= 32, K <= 64) ----
+// One NCHW gy read feeds gradInput (gcol GEMM + in-smem fold), gradWeight and gradBias;
+// gx / gw may be null (that product skipped); gb only with gw. gw takes (scale, accumulate),
+// gb (bscale, bacc).
+bool scbwd_ok(const Geo& g);
+size_t scbwd_workspace(const Geo& g);
+void scbwd(const Geo& g, const float* x, const float* gy, const float* w, float* gx, float* gw, float* gb,
+           float scale, int accumulate, float bscale, int bacc, void* ws, cudaStream_t st);
+
 // ---- s2d.cu: space-to-depth for strided small-C layers ----
 bool s2d_applies(const Geo& g);
 Geo s2d_geo(const Geo& g);  // the equivalent stride-1 conv over C*s*s channels

@@ -36,6 +36,8 @@ for _ in range(a.iters):
         pt.conv_forward(g, x, w, b, y, math=a.math)
     elif a.which == "dgrad":
         pt.conv_backward_input(g, gy, w, gx, math=a.math)
+    elif a.which == "bwd":
+        pt.conv_backward(g, x, gy, w, gx, gw, gb, math=a.math)
     else:
         pt.conv_backward_weight(g, x, gy, gw, gb, math=a.math)
 torch.cuda.synchronize()

@@ -36,6 +36,9 @@ GEOMS = [
     po.geom(3, 64, 12, 12, 32, 1, 1, 0, 0, 1, 1),        # 1x1
     po.geom(2, 128, 17, 17, 64, 9, 9, 4, 4, 1, 1),       # large zero border (flat tiling)
     po.geom(1, 4, 21, 70, 128, 7, 7, 3, 3, 1, 1),        # C = 4, padded 7x7
+    po.geom(2, 3, 38, 44, 64, 3, 3, 1, 1, 1, 1),         # VGG c1-like, fused small-C backward
+    po.geom(2, 1, 20, 40, 48, 5, 5, 2, 2, 1, 1),         # fused small-C bwd, K = 48 (padded), 5x5
+    po.geom(3, 2, 18, 36, 32, 3, 5, 1, 2, 1, 1),         # fused small-C bwd, rectangular, K = 32
 ]
 
 CONFIGS = {
@@ -57,6 +60,7 @@ CONFIGS = {
     "rowconv-epi4": {"PT_B200_ROWCONV_EPI": "4"},
     "serial-bwd": {"PT_B200_BWD_STREAMS": "0"},
     "fdgrad": {"PT_B200_FDGRAD": "1"},
+    "scbwd-off": {"PT_B200_SCBWD": "0"},
 }
 
 
