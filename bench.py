@@ -466,7 +466,7 @@ def main():
     per = {}
     for s_ in st:
         for cls in ("umma_conv", "umma_wgrad", "simt_conv"):
-            for ps in ("fwd", "dgrad", "wgrad"):
+            for ps in ("fwd", "dgrad", "wgrad", "bwd"):  # bwd: the fused small-C backward
                 v = L.profile_read(f"{cls}@{s_['name']}.{ps}")
                 if v[1] > 0:
                     per[f"{cls}@{s_['name']}.{ps}"] = v
