@@ -101,6 +101,9 @@ struct HConvTiling {
     int64_t P_img = 0;  // positions per image
     int64_t tiles = 0;  // 256-position pair tiles
 };
+// position rows carry only the left zero border (a right-edge tap wraps into the next
+// row's left border); PT_B200_HCONV_WRAP=0: both borders
+bool hconv_wrap();
 HConvTiling hconv_tiling(int64_t N, int64_t Wp, int64_t oH, int64_t cta_span = 128);
 // act: dense NHWC [N][aH][aW][cin_p]; the (aph, apw) zero border comes from TMA
 // out-of-bounds fill. Stride-1 kH x kW conv -> oH x oW NCHW.

@@ -82,11 +82,11 @@ void tmap_cache_stats(int64_t* hits, int64_t* encodes) {
 
 void tmap_im2col(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t W, int64_t Cp,
                  int kH, int kW, int pH, int pW, int sH, int sW, int channels, int pixels,
-                 CUtensorMapSwizzle swizzle) {
+                 CUtensorMapSwizzle swizzle, int pW_right) {
     TmapKey key{};
     const uint64_t a[] = {1, (uint64_t)(uintptr_t)act, (uint64_t)N, (uint64_t)H, (uint64_t)W, (uint64_t)Cp,
                           (uint64_t)kH, (uint64_t)kW, (uint64_t)pH, (uint64_t)pW, (uint64_t)sH, (uint64_t)sW,
-                          (uint64_t)channels, (uint64_t)pixels, (uint64_t)swizzle};
+                          (uint64_t)channels, (uint64_t)pixels, (uint64_t)swizzle, (uint64_t)(int64_t)pW_right};
     std::memcpy(key.w, a, sizeof a);
     if (tmap_cache_on()) {
         auto& c = tmap_cache();
@@ -96,23 +96,23 @@ void tmap_im2col(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t
             g_tmap_hits.fetch_add(1, std::memory_order_relaxed);
             return;
         }
-        tmap_im2col_encode(m, act, N, H, W, Cp, kH, kW, pH, pW, sH, sW, channels, pixels, swizzle);
+        tmap_im2col_encode(m, act, N, H, W, Cp, kH, kW, pH, pW, sH, sW, channels, pixels, swizzle, pW_right);
         c.emplace(key, *m);
         return;
     }
-    tmap_im2col_encode(m, act, N, H, W, Cp, kH, kW, pH, pW, sH, sW, channels, pixels, swizzle);
+    tmap_im2col_encode(m, act, N, H, W, Cp, kH, kW, pH, pW, sH, sW, channels, pixels, swizzle, pW_right);
 }
 
 void tmap_im2col_encode(CUtensorMap* m, const float* act, int64_t N, int64_t H, int64_t W, int64_t Cp,
                         int kH, int kW, int pH, int pW, int sH, int sW, int channels, int pixels,
-                        CUtensorMapSwizzle swizzle) {
+                        CUtensorMapSwizzle swizzle, int pW_right) {
     load();
     g_tmap_encodes.fetch_add(1, std::memory_order_relaxed);
     cuuint64_t dims[4] = {(cuuint64_t)Cp, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
     cuuint64_t strides[3] = {(cuuint64_t)(Cp * 4), (cuuint64_t)(W * Cp * 4),
                              (cuuint64_t)(H * W * Cp * 4)};
     int lower[2] = {-pW, -pH};
-    int upper[2] = {pW - (kW - 1), pH - (kH - 1)};
+    int upper[2] = {(pW_right < 0 ? pW : pW_right) - (kW - 1), pH - (kH - 1)};
     cuuint32_t estr[4] = {1, (cuuint32_t)sW, (cuuint32_t)sH, 1};
     CUresult r = g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(act), dims,
                                  strides, lower, upper, (cuuint32_t)channels, (cuuint32_t)pixels, estr,

@@ -479,7 +479,8 @@ int hconv_pair_max() {
 void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, int64_t pw, int64_t kW,
                  int64_t oH, int64_t oW) {
     if (pl.cb != 32 || pl.cg != 2 || kW < 3 || kW > 120 || hconv_env() == 0) return;
-    const int64_t Hp = aH + 2 * ph, Wp = aW + 2 * pw;
+    // position rows carry the left border only (hconv_wrap, umma_hconv.cu)
+    const int64_t Hp = aH + 2 * ph, Wp = aW + (hconv_wrap() ? 1 : 2) * pw;
     if (Wp > 256 || N * aH * aW >= (1ll << 31)) return;  // a padded row is one TMA box dimension
     // efficiency from the geometry alone (not N) so a batch and its per-image slices
     // always take the same engine (batched == per-image bitwise): each image's

@@ -502,6 +502,14 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
 // Tiling: each image's output rows are split into two halves of R rows; CTA 0 of a pair
 // walks the top half and CTA 1 the bottom half at the same offset, so both CTAs' pixel
 // runs start at the same column and one shared descriptor addresses both.
+bool hconv_wrap() {
+    static const bool wrap = [] {
+        const char* e = std::getenv("PT_B200_HCONV_WRAP");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return wrap;
+}
+
 HConvTiling hconv_tiling(int64_t N, int64_t Wp, int64_t oH, int64_t cta_span) {
     HConvTiling t;
     const int64_t R = (oH + 1) / 2;
@@ -514,7 +522,13 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
                int64_t aW, int64_t aph, int64_t apw, int kH, int kW, int64_t oH, int64_t oW,
                float* out, const float* bias, double alg_flops, cudaStream_t st) {
     PTB_REQUIRE(pl.cb == 32 && pl.cg == 2, "hconv: needs the 32-channel CTA-pair plan");
-    const int64_t Wp = aW + 2 * apw;
+    // Position rows carry only the LEFT border: a tap reading past the right edge of row i
+    // wraps into row i+1's left border, which is zero (TMA out-of-bounds) exactly like the
+    // right border it replaces — valid because the right border is never wider than the left
+    // (symmetric padding). Each row then wastes kW-1-apw junk positions instead of kW-1 (the
+    // full-padding transposed conv of a pad-0 layer: none; convnet L2 dgrad 72 -> 64).
+    // PT_B200_HCONV_WRAP=0 restores the two-sided border.
+    const int64_t Wp = aW + (hconv_wrap() ? 1 : 2) * apw;
     PTB_REQUIRE(Wp <= 256 && kW <= 120, "hconv: padded row too wide for one TMA box");
     const int G = pl.tap_group;
     const bool pair = G > 1;
@@ -567,7 +581,7 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         tmap_tiled(&p.tmap_a2, act, 5, dims, strides, box2, CU_TENSOR_MAP_SWIZZLE_128B);
         if (p.a_run)  // positions (i, j < Wp) -> input (i + r - aph, j - apw): a kH x 1 "conv" with pad (aph, apw)
             tmap_im2col(&p.tmap_run, act, N, aH, aW, pl.cin_p, kH, 1, (int)aph, (int)apw, 1, 1, 32, p.run_px,
-                        CU_TENSOR_MAP_SWIZZLE_128B);
+                        CU_TENSOR_MAP_SWIZZLE_128B, (int)(Wp - aW - apw));
     }
     if (!pair) {
         // {32, weight rows, 32-wide k blocks}: one box = the CPS chunks of one tap
