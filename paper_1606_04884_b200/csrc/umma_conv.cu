@@ -439,6 +439,35 @@ void plan_rows(UmmaPlan& pl) {
     pl.wt_elems = pl.cb == 32 ? pl.n_pad * kdim_p : pl.slots_p * pl.n_pad * 4;
 }
 
+// Wave quantisation of the im2col engine on small layers: with few 256-pixel tiles (13x13
+// maps at batch 128: 85) a 256-row N tile leaves 85 units for 74 CTA pairs — two rounds,
+// 57 % busy. N tiles of 128 rows (an N=128 MMA costs the same ~64 cycles as N=256 costs
+// 128) give more units; pick the tiling with the fewest MMA cycles over whole rounds,
+// rounds x max(64, bn/2). Tiling never changes a sum's order (each output channel's
+// reduction is the same), so this may depend on N. PT_B200_CONV_REBALANCE=0: off.
+void rebalance_rows(UmmaPlan& pl, int64_t M) {
+    static const bool on = [] {
+        const char* e = std::getenv("PT_B200_CONV_REBALANCE");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    if (!on || pl.n_rows <= 128) return;
+    const int64_t pairs = std::max(1, sm_count() / 2);
+    const int64_t m_tiles = ceil_div(M, 256);
+    auto cost = [&](int64_t bn, int64_t nt) {
+        const int64_t rounds = ceil_div(m_tiles * nt, pairs);
+        return rounds * std::max<int64_t>(64, bn / 2) * 2;  // x2: keep integers for odd bn/2
+    };
+    const int64_t nt0 = pl.n_tiles, bn0 = pl.bn;
+    const int64_t nt1 = ceil_div(pl.n_rows, 128);
+    const int64_t bn1 = (ceil_div(pl.n_rows, nt1) + 15) / 16 * 16;
+    if (cost(bn1, nt1) < cost(bn0, nt0)) {
+        pl.bn = (int)bn1;
+        pl.n_tiles = (int)ceil_div(pl.n_rows, bn1);
+        pl.n_pad = (int64_t)pl.n_tiles * pl.bn;
+        pl.wt_elems = pl.n_pad * pl.kdim;
+    }
+}
+
 // Hankel engine choice: the pixel-run kernel wastes the border columns it computes
 // (valid / computed positions); the im2col kernel wastes nothing but is L2->SM bound.
 int hconv_env() {
@@ -596,6 +625,7 @@ UmmaPlan umma_plan(const Geo& g, bool dgrad) {
         }
     }
     if (pl.taps * pl.cin_p > (1ll << 31) / 4) return pl;
+    if (!pl.hankel && pl.cb == 32 && pl.cg == 2) rebalance_rows(pl, dgrad ? g.N * g.HW : g.M);
     pl.ws_bytes = align_up(pl.act_elems * 4, 256) + align_up(pl.wt_elems * 4, 256) +
                   align_up(pl.extra_elems * 4, 256);
     pl.ok = true;

@@ -204,11 +204,15 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
                     tmem_ld_32x32b_x16(taddr + c0, v);
                     tmem_ld_wait();
                     if (valid) {
+                        // partials stay in L2 for the reduce (umma.cuh: l2_evict_last_policy)
+                        const uint64_t pol = l2_evict_last_policy();
                         float4* d4 = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
                         for (int jj = 0; jj < 4; ++jj)
-                            d4[jj] = make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
-                                                 __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3]));
+                            st_f4_l2hint(d4 + jj,
+                                         make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
+                                                     __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3])),
+                                         pol);
                     }
                 }
             }

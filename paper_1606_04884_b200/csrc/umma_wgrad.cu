@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
         }
     } else {
         const uint32_t q = warp & 3;
+        const uint64_t pol = l2_evict_last_policy();
         int it = 0;
         for (int u = cluster; u < units; u += nclusters, ++it) {
             int mt, nt, sp;
@@ -216,8 +217,10 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
                     float4* d4 = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
                     for (int jj = 0; jj < 4; ++jj)
-                        d4[jj] = make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
-                                             __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3]));
+                        st_f4_l2hint(d4 + jj,
+                                     make_float4(__uint_as_float(v[4 * jj]), __uint_as_float(v[4 * jj + 1]),
+                                                 __uint_as_float(v[4 * jj + 2]), __uint_as_float(v[4 * jj + 3])),
+                                     pol);
                 }
             }
             tc_fence_before();
@@ -246,6 +249,7 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
     const int K4 = K / 4;
     const int taps = kH * kW;
     const int total = K4 * C * taps;
+    const uint64_t pol = l2_evict_first_policy();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int crs = i / K4, k = (i - crs * K4) * 4;
         const int c = crs / taps, rs = crs - c * taps;  // rs = r*kW + s
@@ -253,7 +257,7 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
         for (int sp = 0; sp < splits; ++sp) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (int64_t)sp * split_stride));
+            const float4 v = ld_f4_l2hint(reinterpret_cast<const float4*>(src + (int64_t)sp * split_stride), pol);
             acc.x += v.x;
             acc.y += v.y;
             acc.z += v.z;
@@ -275,13 +279,14 @@ __global__ void wgrad_reduce1_kernel(const float* __restrict__ part, float* __re
                                      int accumulate) {
     const int total = K * C * kH * kW;
     const int taps = kH * kW;
+    const uint64_t pol = l2_evict_first_policy();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         const int crs = i / K, k = i - crs * K;
         const int c = crs / taps, rs = crs - c * taps;
         const float* src = part + ((int64_t)rs * Cp + c) * ld + k;
         float acc = 0.f;
 #pragma unroll 8
-        for (int sp = 0; sp < splits; ++sp) acc += __ldg(src + (int64_t)sp * split_stride);
+        for (int sp = 0; sp < splits; ++sp) acc += ld_f_l2hint(src + (int64_t)sp * split_stride, pol);
         const int64_t o = (int64_t)k * C * taps + crs;
         gw[o] = (accumulate ? gw[o] : 0.f) + scale * acc;
     }
