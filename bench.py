@@ -487,26 +487,38 @@ def main():
     tf32_mma = float(L.lib().pt_b200_tf32_mma_peak()) if rank == 0 else -1.0
     peak_tf = max(tf32_mma, tf32_derived, tf32_cublas or 0.0)
     dom = max(per, key=lambda k: per[k][0])
-    dms, dn, dfl, _ = per[dom]
+    dms, dn, dfl, dby = per[dom]
     avg_ms = dms / dn
-    roof = {"bound": "tensor", "achieved": dfl / dn / (avg_ms * 1e-3) / 1e12, "peak": peak_tf,
-            "unit": "TFLOP/s"}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    if dby > 0 and dfl / dby < peak_tf * 1e12 / (hbm_peak * 1e9):
+        # below the ridge point (e.g. the fused small-C backward: 11 GFLOP over 0.9 GB): the
+        # HBM roofline binds; achieved = its algorithmic bytes per launch / launch time
+        roof = {"bound": "hbm", "achieved": dby / dn / (avg_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s", "tensor_tflops": dfl / dn / (avg_ms * 1e-3) / 1e12}
+    else:
+        roof = {"bound": "tensor", "achieved": dfl / dn / (avg_ms * 1e-3) / 1e12, "peak": peak_tf,
+                "unit": "TFLOP/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = ncu_traffic(args.workload, dom)
     roof["kernel"] = dom
     roof["avg_launch_ms"] = avg_ms
     roof["flops_per_launch"] = dfl / dn
+    roof["bytes_per_launch"] = dby / dn
     roof["share_of_step"] = dms / ms_serial if ms_serial > 0 else None
     roof["step_frac"] = value / 1e3 / peak_tf
     roof["timing"] = ("per-launch CUDA events in a serialised, eagerly launched pass of the same steps "
                       f"right after the timed region ({ms_serial / args.steps:.3f} ms/step serialised vs "
                       f"{ms / args.steps:.3f} ms/step timed: backward's two streams, "
                       + ("CUDA-graph replay)" if graph is not None else "eager launches)"))
-    roof["peak_source"] = (f"max(measured TF32 MMA ceiling on this box = {tf32_mma:.1f} "
-                           f"[pt_b200_tf32_mma_peak], cuBLAS TF32 8192^3 = {tf32_cublas}, "
-                           f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})")
-    roof["frac_vs_bf16_half"] = roof["achieved"] / tf32_derived
-    roof["per_launch"] = {k: {"ms": v[0] / v[1], "tflops": v[2] / v[0] * 1e-9}
+    if roof["bound"] == "hbm":
+        roof["peak_source"] = f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, copy bandwidth)"
+    else:
+        roof["peak_source"] = (f"max(measured TF32 MMA ceiling on this box = {tf32_mma:.1f} "
+                               f"[pt_b200_tf32_mma_peak], cuBLAS TF32 8192^3 = {tf32_cublas}, "
+                               f"{peak_kind} bf16 burst/2 = {tf32_derived:.1f})")
+        roof["frac_vs_bf16_half"] = roof["achieved"] / tf32_derived
+    roof["per_launch"] = {k: {"ms": v[0] / v[1], "tflops": v[2] / v[0] * 1e-9,
+                              **({"gbs": v[3] / v[0] * 1e-6} if v[3] > 0 else {})}
                           for k, v in sorted(per.items())}
 
     result = {

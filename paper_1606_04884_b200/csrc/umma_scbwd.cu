@@ -668,7 +668,10 @@ void scbwd(const Geo& g, const float* x, const float* gy, const float* w, float*
     });
     {
         const double flops = 2.0 * g.M * g.K * g.CRS * ((gx ? 1 : 0) + (gw ? 1 : 0));
-        ProfScope prof(gw ? "umma_wgrad" : "umma_conv", st, flops, 0.0);
+        // algorithmic bytes: gy read once, gx written, x read (the HBM roofline of this kernel)
+        const double bytes = 4.0 * ((double)g.N * g.K * g.oHW + (gx ? (double)g.N * g.C * g.HW : 0.0) +
+                                    (gw ? (double)g.N * g.C * g.HW : 0.0));
+        ProfScope prof(gw ? "umma_wgrad" : "umma_conv", st, flops, bytes);
         const bool f3 = g.kH == 3 && g.kW == 3 && g.C == 3;
         const dim3 grid((unsigned)pl.ctas);
         if (pl.Kp == 32 && f3) umma_scbwd_kernel<32, 1><<<grid, kThreadsB, pl.smem, st>>>(p);
