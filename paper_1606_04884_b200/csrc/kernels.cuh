@@ -164,13 +164,6 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
                           int64_t xpw = 0);
 int64_t umma_wgrad_kp(const Geo& g);  // channel padding of the wgrad gy operand
 
-// ---- umma_fdgrad.cu: small-C stride-1 input gradient (gcol GEMM + fused col2im fold) ----
-bool fdgrad_ok(const Geo& g);
-size_t fdgrad_workspace(const Geo& g);
-// gyh_pre: gy NHWC with (K+31)/32*32 channels (TF32-rounded), or null to transform here
-void fdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st,
-            const float* gyh_pre);
-
 // ---- umma_hwgrad.cu: stride-1 wide-filter weight gradient (Hankel tap quads) ----
 bool hwgrad_ok(const Geo& g);
 size_t hwgrad_part_bytes(const Geo& g);

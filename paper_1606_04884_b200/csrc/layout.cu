@@ -204,43 +204,6 @@ __global__ void pack_weights_kernel(const float* __restrict__ w, float* __restri
     }
 }
 
-// Layout-32 fprop / dgrad-flip packing, one block per packed row: the row's source
-// weights are staged in smem with coalesced reads (fprop: W[row][c][r][s] is contiguous;
-// dgrad: W[k][row][r][s] is one contiguous run of taps per k), then the packed row
-// dst[row][tap*cin_p + ch] (zero past the real taps / channels) is written coalesced.
-__global__ void pack_rows_kernel(const float* __restrict__ w, float* __restrict__ dst, int K, int C, int kH,
-                                 int kW, int dgrad, int n_real, int cin_p, int kdim_p) {
-    extern __shared__ float sw[];  // [cin_real][taps]
-    const int row = blockIdx.x;
-    const int taps = kH * kW;
-    const int cin_real = dgrad ? K : C;
-    float* out = dst + (int64_t)row * kdim_p;
-    if (row < n_real) {
-        // several loads in flight per thread (a load -> smem store per iteration otherwise
-        // serialises on the load latency)
-        if (!dgrad) {
-            const float* src = w + (int64_t)row * C * taps;
-#pragma unroll 4
-            for (int e = threadIdx.x; e < C * taps; e += blockDim.x) sw[e] = __ldg(src + e);
-        } else {
-#pragma unroll 4
-            for (int e = threadIdx.x; e < K * taps; e += blockDim.x) {
-                const int k = e / taps, t = e - k * taps;
-                sw[e] = __ldg(w + ((int64_t)k * C + row) * taps + t);
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int kd = threadIdx.x; kd < kdim_p; kd += blockDim.x) {
-        const int tap = kd / cin_p, ch = kd - tap * cin_p;
-        float v = 0.f;
-        if (row < n_real && tap < taps && ch < cin_real)
-            v = sw[ch * taps + (dgrad ? taps - 1 - tap : tap)];  // flip = (kH-1-r, kW-1-s)
-        out[kd] = to_tf32(v);
-    }
-}
-
 // Stage 1: block (k, split) sums its contiguous share of the N*HW run of channel k.
 __global__ void bias_grad_partial_kernel(const float* __restrict__ gy, float* __restrict__ part,
                                          int64_t N, int64_t K, int64_t HW, int splits) {
@@ -364,27 +327,6 @@ void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, 
                   int mode, int layout, int64_t n_pad, int64_t cin_p, int64_t slots_p,
                   int64_t total, bool round_tf32, cudaStream_t st) {
     PTB_REQUIRE(total < (1ll << 31) && K * C * kH * kW < (1ll << 31), "pack_weights: weights too large");
-    const size_t row_smem = sizeof(float) * (size_t)(mode == kPackDgradFlip ? K : C) * kH * kW;
-    // one block per packed row: coalesced reads of the row's source weights, coalesced
-    // row writes (the flat kernel's per-element reads are 4 bytes at a kH*kW stride);
-    // 1024 threads and unrolled loads keep enough bytes in flight (PT_B200_PACK_ROWS=0:
-    // flat kernel)
-    static const bool rows_on = [] {
-        const char* e = std::getenv("PT_B200_PACK_ROWS");
-        return e ? std::atoi(e) != 0 : false;  // measured equal to the flat kernel (~10 us, latency-bound)
-    }();
-    if (rows_on && layout == 32 && round_tf32 && (mode == kPackFprop || mode == kPackDgradFlip) &&
-        row_smem <= 96 * 1024) {
-        once_per_device((const void*)pack_rows_kernel, [&] {  // the smem limit is a per-device attribute
-            PTB_CUDA(cudaFuncSetAttribute(pack_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        });
-        const int n_real = (int)(mode == kPackFprop ? K : C);
-        pack_rows_kernel<<<(unsigned)n_pad, 1024, row_smem, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW,
-                                                                 mode == kPackDgradFlip ? 1 : 0, n_real,
-                                                                 (int)cin_p, (int)(total / n_pad));
-        after_launch("pack_rows");
-        return;
-    }
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 32 * (int64_t)sm_count());
     pack_weights_kernel<<<blocks, 256, 0, st>>>(w, dst, (int)K, (int)C, (int)kH, (int)kW, mode, layout,
                                                 (int)n_pad, (int)cin_p, (int)slots_p, (int)total, round_tf32);

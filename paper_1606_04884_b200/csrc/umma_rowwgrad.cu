@@ -241,7 +241,6 @@ bool rowdgrad_ok(const Geo& g, UmmaPlan* plan) {
 size_t rowdgrad_workspace(const Geo& g) {
     UmmaPlan pl;
     if (!rowdgrad_ok(g, &pl)) return 0;
-    if (fdgrad_ok(g)) return fdgrad_workspace(g);
     const Geo e = dgrad_rows_geo(g);
     return align_up((size_t)(g.K * g.CRS) * 4, 256) + align_up((size_t)(e.N * e.C * e.H * e.W) * 4, 256) +
            align_up(pl.ws_bytes, 256);
@@ -256,10 +255,6 @@ void rowdgrad(const Geo& g, const float* gy, const float* w, float* gx, void* ws
               const float* gyh_pre, bool pre_padded) {
     UmmaPlan pl;
     PTB_REQUIRE(rowdgrad_ok(g, &pl), "rowdgrad: unsupported geometry");
-    if (fdgrad_ok(g) && !pre_padded) {  // gcol GEMM with the col2im fold fused (umma_fdgrad.cu)
-        fdgrad(g, gy, w, gx, ws, st, gyh_pre);
-        return;
-    }
     const Geo e = dgrad_rows_geo(g);
     char* base = reinterpret_cast<char*>(ws);
     float* we = reinterpret_cast<float*>(base);

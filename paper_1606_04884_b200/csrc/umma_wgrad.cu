@@ -323,14 +323,6 @@ int wgrad_kp_env() {
     return v;
 }
 
-int wgrad_mt_env() {
-    static const int v = [] {
-        const char* e = std::getenv("PT_B200_WGRAD_MT");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
-
 struct WPlan {
     int64_t Cp, Kp, kdim;
     int mt;  // m-tiles per unit (1 or 2)
@@ -347,10 +339,10 @@ WPlan wplan(const Geo& g) {
     w.n_tiles = (int)ceil_div(w.Kp, 256);
     w.bn = (int)(ceil_div(ceil_div(w.Kp, w.n_tiles), 64) * 64);
     w.m_tiles = (int)ceil_div(w.kdim, 256);
-    // two m-tiles per unit can share the B stage (PT_B200_WGRAD_MT=2); measured slower on
-    // convnet L1-L3 (L2 wgrad 1.00 -> 1.42 ms: the 32-pixel boxes it needs to keep the ring
-    // depth halve the bytes per TMA request), so one m-tile per unit is the default
-    w.mt = (wgrad_mt_env() == 2 && w.bn <= 128 && w.m_tiles >= 2) ? 2 : 1;
+    // one m-tile per unit (two m-tiles sharing each B stage measured slower in round 1: L2
+    // wgrad 1.00 -> 1.42 ms — the 32-pixel boxes needed to keep the ring depth halve the
+    // bytes per TMA request — and were removed)
+    w.mt = 1;
     w.kp = w.mt == 2 ? 32 : wgrad_kp_env();
     // <= 64 channels (two 32-channel chunks): 64-pixel stages measured faster (AlexNet conv2
     // wgrad 0.110 -> 0.099 ms)
@@ -464,8 +456,6 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
                                       kSmemLimit));
         PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kSmemLimit));
-        PTB_CUDA(cudaFuncSetAttribute(umma_wgrad_kernel<2, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      kSmemLimit));
     });
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
@@ -481,8 +471,7 @@ void umma_conv_bwd_filter(const Geo& g, const float* x, const float* gy, float* 
     cfg.numAttrs = 1;
     {
         ProfScope prof("umma_wgrad", st, alg_flops >= 0 ? alg_flops : 2.0 * g.M * g.K * g.CRS, 0.0);
-        if (w.mt == 2) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<2, 32>, p));
-        else if (w.kp == 128) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1, 128>, p));
+        if (w.kp == 128) PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1, 128>, p));
         else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_wgrad_kernel<1, 64>, p));
         after_launch("umma_wgrad");
     }

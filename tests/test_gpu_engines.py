@@ -59,7 +59,6 @@ CONFIGS = {
     "rowdgrad-horizontal": {"PT_B200_ROWDGRAD": "0"},
     "rowconv-epi4": {"PT_B200_ROWCONV_EPI": "4"},
     "serial-bwd": {"PT_B200_BWD_STREAMS": "0"},
-    "fdgrad": {"PT_B200_FDGRAD": "1"},
     "scbwd-off": {"PT_B200_SCBWD": "0"},
 }
 
@@ -71,7 +70,7 @@ def _extra(cfg):
         return HANKEL_EDGE
     if cfg.startswith("hwgrad"):
         return HWGRAD_EDGE
-    if cfg in ("swgrad-off", "no-rowconv", "rowdgrad-horizontal", "rowconv-epi4", "fdgrad"):
+    if cfg in ("swgrad-off", "no-rowconv", "rowdgrad-horizontal", "rowconv-epi4"):
         return SMALLC_GEOMS
     return []
 
