@@ -51,7 +51,7 @@ $(LIBDIR)/libpt_b200.so: $(CU_OBJS) $(CC_OBJS)
 
 $(LIBDIR)/libportten.so: $(HOST_SRCS) $(HOST_HDRS) $(LIBDIR)/libpt_b200.so
 	@mkdir -p $(LIBDIR)
-	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIBDIR) -lpt_b200 -Wl,-rpath,'$$ORIGIN'
+	$(CXX) $(CXXFLAGS) -shared -o $@ $(HOST_SRCS) -L$(LIBDIR) -lpt_b200 -lnccl -Wl,-rpath,'$$ORIGIN'
 
 # test driver: links the product libraries and, as the checker only, the oracle
 tests/cpp/portten_tests: tests/cpp/portten_tests.cpp $(LIBDIR)/libportten.so oracle/oracle.h oracle

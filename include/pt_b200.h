@@ -97,6 +97,9 @@ int pt_b200_free(void* ptr);
 int pt_b200_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 int pt_b200_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
 int pt_b200_stream_sync(void* stream);
+/* Non-blocking completion check of `stream`: PT_OK when all its work is done, 1 while work
+ * is pending, PT_EBACKEND on a device error (used to poll NCCL's async error meanwhile). */
+int pt_b200_stream_query(void* stream);
 /* Same generator as oracle or_fill_uniform (counter-based splitmix64). */
 int pt_b200_fill_uniform(float* dst, int64_t n, uint64_t seed, float lo, float hi, void* stream);
 

@@ -66,6 +66,7 @@ _SIGS = {
     "pt_b200_memcpy_h2d": (C.c_int, [_P, _P, C.c_size_t, _P]),
     "pt_b200_memcpy_d2h": (C.c_int, [_P, _P, C.c_size_t, _P]),
     "pt_b200_stream_sync": (C.c_int, [_P]),
+    "pt_b200_stream_query": (C.c_int, [_P]),
     "pt_b200_fill_uniform": (C.c_int, [_P, C.c_int64, C.c_uint64, C.c_float, C.c_float, _P]),
     "pt_b200_conv_validate": (C.c_int, [C.POINTER(PtConvGeom)]),
     "pt_b200_conv_workspace_bytes": (C.c_size_t, [C.POINTER(PtConvGeom), C.c_int, C.c_int]),

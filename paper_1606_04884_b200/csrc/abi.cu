@@ -561,6 +561,14 @@ int pt_b200_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
     });
 }
 
+int pt_b200_stream_query(void* stream) {
+    const cudaError_t e = cudaStreamQuery(as_stream(stream));
+    if (e == cudaSuccess) return PT_OK;
+    if (e == cudaErrorNotReady) return 1;
+    set_last_error(cudaGetErrorString(e));
+    return PT_EBACKEND;
+}
+
 int pt_b200_stream_sync(void* stream) {
     return guarded([&] { PTB_CUDA(cudaStreamSynchronize(as_stream(stream))); });
 }

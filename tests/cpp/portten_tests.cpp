@@ -13,6 +13,7 @@
 #include "../../oracle/oracle.h"
 #include "portten/backend.hpp"
 #include "portten/convolution.hpp"
+#include "portten/data_parallel.hpp"
 
 using namespace portten;
 
@@ -305,6 +306,56 @@ static void test_gpu_layer_and_ops() {
     EXPECT(std::memcmp(col.data(), rcol.data(), sizeof(float) * col.numel()) == 0);
 }
 
+// ---------------------------------------------------------------- data parallelism
+static void test_shard_range() {
+    for (std::int64_t n : {128, 64, 7, 1}) {
+        for (int world = 1; world <= 8; ++world) {
+            std::int64_t next = 0;
+            for (int r = 0; r < world; ++r) {
+                const dp::ShardRange s = dp::shard_range(n, r, world);
+                EXPECT(s.start == next);  // contiguous, in rank order
+                const std::int64_t len = s.stop - s.start;
+                EXPECT(len == n / world + (r < n % world ? 1 : 0));  // remainder to the low ranks
+                next = s.stop;
+            }
+            EXPECT(next == n);
+        }
+    }
+    EXPECT(throws<ValidationError>([] { dp::shard_range(8, 2, 2); }));
+    EXPECT(throws<ValidationError>([] { dp::shard_range(8, 0, 0); }));
+}
+
+// one GPU: the shards' gradients sum to the full batch's (the DP identity), and a world-1 NCCL
+// communicator's allreduce + error-polling synchronize leave the gradients bitwise unchanged
+static void test_gpu_dp() {
+    const conv::ConvGeometry full(4, 32, 12, 12, 48, 3, 3, 1, 1, 1, 1);
+    Tensor x = seeded({4, 32, 12, 12}, 31), gy = seeded({4, 48, 12, 12}, 32);
+    DeviceTensor dx = DeviceTensor::upload(x), dgy = DeviceTensor::upload(gy);
+    DeviceTensor gw = DeviceTensor::empty({48, 32, 3, 3}), gb = DeviceTensor::empty({48});
+    conv::conv_backward_weight(full, dx, dgy, gw, &gb);
+    // two emulated ranks: each its shard, accumulated into one buffer (= the allreduce's sum)
+    DeviceTensor sw = DeviceTensor::empty({48, 32, 3, 3}), sb = DeviceTensor::empty({48});
+    for (int r = 0; r < 2; ++r) {
+        const dp::ShardRange s = dp::shard_range(4, r, 2);
+        const conv::ConvGeometry part(s.stop - s.start, 32, 12, 12, 48, 3, 3, 1, 1, 1, 1);
+        conv::conv_backward_weight(part, dx.narrow(0, s.start, s.stop - s.start),
+                                   dgy.narrow(0, s.start, s.stop - s.start), sw, &sb, 1.0f, r > 0);
+    }
+    Tensor hf = gw.download(), hs = sw.download();
+    std::vector<float> ref(hf.data(), hf.data() + hf.numel());
+    EXPECT(rel_err(hs, ref) < 1e-5);  // same TF32 products, two fp32 partial sums
+    Tensor hb = gb.download(), hsb = sb.download();
+    std::vector<float> refb(hb.data(), hb.data() + hb.numel());
+    EXPECT(rel_err(hsb, refb) < 1e-6);
+    dp::Communicator comm(dp::new_unique_id(), 0, 1, 0);
+    EXPECT(comm.rank() == 0 && comm.world() == 1);
+    comm.allreduceGradients(gw, &gb, nullptr);
+    comm.synchronize(nullptr, 60.0);
+    Tensor aw = gw.download(), ab = gb.download();
+    EXPECT(std::memcmp(aw.data(), hf.data(), sizeof(float) * hf.numel()) == 0);
+    EXPECT(std::memcmp(ab.data(), hb.data(), sizeof(float) * hb.numel()) == 0);
+}
+
 int main(int argc, char** argv) {
     const bool gpu = argc > 1 && std::strcmp(argv[1], "--gpu") == 0;
     test_tensor_views();
@@ -312,7 +363,9 @@ int main(int argc, char** argv) {
     test_expression();
     test_launch_and_selection();
     test_registry();
+    test_shard_range();
     if (gpu) {
+        test_gpu_dp();
         test_gpu_conv();
         test_gpu_layer_and_ops();
         test_gpu_bench_layers_exact();
