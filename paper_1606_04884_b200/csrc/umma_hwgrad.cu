@@ -20,6 +20,14 @@
 // per stage one x box {32 ch, KP + 4*qpr - 1 px, R rows} (CTA's chunk) and one gy box
 // {32 k, KP px, R rows, BN/64 blocks}. Partials [split][(r*kW+s)*Cp + c][k] are reduced
 // by umma_wgrad.cu's fixed-order wgrad_reduce_kernel (deterministic).
+//
+// Vertical quads. With kW % 4 != 0 the last quad of every row wastes slots (kW = 9: 12 slots
+// for 9 taps). The leftover columns s >= 4*floor(kW/4) are instead covered by quads of four
+// consecutive FILTER ROWS r..r+3 of one column s: the same staged data read with LBO = one
+// box row (Wbox pixels) instead of one pixel, from a box of R + 3 input rows. A "vertical"
+// unit = (band of 4 filter rows, chunk pair, n-tile, split) owns one such quad per leftover
+// column; "horizontal" units keep floor(kW/4) quads per row. kW = kH = 9: 21 quads instead
+// of 27 (84 slots for 81 taps).
 #include <cuda.h>
 
 #include <cstdlib>
@@ -40,7 +48,10 @@ constexpr int kSmemLimitHW = 232448;
 struct HWParams {
     CUtensorMap tmap_x;   // x NHWC 5-D {32, W, H, N, Cp/32}, box {32, Wbox, R, 1, 1}, SW128_32B
     CUtensorMap tmap_gy;  // gy NHWC 5-D {32, oW, oH, N, Kp/32}, box {32, KP, R, 1, BN/64}, SW128_32B
+    CUtensorMap tmap_xv;  // vertical units: x box {32, Wbox, R + 3, 1, 1}
     int oH, oW, pH, pW, kW, Cp;
+    int qh, ql, nbands;   // vertical quads: horizontal quads per row, leftover columns, 4-row bands (0: off)
+    uint32_t tx_v;        // TMA bytes of a vertical unit's stage
     int R, KP, Wbox, jsegs, rgs;
     int qpr;              // quads per filter row
     int cps, n_tiles, splits, kH;
@@ -85,16 +96,22 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
-    const int units = p.kH * p.cps * p.n_tiles * p.splits;
+    const int units_h = p.kH * p.cps * p.n_tiles * p.splits;
+    const int units = units_h + p.nbands * p.cps * p.n_tiles * p.splits;
     const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-    // unit -> (r, chunk pair, n-tile, split); r fastest: concurrent pairs share gy stages in L2
-    auto decode = [&](int u, int& r, int& cp, int& nt, int& sp) {
-        r = u % p.kH;
-        int v = u / p.kH;
+    // unit -> (r, chunk pair, n-tile, split); r fastest: concurrent pairs share gy stages in L2.
+    // Units past units_h are vertical: r = the band's first filter row (4 * band), vt = true.
+    auto decode = [&](int u, int& r, int& cp, int& nt, int& sp, bool& vt) {
+        vt = u >= units_h;
+        const int rows = vt ? p.nbands : p.kH;
+        if (vt) u -= units_h;
+        r = u % rows;
+        int v = u / rows;
         cp = v % p.cps;
         v /= p.cps;
         nt = v % p.n_tiles;
         sp = v / p.n_tiles;
+        if (vt) r *= 4;
     };
     // 32-bit only: a 64-bit division is a call, after which the compiler keeps the MMA
     // loop's descriptor state in vector registers (R2UR + elect per MMA)
@@ -110,7 +127,8 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
             const uint32_t tx = p.tx;
             for (int u = cluster; u < units; u += nclusters) {
                 int r, cp, nt, sp, lo, hi;
-                decode(u, r, cp, nt, sp);
+                bool vt;
+                decode(u, r, cp, nt, sp, vt);
                 range(sp, lo, hi);
                 const int chunk = 2 * cp + (int)rank;
                 const int kb = (nt * p.bn + (int)rank * (p.bn / 2)) / 32;
@@ -121,9 +139,11 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
                     const int j0 = js * p.KP, i0 = rg * p.R;
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a = smem + (size_t)stage * stage_bytes;
-                    if (leader) mbar_arrive_expect_tx(&full[stage], tx);
-                    // the input-row runs of filter row r for the stage's R output rows
-                    tma_load_5d_cg2(a, &p.tmap_x, &full[stage], 0, j0 - p.pW, i0 + r - p.pH, n, chunk);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], vt ? p.tx_v : tx);
+                    // the input-row runs of filter row r (vertical: rows r .. r+3) for the
+                    // stage's R output rows
+                    tma_load_5d_cg2(a, vt ? &p.tmap_xv : &p.tmap_x, &full[stage], 0, j0 - p.pW, i0 + r - p.pH, n,
+                                    chunk);
                     tma_load_5d_cg2(a + p.stage_a, &p.tmap_gy, &full[stage], 0, j0, i0, n, kb);
                     if (++stage == S) {
                         stage = 0;
@@ -146,8 +166,14 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
             int it_u = 0;
             for (int u = cluster; u < units; u += nclusters, ++it_u) {
                 int r, cp, nt, sp, lo, hi;
-                decode(u, r, cp, nt, sp);
+                bool vt;
+                decode(u, r, cp, nt, sp, vt);
                 range(sp, lo, hi);
+                // horizontal: quad q = taps 4q..4q+3 one pixel (128 B) apart; vertical: quad q =
+                // column 4*qh + q of filter rows r..r+3, one box row (Wbox px) apart
+                const int nq = vt ? p.ql : p.qh;
+                const uint32_t a_lbo = vt ? (uint32_t)p.Wbox * 128u : 128u;
+                const uint32_t q_step = vt ? 8u : 32u, q_base = vt ? (uint32_t)(4 * p.qh) * 8u : 0u;
                 mbar_wait(tempty, (it_u & 1) ^ 1);
                 tc_fence_after();
                 uint32_t accum = 0;
@@ -156,14 +182,15 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(smem + (size_t)stage * stage_bytes);
                     // A: taps s..s+3 = M atoms one pixel row (128 B) apart; B: BN/64 k-blocks
-                    uint32_t alo = desc_lo(a_addr, 128), blo = desc_lo(a_addr + p.stage_a, b_lbo);
+                    uint32_t alo = desc_lo(a_addr, a_lbo) + q_base, blo = desc_lo(a_addr + p.stage_a, b_lbo);
                     int k8 = 0;
                     for (int ks = 0; ks < nks; ++ks) {
                         const uint64_t bd = desc_make(blo, kHi);
 #pragma unroll
                         for (int q = 0; q < QPR; ++q)
-                            mma_tf32_cg2_warp(tmem_base + (uint32_t)q * bn, desc_make(alo + (uint32_t)(32 * q), kHi), bd,
-                                              idesc, accum);
+                            if (q < nq)
+                                mma_tf32_cg2_warp(tmem_base + (uint32_t)q * bn, desc_make(alo + q_step * (uint32_t)q, kHi),
+                                                  bd, idesc, accum);
                         accum = 1;
                         blo += 64u;  // 8 pixel rows
                         alo += 64u;
@@ -189,15 +216,18 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
         int it_u = 0;
         for (int u = cluster; u < units; u += nclusters, ++it_u) {
             int r, cp, nt, sp;
-            decode(u, r, cp, nt, sp);
+            bool vt;
+            decode(u, r, cp, nt, sp, vt);
             mbar_wait(tfull, it_u & 1);
             tc_fence_after();
             const int c = (2 * cp + (int)rank) * 32 + (int)lane;
-            for (int q = 0; q < p.qpr; ++q) {
-                const int s = 4 * q + (int)qtr;
-                const bool valid = s < p.kW && c < p.Cp;
+            const int nq = vt ? p.ql : p.qh;
+            for (int q = 0; q < nq; ++q) {
+                // lane quarter = tap s = 4q + quarter (horizontal) / filter row r + quarter (vertical)
+                const int s = vt ? 4 * p.qh + q : 4 * q + (int)qtr, rr = vt ? r + (int)qtr : r;
+                const bool valid = s < p.kW && rr < p.kH && c < p.Cp;
                 float* dst = p.part + (int64_t)sp * p.part_split +
-                             ((int64_t)(r * p.kW + s) * p.Cp + c) * p.part_ld + (int64_t)nt * p.bn;
+                             ((int64_t)(rr * p.kW + s) * p.Cp + c) * p.part_ld + (int64_t)nt * p.bn;
                 const uint32_t taddr = tmem_base + ((qtr * 32u) << 16) + (uint32_t)(q * p.bn);
                 for (int c0 = half * 16; c0 < p.bn; c0 += 32) {
                     uint32_t v[16];
@@ -234,6 +264,8 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
 
 struct HWPlan {
     int Cp, Kp, bn, n_tiles, qpr, KP, R, Wbox, jsegs, rgs, cps, splits, stages;
+    int qh, ql, nbands;  // horizontal quads per row, leftover columns, vertical bands (0: off)
+    int64_t quads;       // MMA quads per (chunk pair, n-tile, split) over all units
     int64_t items;
     uint32_t stage_a, stage_b, tmem_cols;
     int64_t part_elems;
@@ -254,17 +286,39 @@ HWPlan hwplan(const Geo& g) {
     w.n_tiles = (int)ceil_div(w.Kp, 256);
     w.bn = (int)(ceil_div(ceil_div(w.Kp, w.n_tiles), 64) * 64);
     w.qpr = (int)ceil_div(g.kW, 4);
+    w.qh = w.qpr;
+    w.ql = 0;
+    w.nbands = 0;
+    w.quads = g.kH * w.qpr;
+    {
+        // vertical quads for the leftover columns when they need fewer MMAs and every unit
+        // keeps >= 2 quads per staged box (kW = 5, one horizontal quad per row, measured
+        // slower: AlexNet conv2 wgrad, each gy stage then feeds one MMA per K step)
+        static const bool vert_on = [] {
+            const char* e = std::getenv("PT_B200_HWGRAD_VERT");
+            return e ? std::atoi(e) != 0 : true;
+        }();
+        const int qh = (int)(g.kW / 4), ql = (int)(g.kW % 4), nb = (int)ceil_div(g.kH, 4);
+        const int64_t q_new = g.kH * qh + (int64_t)nb * ql;
+        if (vert_on && qh >= 2 && ql >= 1 && q_new < w.quads) {
+            w.qh = qh;
+            w.ql = ql;
+            w.nbands = nb;
+            w.qpr = std::max(qh, ql);
+            w.quads = q_new;
+        }
+    }
     const int jsegs = (int)ceil_div(g.oW, 128);
     w.jsegs = jsegs;
     w.KP = (int)(ceil_div(ceil_div(g.oW, jsegs), 8) * 8);
     // R output rows per stage (<= 128 pixels), balanced so the last row group is not mostly empty
     const int rmax = std::max(1, 128 / w.KP);
     w.R = (int)ceil_div(g.oH, ceil_div(g.oH, rmax));
-    w.Wbox = w.KP + 4 * w.qpr - 1;
+    w.Wbox = w.nbands ? w.KP + (int)g.kW - 1 : w.KP + 4 * w.qpr - 1;
     w.rgs = (int)ceil_div(g.oH, w.R);
     w.items = g.N * w.rgs * w.jsegs;
     w.cps = (int)ceil_div(w.Cp / 32, 2);
-    w.stage_a = (uint32_t)align_up((size_t)w.R * w.Wbox * 128, 1024);
+    w.stage_a = (uint32_t)align_up((size_t)(w.R + (w.nbands ? 3 : 0)) * w.Wbox * 128, 1024);
     w.stage_b = (uint32_t)align_up((size_t)(w.bn / 64) * w.R * w.KP * 128, 1024);
     w.stages = std::min(8, (kSmemLimitHW - 1024 - 256) / (int)(w.stage_a + w.stage_b));
     uint32_t cols = 32;
@@ -272,7 +326,7 @@ HWPlan hwplan(const Geo& g) {
     w.tmem_cols = cols;
     // pixel splits: enough units for every CTA pair with a small tail (static schedule)
     const int64_t pairs = sm_count() / 2;
-    const int64_t base = (int64_t)g.kH * w.cps * w.n_tiles;
+    const int64_t base = (int64_t)(g.kH + w.nbands) * w.cps * w.n_tiles;
     int best = 1;
     double best_cost = 1e30;
     for (int sp = 1; sp <= 96; ++sp) {
@@ -307,7 +361,7 @@ bool hwgrad_ok(const Geo& g) {
     // useful fraction of the MMA work: tap slots x pixel columns x pixel rows computed
     // (convnet L2 0.75, L3 0.72 -> faster than the im2col engine; L4, 10x10 outputs in
     // 16-column stages: 0.55 -> slower, 0.046 -> 0.052 ms)
-    const double eff = (double)g.kW / (4.0 * w.qpr) * (double)g.oW / ((double)w.KP * w.jsegs) *
+    const double eff = (double)(g.kH * g.kW) / (4.0 * w.quads) * (double)g.oW / ((double)w.KP * w.jsegs) *
                        (double)g.oH / ((double)w.R * w.rgs);
     if (env != 2 && eff < 0.7) return false;
     if (w.qpr > 4 || w.qpr * w.bn > 512 || w.Wbox > 256 || w.R > 256 || w.stages < 2) return false;
@@ -328,6 +382,10 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
                                      128};
         const uint32_t box[5] = {32, (uint32_t)w.Wbox, (uint32_t)w.R, 1, 1};
         tmap_tiled(&p.tmap_x, xh, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        if (w.nbands) {
+            const uint32_t boxv[5] = {32, (uint32_t)w.Wbox, (uint32_t)(w.R + 3), 1, 1};
+            tmap_tiled(&p.tmap_xv, xh, 5, dims, strides, boxv, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+        }
     }
     {
         const uint64_t dims[5] = {32, (uint64_t)g.oW, (uint64_t)g.oH, (uint64_t)g.N, (uint64_t)(w.Kp / 32)};
@@ -348,6 +406,9 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
     p.jsegs = w.jsegs;
     p.rgs = w.rgs;
     p.qpr = w.qpr;
+    p.qh = w.qh;
+    p.ql = w.ql;
+    p.nbands = w.nbands;
     p.cps = w.cps;
     p.n_tiles = w.n_tiles;
     p.splits = w.splits;
@@ -360,12 +421,13 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
     p.stage_a = w.stage_a;
     p.stage_b = w.stage_b;
     p.tx = (uint32_t)(2 * ((size_t)w.R * w.Wbox * 128 + (size_t)(w.bn / 64) * w.R * w.KP * 128));
+    p.tx_v = (uint32_t)(2 * ((size_t)(w.R + 3) * w.Wbox * 128 + (size_t)(w.bn / 64) * w.R * w.KP * 128));
     p.tmem_cols = w.tmem_cols;
     p.part = part;
     p.part_ld = (int64_t)w.n_tiles * w.bn;
     p.part_split = g.kH * g.kW * w.Cp * p.part_ld;
     const size_t smem = 1024 + (size_t)w.stages * (w.stage_a + w.stage_b) + (2 * w.stages + 4) * 8 + 16;
-    const int units = (int)(g.kH * w.cps * w.n_tiles * w.splits);
+    const int units = (int)((g.kH + w.nbands) * w.cps * w.n_tiles * w.splits);
     const int pairs = std::min(units, sm_count() / 2);
     once_per_device((const void*)umma_hwgrad_kernel<1>, [&] {  // the smem limit is a per-device attribute
         PTB_CUDA(cudaFuncSetAttribute(umma_hwgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
