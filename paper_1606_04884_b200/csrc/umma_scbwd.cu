@@ -65,6 +65,8 @@ struct SCParams {
     int stages;
     uint32_t sz_gyt, sz_gyk, sz_xe, sz_x, stage_bytes, wt_off, ring_off, sd_off, bar_off;
     uint32_t tx;          // TMA bytes per stage
+    int dstages;          // derived-operand ring depth (K-major gy copy + Xe)
+    uint32_t dstage_bytes, d_off;
     int do_dg, do_wg, do_bias;
     uint32_t xbox;        // bytes of one x box (1024-aligned)
     int xoff;             // x tile starts xoff (= pW rounded up to 4) columns left of the gy block
@@ -97,11 +99,17 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
     const int S = p.stages;
     uint8_t* wt = smem + p.wt_off;                                   // W^T [KP/32][32 n][32 k]
     float* ring = reinterpret_cast<float*>(smem + p.ring_off);       // [C][B][W]
+    // two rings: TMA stages {gy tile (the dgrad operand, rounded in place), x tile} and
+    // derived stages {K-major gy copy, Xe} (the wgrad operands): a TMA stage is released as
+    // soon as the dgrad MMA and the Xe build are done with it, so more gy bytes are in flight
+    const int SD = p.dstages;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
-    uint64_t* ready = full + S;
-    uint64_t* empty = ready + S;
-    uint64_t* tfull = empty + S;   // [2]
-    uint64_t* tempty = tfull + 2;  // [2]
+    uint64_t* ready = full + S;      // builders' pass over the gy tile (dgrad operand ready)
+    uint64_t* empty = ready + S;     // dgrad MMA commit + the epilogue's Xe reads of the x tile
+    uint64_t* dready = empty + S;    // [SD] K-major copy + Xe written
+    uint64_t* dfree = dready + SD;   // [SD] wgrad MMAs done with them
+    uint64_t* tfull = dfree + SD;    // [2]
+    uint64_t* tempty = tfull + 2;    // [2]
     uint64_t* tdone = tempty + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tdone + 1);
 
@@ -116,8 +124,12 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
         if (p.do_wg) tma_prefetch(&p.tmap_x);
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&ready[i], p.do_wg ? 8 : 4);  // builders (+ the epilogue's Xe)
-            mbar_init(&empty[i], 1);
+            mbar_init(&ready[i], 4);                // builder warps
+            mbar_init(&empty[i], p.do_wg ? 5 : 1);  // dgrad MMA commit (+ 4 builder warps: x tile read)
+        }
+        for (int i = 0; i < SD; ++i) {
+            mbar_init(&dready[i], 4);  // builder warps (K-major copy + Xe)
+            mbar_init(&dfree[i], 1);   // wgrad MMA commit
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
@@ -187,7 +199,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                 if (p.do_wg) {
                     // the box's first column must be 16-byte aligned: start xoff >= pW columns
                     // early (xoff % 4 == 0), the Xe builder skips xoff - pW
-                    uint8_t* xs = sb + p.sz_gyt + p.sz_gyk + p.sz_xe;
+                    uint8_t* xs = sb + p.sz_gyt;
                     tma_load_3d(xs, &p.tmap_x, &full[stage], jb * 32 - p.xoff, i0 - p.pH, n * p.C);
                     tma_load_3d(xs + p.xbox, &p.tmap_x, &full[stage], jb * 32 - p.xoff + 32, i0 - p.pH, n * p.C);
                 }
@@ -203,8 +215,8 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
         constexpr uint32_t kIdescWg = idesc_tf32(128, kPairs * 32, 0, 0);
         constexpr uint32_t kHiMN = desc_hi(512, kSwizzle128B_Base32B), kHiK = desc_hi(1024, kSwizzle128B);
         const uint32_t wt_lo = desc_lo(smem_u32(wt), 16);
-        int stage = 0, buf = 0;
-        uint32_t phase = 0, tphase = 0, wacc = 0;
+        int stage = 0, buf = 0, dstage = 0;
+        uint32_t phase = 0, tphase = 0, dphase = 0, wacc = 0;
         const int total = (hi - lo) * nstage_unit;
         for (int it = 0; it < total; ++it) {
             mbar_wait(&ready[stage], phase);
@@ -227,8 +239,16 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                     tphase ^= 1;
                 }
             }
+            mma_commit_warp(&empty[stage]);  // the gy tile is free once the dgrad MMAs are done
+            if (++stage == S) {
+                stage = 0;
+                phase ^= 1;
+            }
             if (p.do_wg) {
-                const uint32_t klo = desc_lo(sb + p.sz_gyt, 16), xlo = desc_lo(sb + p.sz_gyt + p.sz_gyk, 16);
+                mbar_wait(&dready[dstage], dphase);
+                tc_fence_after();
+                const uint32_t db = smem_u32(smem + p.d_off + (size_t)dstage * p.dstage_bytes);
+                const uint32_t klo = desc_lo(db, 16), xlo = desc_lo(db + p.sz_gyk, 16);
 #pragma unroll
                 for (int g = 0; g < kWgMmas; ++g) {
 #pragma unroll
@@ -241,11 +261,11 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                         wacc = 1;
                     }
                 }
-            }
-            mma_commit_warp(&empty[stage]);
-            if (++stage == S) {
-                stage = 0;
-                phase ^= 1;
+                mma_commit_warp(&dfree[dstage]);
+                if (++dstage == SD) {
+                    dstage = 0;
+                    dphase ^= 1;
+                }
             }
         }
         mma_commit_warp(tdone);
@@ -257,8 +277,25 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
 #pragma unroll
         for (int j = 0; j < kJ; ++j) bsum[j] = 0.f;
         const int chunk = (int)(lane & 7), kq = (int)(lane >> 3);
-        int stage = 0;
-        uint32_t phase = 0;
+        const int bt = (int)threadIdx.x - 64;
+        const int kWC = p.kW * p.C;
+        // Xe items of this thread (fixed per stage): 8 float4 per (t, n) row
+        constexpr int kXeIt = (kRowsB * 32 * 8 + 127) / 128;
+        int xs_row[kXeIt], xs_col[kXeIt], xs_dst[kXeIt], xs_t[kXeIt];
+        const int x_rows = kRowsB + p.kH - 1;
+#pragma unroll
+        for (int it = 0; it < kXeIt; ++it) {
+            const int e = bt + 128 * it;
+            const int qq = e & 7, tn = e >> 3;
+            const int t = tn / p.ntaps, nn = tn - t * p.ntaps;
+            const int r = nn / kWC, sc = nn - r * kWC, ss = sc / p.C, c = sc - ss * p.C;
+            xs_t[it] = e < kRowsB * p.ntaps * 8 ? t : -1;
+            xs_row[it] = (c * x_rows + t + r) * 128;
+            xs_col[it] = p.xoff - p.pW + qq * 4 + ss;
+            xs_dst[it] = (int)sw16((uint32_t)((t * 32 + nn) * 128 + qq * 16));
+        }
+        int stage = 0, dstage = 0;
+        uint32_t phase = 0, dphase = 0;
         for (int u = lo; u < hi; ++u) {
             const int n = u / p.nb, band = u - n * p.nb;
             const int i_start = band * p.B + p.pH - p.kH + 1;
@@ -269,8 +306,9 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                 for (int jb = 0; jb < p.jbs; ++jb) {
                     mbar_wait(&full[stage], phase);
                     uint8_t* sb = smem + (size_t)stage * p.stage_bytes;
-                    uint8_t* gyk = sb + p.sz_gyt;
-                    // gy tile: rows (t, k), 8 lanes per 128-byte row
+                    // gy tile: rows (t, k), 8 lanes per 128-byte row; the rounded values stay in
+                    // registers for the K-major copy, so the tile itself is done with here
+                    float4 rv[kRowsB][kJ];
 #pragma unroll
                     for (int t = 0; t < kRowsB; ++t) {
                         const bool own = i0 + t >= own_lo && i0 + t < own_hi;
@@ -285,12 +323,57 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                             v.z = rna(v.z);
                             v.w = rna(v.w);
                             if (p.do_dg) *reinterpret_cast<float4*>(sb + sw32(o)) = v;
-                            if (p.do_wg) *reinterpret_cast<float4*>(gyk + sw16(o)) = v;
+                            rv[t][j] = v;
                         }
                     }
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&ready[stage]);
+                    if (p.do_wg) {
+                        // the wgrad operands: the same gy rows K-major (16-byte-atom swizzle) and
+                        // Xe[t][n][px] = tf32(x[c][t + r][px + s]) from the x tile (two SW128
+                        // boxes [c][row][32 px]), zero for gy rows this band does not own
+                        mbar_wait(&dfree[dstage], dphase ^ 1);
+                        uint8_t* gyk = smem + p.d_off + (size_t)dstage * p.dstage_bytes;
+#pragma unroll
+                        for (int t = 0; t < kRowsB; ++t) {
+#pragma unroll
+                            for (int j = 0; j < kJ; ++j) {
+                                const int k = wb * kKPerWarp + j * 4 + kq;
+                                const uint32_t o = (uint32_t)((t * KP + k) * 128 + chunk * 16);
+                                *reinterpret_cast<float4*>(gyk + sw16(o)) = rv[t][j];
+                            }
+                        }
+                        const uint8_t* xt8 = sb + p.sz_gyt;
+                        uint8_t* xe = gyk + p.sz_gyk;
+#pragma unroll
+                        for (int it = 0; it < kXeIt; ++it) {
+                            if (xs_t[it] < 0) continue;
+                            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                            const int gi = i0 + xs_t[it];
+                            if (gi >= own_lo && gi < own_hi) {
+                                float e4[4];
+#pragma unroll
+                                for (int z = 0; z < 4; ++z) {
+                                    const int col = xs_col[it] + z;
+                                    const uint32_t o = (uint32_t)(xs_row[it] + (col & 31) * 4);
+                                    e4[z] = rna(*reinterpret_cast<const float*>(xt8 + (col >> 5) * p.xbox + sw16(o)));
+                                }
+                                v = make_float4(e4[0], e4[1], e4[2], e4[3]);
+                            }
+                            *reinterpret_cast<float4*>(xe + xs_dst[it]) = v;
+                        }
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) {
+                            mbar_arrive(&dready[dstage]);
+                            mbar_arrive(&empty[stage]);  // done with this stage's x tile
+                        }
+                        if (++dstage == SD) {
+                            dstage = 0;
+                            dphase ^= 1;
+                        }
+                    }
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -323,64 +406,12 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
         // gather cells of one stage: (c, gx row hr, gx col ur) over (4 + kH - 1) x (32 + kW - 1)
         const int g_rows = kRowsB + kH_ - 1, g_cols = 32 + kW_ - 1;
         const int g_cells = C_ * g_rows * g_cols;
-        // Xe items of this thread (fixed per stage): 8 float4 per (t, n) row
-        constexpr int kXeIt = (kRowsB * 32 * 8 + 127) / 128;
-        int xs_row[kXeIt], xs_col[kXeIt], xs_dst[kXeIt], xs_t[kXeIt];
-        const int x_rows = kRowsB + p.kH - 1;
-#pragma unroll
-        for (int it = 0; it < kXeIt; ++it) {
-            const int e = et + 128 * it;
-            const int qq = e & 7, tn = e >> 3;
-            const int t = tn / p.ntaps, nn = tn - t * p.ntaps;
-            const int r = nn / kWC, sc = nn - r * kWC, ss = sc / p.C, c = sc - ss * p.C;
-            xs_t[it] = e < kRowsB * p.ntaps * 8 ? t : -1;
-            xs_row[it] = (c * x_rows + t + r) * 128;
-            xs_col[it] = p.xoff - p.pW + qq * 4 + ss;
-            xs_dst[it] = (int)sw16((uint32_t)((t * 32 + nn) * 128 + qq * 16));
-        }
-        int xstage = 0;
-        uint32_t xphase = 0;
-        if (p.do_dg || p.do_wg) {
+        if (p.do_dg) {
             for (int u = lo; u < hi; ++u) {
                 const int n = u / p.nb, band = u - n * p.nb;
                 const int i_start = band * p.B + p.pH - p.kH + 1;
-                const int own_lo = max(0, i_start);
-                const int own_hi = band == p.nb - 1 ? p.oH : (band + 1) * p.B + p.pH - p.kH + 1;
                 for (int rs = 0; rs < p.rstages; ++rs) {
                     for (int jb = 0; jb < p.jbs; ++jb) {
-                        if (p.do_wg) {
-                            // Xe[t][n][px] = tf32(x[c][t + r][px + s]) from the x tile (two SW128
-                            // boxes [c][row][32 px]); zero for gy rows this band does not own
-                            mbar_wait(&full[xstage], xphase);
-                            uint8_t* sb = smem + (size_t)xstage * p.stage_bytes;
-                            const uint8_t* xt8 = sb + p.sz_gyt + p.sz_gyk + p.sz_xe;
-                            uint8_t* xe = sb + p.sz_gyt + p.sz_gyk;
-                            const int i0 = i_start + rs * kRowsB;
-#pragma unroll
-                            for (int it = 0; it < kXeIt; ++it) {
-                                if (xs_t[it] < 0) continue;
-                                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                                const int gi = i0 + xs_t[it];
-                                if (gi >= own_lo && gi < own_hi) {
-                                    float e4[4];
-#pragma unroll
-                                    for (int z = 0; z < 4; ++z) {
-                                        const int col = xs_col[it] + z;
-                                        const uint32_t o = (uint32_t)(xs_row[it] + (col & 31) * 4);
-                                        e4[z] = rna(*reinterpret_cast<const float*>(xt8 + (col >> 5) * p.xbox + sw16(o)));
-                                    }
-                                    v = make_float4(e4[0], e4[1], e4[2], e4[3]);
-                                }
-                                *reinterpret_cast<float4*>(xe + xs_dst[it]) = v;
-                            }
-                            fence_proxy_async();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&ready[xstage]);
-                            if (++xstage == S) {
-                                xstage = 0;
-                                xphase ^= 1;
-                            }
-                        }
                         if (!p.do_dg) continue;
                         mbar_wait(&tfull[buf], tphase);
                         tc_fence_after();
@@ -527,7 +558,8 @@ __global__ void scbwd_breduce_kernel(const float* __restrict__ part, float* __re
 
 struct SCPlan {
     bool ok = false;
-    int Kp, ntaps, B, nb, rstages, jbs, units, ctas, stages;
+    int Kp, ntaps, B, nb, rstages, jbs, units, ctas, stages, dstages;
+    uint32_t dstage_bytes, d_off;
     uint32_t xbox;
     uint32_t sz_gyt, sz_gyk, sz_xe, sz_x, stage_bytes, wt_off, ring_off, sd_off, bar_off;
     size_t smem;
@@ -547,7 +579,8 @@ SCPlan scplan(const Geo& g) {
     pl.sz_gyk = pl.sz_gyt;
     pl.sz_xe = (uint32_t)(kRowsB * 32 * 128);
     pl.sz_x = 2 * pl.xbox;
-    pl.stage_bytes = pl.sz_gyt + pl.sz_gyk + pl.sz_xe + pl.sz_x;
+    pl.stage_bytes = pl.sz_gyt + pl.sz_x;          // TMA ring stage
+    pl.dstage_bytes = pl.sz_gyk + pl.sz_xe;        // derived ring stage
     const uint32_t wt_bytes = (uint32_t)(pl.Kp * 128);
     const uint32_t sd_bytes = (uint32_t)align_up((size_t)kRowsB * pl.ntaps * 32 * 4, 1024);  // D staging
     const int sms = sm_count();
@@ -559,7 +592,8 @@ SCPlan scplan(const Geo& g) {
     auto fits = [&](int jj) {
         const int B = 4 * jj - (int)(g.kH - 1);
         const uint32_t ring_bytes = (uint32_t)align_up((size_t)g.C * B * g.W * 4, 1024);
-        return B >= 1 && (int)(wt_bytes + ring_bytes + sd_bytes + 1024 + 2 * pl.stage_bytes) + 1024 <= kSmemLimitB;
+        return B >= 1 && (int)(wt_bytes + ring_bytes + sd_bytes + 1024 + 2 * pl.stage_bytes + pl.dstage_bytes) + 1024 <=
+                             kSmemLimitB;
     };
     while (j > 1 && !fits(j)) --j;
     if (!fits(j)) return pl;
@@ -570,9 +604,12 @@ SCPlan scplan(const Geo& g) {
     pl.ctas = std::min(pl.units, sms);
     const uint32_t ring_bytes = (uint32_t)align_up((size_t)g.C * pl.B * g.W * 4, 1024);
     const int budget = kSmemLimitB - 1024 - (int)(wt_bytes + ring_bytes + sd_bytes + 1024);
-    pl.stages = std::min(4, budget / (int)pl.stage_bytes);
+    // the derived ring: 2 stages when 3 TMA stages still fit beside them, else 1
+    pl.dstages = budget >= (int)(3 * pl.stage_bytes + 2 * pl.dstage_bytes) ? 2 : 1;
+    pl.stages = std::min(6, (budget - pl.dstages * (int)pl.dstage_bytes) / (int)pl.stage_bytes);
     if (pl.stages < 2) return pl;
-    pl.wt_off = (uint32_t)pl.stages * pl.stage_bytes;
+    pl.d_off = (uint32_t)pl.stages * pl.stage_bytes;
+    pl.wt_off = pl.d_off + (uint32_t)pl.dstages * pl.dstage_bytes;
     pl.ring_off = pl.wt_off + wt_bytes;
     pl.sd_off = pl.ring_off + ring_bytes;
     pl.bar_off = pl.sd_off + sd_bytes;
@@ -649,6 +686,9 @@ void scbwd(const Geo& g, const float* x, const float* gy, const float* w, float*
     p.sz_xe = pl.sz_xe;
     p.sz_x = pl.sz_x;
     p.stage_bytes = pl.stage_bytes;
+    p.dstages = pl.dstages;
+    p.dstage_bytes = pl.dstage_bytes;
+    p.d_off = pl.d_off;
     p.wt_off = pl.wt_off;
     p.ring_off = pl.ring_off;
     p.sd_off = pl.sd_off;
