@@ -68,7 +68,28 @@ __global__ void s2d_input_nhwc_kernel(const float* __restrict__ x, float4* __res
         const int nb = Wt - (hi - lo), ca = e / nb, k = e - ca * nb;
         tile[ca * Wt + (k < lo ? k : k + (hi - lo))] = 0.f;
     }
-    if (vec_load) {  // W % 4 == 0 and x 16-byte aligned: float4 loads, several in flight
+    if (vec_load && W / 4 <= (int)blockDim.x) {
+        // one (c, a) row per threadIdx.y, one float4 per lane: no index division, all of a
+        // thread's loads issued before the first store
+        const int nq = W / 4, q = (int)threadIdx.x;
+#pragma unroll 4
+        for (int ca = threadIdx.y; ca < C * S; ca += blockDim.y) {
+            const int c = ca / S, a = ca - c * S;
+            const int h = S * I + a - pH;
+            if (q >= nq) continue;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (h >= 0 && h < H) v = __ldg(reinterpret_cast<const float4*>(x + (((int64_t)n * C + c) * H + h) * W) + q);
+            float* t = tile + ca * Wt + pW + 4 * q;
+            const int room = Wt - (pW + 4 * q);
+            if (room >= 4) {
+                t[0] = v.x; t[1] = v.y; t[2] = v.z; t[3] = v.w;
+            } else {
+                if (room > 0) t[0] = v.x;
+                if (room > 1) t[1] = v.y;
+                if (room > 2) t[2] = v.z;
+            }
+        }
+    } else if (vec_load) {  // W % 4 == 0 and x 16-byte aligned: float4 loads, several in flight
         const int nq = W / 4;
 #pragma unroll 4
         for (int e = tid; e < C * S * nq; e += nthr) {
@@ -103,6 +124,27 @@ __global__ void s2d_input_nhwc_kernel(const float* __restrict__ x, float4* __res
     __syncthreads();
     const int Cs = C * S * S, q4 = Cp / 4;
     float4* dst = xh + ((int64_t)n * Hs + I) * Ws * q4;
+    if (nthr % q4 == 0) {
+        // each thread always writes the same four channels: their tile offsets are decoded
+        // once (the per-element decode made this pass issue-bound: 49 M instructions for
+        // 127 MB, 2.3 TB/s)
+        const int ch0 = (tid % q4) * 4;
+        int off[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int ch = ch0 + u;
+            off[u] = ch < Cs ? (ch / S) * Wt + (ch % S) : -1;
+        }
+        const int jstep = nthr / q4;
+#pragma unroll 4
+        for (int J = tid / q4; J < Ws; J += jstep) {
+            float v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = off[u] >= 0 ? to_tf32_s2d(tile[off[u] + J * S]) : 0.f;
+            dst[(int64_t)J * q4 + (tid % q4)] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+        return;
+    }
     for (int e = tid; e < Ws * q4; e += nthr) {
         const int J = e / q4, ch0 = (e - J * q4) * 4;
         float v[4];
@@ -150,6 +192,31 @@ __global__ void d2s_grad_kernel(const float* __restrict__ gxs, float* __restrict
     for (int w = threadIdx.x; w < W; w += blockDim.x) {
         const int ww = w + pW, J = ww / S;
         dst[w] = (I < Hs && J < Ws) ? __ldg(src + (ww % S) * plane + J) : 0.f;
+    }
+}
+
+// Four consecutive w per thread (four independent phase-plane loads in flight, one float4
+// store): the one-element-per-thread form above ran latency-bound at ~1.6 TB/s.
+template <int S>
+__global__ void d2s_grad4_kernel(const float* __restrict__ gxs, float4* __restrict__ gx4, int rows, int C, int H,
+                                 int W, int pH, int pW, int Hs, int Ws) {
+    const int row = blockIdx.x * blockDim.y + threadIdx.y;  // (n, c, h)
+    if (row >= rows) return;
+    const int h = row % H;
+    const int c = (row / H) % C;
+    const int n = row / (H * C);
+    const int hh = h + pH, I = hh / S;
+    const int64_t plane = (int64_t)Hs * Ws;
+    const float* src = gxs + (((int64_t)n * C * S * S + (c * S + hh % S) * S) * Hs + I) * (int64_t)Ws;
+    float4* dst = gx4 + (int64_t)row * (W / 4);
+    for (int w4 = threadIdx.x; w4 < W / 4; w4 += blockDim.x) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int ww = 4 * w4 + u + pW, J = ww / S;
+            v[u] = (I < Hs && J < Ws) ? __ldg(src + (ww % S) * plane + J) : 0.f;
+        }
+        dst[w4] = make_float4(v[0], v[1], v[2], v[3]);
     }
 }
 
@@ -245,6 +312,21 @@ void d2s_grad(const Geo& g, const float* gxs, float* gx, cudaStream_t st) {
     const Geo e = s2d_geo(g);
     ProfScope prof("layout", st, 0.0, 4.0 * (g.N * g.C * g.HW * 2));
     const int rows = (int)(g.N * g.C * g.H);
+    if (g.W % 4 == 0 && (reinterpret_cast<uintptr_t>(gx) & 15) == 0) {
+        const int tx = g.W / 4 >= 64 ? 64 : 32;
+        const dim3 blk(tx, 256 / tx);
+#define PTB_D2S4(S_)                                                                                    \
+    d2s_grad4_kernel<S_><<<(unsigned)ceil_div(rows, (int)blk.y), blk, 0, st>>>(                       \
+        gxs, reinterpret_cast<float4*>(gx), rows, (int)g.C, (int)g.H, (int)g.W, (int)g.pH, (int)g.pW,   \
+        (int)e.H, (int)e.W)
+        if (g.sH == 2) PTB_D2S4(2);
+        else if (g.sH == 3) PTB_D2S4(3);
+        else if (g.sH == 4) PTB_D2S4(4);
+        else PTB_D2S4(8);
+#undef PTB_D2S4
+        after_launch("d2s_grad4");
+        return;
+    }
 #define PTB_D2S(S_)                                                                                    \
     d2s_grad_kernel<S_><<<(unsigned)ceil_div(rows, 2), dim3(128, 2), 0, st>>>(                         \
         gxs, gx, rows, (int)g.C, (int)g.H, (int)g.W, (int)g.pH, (int)g.pW, (int)e.H, (int)e.W)

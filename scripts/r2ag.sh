@@ -1,5 +1,5 @@
 #!/bin/bash
-O=gpurun_out/r2ah; mkdir -p $O
+O=gpurun_out/r2aj; mkdir -p $O
 for m in dgrad wgrad both; do CUDA_LAUNCH_BLOCKING=1 timeout 60 python tests/scbwd_debug.py $m > $O/$m.txt 2>&1; echo "rc=$?" >> $O/$m.txt; done
 CUDA_LAUNCH_BLOCKING=1 timeout 60 python tests/scbwd_debug.py both big > $O/bothbig.txt 2>&1; echo "rc=$?" >> $O/bothbig.txt
 timeout 900 python -m pytest tests/test_gpu_engines.py tests/test_gpu_fullsize.py tests/test_gpu_workloads.py tests/test_gpu_conv.py tests/test_gpu_dp.py -q -rf -x -k "default or scbwd or vgga or cfg1 or spec" > $O/tests.txt 2>&1; echo "rc=$?" >> $O/tests.txt
