@@ -1,7 +1,8 @@
 """Randomised channel-rich geometries through the default tensor-core engines vs the oracle
 (fwd / dgrad / wgrad / gradBias): bitwise on TF32-exact inputs, elementwise TF32 bounds on
 real-valued ones (tests/engine_check.py). Stress companion of test_gpu_conv.py:
-  python tests/stress_tc.py [count] [seed] [wide]
+  python tests/stress_tc.py [count] [seed] [wide|smallc]
+smallc: stride-1 layers with C*kH*kW <= 32 and K <= 64 (the fused small-C backward).
 """
 import os
 import sys
@@ -14,7 +15,31 @@ import numpy as np  # noqa: E402
 import pyoracle as po  # noqa: E402
 
 
+def smallc_geometries(n, seed):
+    """Fused small-C backward candidates: W, oW multiples of 4 (TMA row strides), odd
+    heights, K padded 32 / 64, rectangular filters, pads 0..k-1."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        C = int(rng.integers(1, 5))
+        kh, kw = int(rng.choice([1, 2, 3, 5])), int(rng.choice([1, 3, 5]))
+        if C * kh * kw > 32:
+            continue
+        K = int(rng.choice([4, 16, 24, 32, 40, 48, 64]))
+        ph, pw = int(rng.integers(0, kh)), int(rng.integers(0, kw))
+        W = 4 * int(rng.integers(2, 20))
+        if (W + 2 * pw - kw + 1) % 4:
+            continue
+        H, N = int(rng.integers(kh, 40)), int(rng.integers(1, 4))
+        g = po.geom(N, C, H, W, K, kh, kw, ph, pw, 1, 1)
+        if po.oracle().or_validate(g) == 0:
+            out.append(g)
+    return out
+
+
 def tc_random_geometries(n, seed, wide=False):
+    if wide == "smallc":
+        return smallc_geometries(n, seed)
     rng = np.random.default_rng(seed)
     out = []
     while len(out) < n:
@@ -55,7 +80,7 @@ def run(n=40, seed=7, wide=False):
 if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 7
-    wide = len(sys.argv) > 3 and sys.argv[3] == "wide"
+    wide = sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] in ("wide", "smallc") else False
     worst, bad = run(n, seed, wide)
     print(f"{n} geometries, worst normwise error {worst:.3e}, failures {len(bad)}")
     for g, e in bad:
