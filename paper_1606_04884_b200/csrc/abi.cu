@@ -78,8 +78,6 @@ size_t fwd_ws(const Geo& g, int math) {
     }
     return 0;
 }
-// small-C stride-1 dgrad with a wide filter: gradCol GEMM + in-SM fold from NCHW gy
-bool dgrad_gfold(const Geo& g, int math) { return math == PT_MATH_TF32 && gfold_ok(g); }
 // small-C stride-1 dgrad: tconv of the row-expanded (kH x 1) layer + 1-D fold
 bool dgrad_row(const Geo& g, int math) {
     static const bool off = std::getenv("PT_B200_NO_ROWCONV") != nullptr;
@@ -87,7 +85,6 @@ bool dgrad_row(const Geo& g, int math) {
 }
 size_t bwd_data_ws(const Geo& g, int math) {
     if (sc_on(g, math)) return scbwd_workspace(g);
-    if (dgrad_gfold(g, math)) return gfold_workspace(g);
     if (dgrad_row(g, math)) return rowdgrad_workspace(g);
     if (math == PT_MATH_TF32) {
         const UmmaPlan pl = umma_plan(g, true);
@@ -102,10 +99,6 @@ void bwd_data_impl(const Geo& g, const float* gy, const float* w, float* gx, int
     PassScope pass("dgrad");
     if (sc_on(g, math)) {
         scbwd(g, nullptr, gy, w, gx, nullptr, nullptr, 1.f, 0, 1.f, 0, ws, st);
-        return;
-    }
-    if (dgrad_gfold(g, math)) {
-        gfold(g, gy, w, gx, ws, st);
         return;
     }
     if (dgrad_row(g, math)) {

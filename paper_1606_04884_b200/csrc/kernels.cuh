@@ -181,11 +181,6 @@ size_t swgrad_workspace(const Geo& g);
 void swgrad(const Geo& g, const float* x, const float* gyh, float* gw, float scale, int accumulate, void* ws,
             cudaStream_t st);
 
-// ---- umma_gfold.cu: small-C stride-1 input gradient from NCHW gy (gradCol GEMM + in-SM fold) ----
-bool gfold_ok(const Geo& g);
-size_t gfold_workspace(const Geo& g);
-void gfold(const Geo& g, const float* gy, const float* w, float* gx, void* ws, cudaStream_t st);
-
 // ---- umma_scbwd.cu: fused backward of small-C stride-1 layers (C*kH*kW <= 32, K <= 64) ----
 // One NCHW gy read feeds gradInput (gcol GEMM + in-smem fold), gradWeight and gradBias;
 // gx / gw may be null (that product skipped); gb only with gw. gw takes (scale, accumulate),

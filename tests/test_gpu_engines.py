@@ -54,10 +54,9 @@ CONFIGS = {
     "hwgrad-forced": {"PT_B200_HWGRAD": "2"},
     "hwgrad-off": {"PT_B200_HWGRAD": "0"},
     "swgrad-off": {"PT_B200_SWGRAD": "0"},
-    "no-rowconv": {"PT_B200_NO_ROWCONV": "1", "PT_B200_GFOLD": "0"},
+    "no-rowconv": {"PT_B200_NO_ROWCONV": "1"},
     "no-s2d": {"PT_B200_NO_S2D": "1"},
-    "rowdgrad-horizontal": {"PT_B200_ROWDGRAD": "0", "PT_B200_GFOLD": "0"},
-    "gfold-off": {"PT_B200_GFOLD": "0"},
+    "rowdgrad-horizontal": {"PT_B200_ROWDGRAD": "0"},
     "rowconv-epi4": {"PT_B200_ROWCONV_EPI": "4"},
     "serial-bwd": {"PT_B200_BWD_STREAMS": "0"},
     "scbwd-off": {"PT_B200_SCBWD": "0"},
@@ -71,18 +70,16 @@ def _extra(cfg):
         return HANKEL_EDGE
     if cfg.startswith("hwgrad"):
         return HWGRAD_EDGE
-    if cfg in ("swgrad-off", "no-rowconv", "rowdgrad-horizontal", "rowconv-epi4", "gfold-off"):
+    if cfg in ("swgrad-off", "no-rowconv", "rowdgrad-horizontal", "rowconv-epi4"):
         return SMALLC_GEOMS
     if cfg == "default":
-        return GFOLD_EDGE
+        return SMALLC_EDGE
     return []
 
 
-# the small-C gradCol + fold dgrad (umma_gfold.cu): odd batch (the pair's spare CTA),
-# several bands (spill + fixup), borders, C = 1 / 2 / 4, K not a multiple of 16, kH = 2 / 13,
-# rows not 16-byte aligned (oW % 4 != 0), rows of several 128-pixel segments, 1 / 2 / 3
-# column chunks
-GFOLD_EDGE = [
+# more small-C stride-1 shapes through the default engines: odd batch, borders, C = 1 / 2 / 4,
+# K not a multiple of 16, kH = 2 / 13, rows not 16-byte aligned (oW % 4 != 0), wide rows
+SMALLC_EDGE = [
     po.geom(3, 3, 40, 40, 96, 11, 11, 0, 0, 1, 1),
     po.geom(1, 1, 50, 37, 40, 9, 7, 3, 2, 1, 1),
     po.geom(2, 2, 33, 100, 64, 5, 13, 2, 6, 1, 1),
