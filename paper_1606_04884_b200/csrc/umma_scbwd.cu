@@ -27,7 +27,8 @@
 // row is OWNED by one band for wgrad / gradBias (halo rows are masked out of Xe and the bias).
 // B + kH - 1 is a multiple of 4 (the dgrad MMA's M = 4 rows x 32 px).
 //
-// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..5 builders, 6..9 epilogue (fold +
+// Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..5 rounding (+ gradBias), 6..9 wgrad
+// operands (K-major copy, Xe), 10..13 epilogue (fold +
 // gx band flush; at the end the wgrad accumulator drain). TMEM: two 32-column dgrad
 // accumulators (double-buffered) and the wgrad accumulator (128/Kp row groups x 32 columns:
 // one MMA covers 128/Kp gy rows with M = rows x Kp, B = their Xe blocks side by side; only
@@ -47,7 +48,7 @@ namespace {
 
 using namespace umma;
 
-constexpr int kThreadsB = 320;
+constexpr int kThreadsB = 448;  // TMA, MMA, 4 rounding, 4 wgrad-operand, 4 epilogue warps
 constexpr int kSmemLimitB = 232448;
 constexpr int kRowsB = 4;  // gy rows per stage = the dgrad M block (4 x 32 px)
 
@@ -125,10 +126,10 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
         for (int i = 0; i < S; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&ready[i], 4);                // builder warps
-            mbar_init(&empty[i], p.do_wg ? 5 : 1);  // dgrad MMA commit (+ 4 builder warps: x tile read)
+            mbar_init(&empty[i], p.do_wg ? 9 : 1);  // dgrad MMA commit (+ 8 builder warps: tile reads)
         }
         for (int i = 0; i < SD; ++i) {
-            mbar_init(&dready[i], 4);  // builder warps (K-major copy + Xe)
+            mbar_init(&dready[i], 8);  // builder warps (K-major copy; Xe)
             mbar_init(&dfree[i], 1);   // wgrad MMA commit
         }
         for (int i = 0; i < 2; ++i) {
@@ -154,8 +155,8 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
         }
         fence_proxy_async();
     }
-    if (warp >= 6) {
-        const int et = (int)threadIdx.x - 192;
+    if (warp >= 10) {
+        const int et = (int)threadIdx.x - 320;
         const int ring_n = p.C * p.B * p.W;
         for (int e = et; e < ring_n; e += 128) ring[e] = 0.f;
     }
@@ -270,30 +271,14 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
         }
         mma_commit_warp(tdone);
     } else if (warp < 6) {
-        // ===== builders: TF32 rounding, the K-major copy, gradBias, Xe =====
+        // ===== rounding warps: the gy tile to TF32 in place (the dgrad operand, and the
+        // source of the wgrad operands), gradBias from the unrounded values =====
         const int wb = (int)warp - 2;
         constexpr int kKPerWarp = KP / 4, kJ = KP / 16;  // k values per warp; per thread
         float bsum[kJ];
 #pragma unroll
         for (int j = 0; j < kJ; ++j) bsum[j] = 0.f;
         const int chunk = (int)(lane & 7), kq = (int)(lane >> 3);
-        const int bt = (int)threadIdx.x - 64;
-        const int kWC = p.kW * p.C;
-        // Xe items of this thread (fixed per stage): 8 float4 per (t, n) row
-        constexpr int kXeIt = (kRowsB * 32 * 8 + 127) / 128;
-        int xs_row[kXeIt], xs_col[kXeIt], xs_dst[kXeIt], xs_t[kXeIt];
-        const int x_rows = kRowsB + p.kH - 1;
-#pragma unroll
-        for (int it = 0; it < kXeIt; ++it) {
-            const int e = bt + 128 * it;
-            const int qq = e & 7, tn = e >> 3;
-            const int t = tn / p.ntaps, nn = tn - t * p.ntaps;
-            const int r = nn / kWC, sc = nn - r * kWC, ss = sc / p.C, c = sc - ss * p.C;
-            xs_t[it] = e < kRowsB * p.ntaps * 8 ? t : -1;
-            xs_row[it] = (c * x_rows + t + r) * 128;
-            xs_col[it] = p.xoff - p.pW + qq * 4 + ss;
-            xs_dst[it] = (int)sw16((uint32_t)((t * 32 + nn) * 128 + qq * 16));
-        }
         int stage = 0, dstage = 0;
         uint32_t phase = 0, dphase = 0;
         for (int u = lo; u < hi; ++u) {
@@ -306,44 +291,112 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                 for (int jb = 0; jb < p.jbs; ++jb) {
                     mbar_wait(&full[stage], phase);
                     uint8_t* sb = smem + (size_t)stage * p.stage_bytes;
-                    // gy tile: rows (t, k), 8 lanes per 128-byte row; the rounded values stay in
-                    // registers for the K-major copy, so the tile itself is done with here
-                    float4 rv[kRowsB][kJ];
+                    // rows (t, k), 8 lanes per 128-byte row; two rows at a time (loads first)
+                    // one pass when the wgrad operands are wanted: the K-major copy is written
+                    // from the same registers (the derived slot must be free first, so the dgrad
+                    // operand waits for the previous stage's wgrad MMA); otherwise round only
+                    uint8_t* gyk = nullptr;
+                    if (p.do_wg) {
+                        mbar_wait(&dfree[dstage], dphase ^ 1);
+                        gyk = smem + p.d_off + (size_t)dstage * p.dstage_bytes;
+                    }
 #pragma unroll
-                    for (int t = 0; t < kRowsB; ++t) {
-                        const bool own = i0 + t >= own_lo && i0 + t < own_hi;
+                    for (int th = 0; th < kRowsB; th += 2) {
+                        float4 rv[2][kJ];
 #pragma unroll
-                        for (int j = 0; j < kJ; ++j) {
-                            const int k = wb * kKPerWarp + j * 4 + kq;
-                            const uint32_t o = (uint32_t)((t * KP + k) * 128 + chunk * 16);
-                            float4 v = *reinterpret_cast<const float4*>(sb + sw32(o));
-                            if (p.do_bias && own) bsum[j] += (v.x + v.y) + (v.z + v.w);
-                            v.x = rna(v.x);
-                            v.y = rna(v.y);
-                            v.z = rna(v.z);
-                            v.w = rna(v.w);
-                            if (p.do_dg) *reinterpret_cast<float4*>(sb + sw32(o)) = v;
-                            rv[t][j] = v;
+                        for (int t = 0; t < 2; ++t)
+#pragma unroll
+                            for (int j = 0; j < kJ; ++j) {
+                                const int k = wb * kKPerWarp + j * 4 + kq;
+                                const uint32_t o = (uint32_t)(((th + t) * KP + k) * 128 + chunk * 16);
+                                rv[t][j] = *reinterpret_cast<const float4*>(sb + sw32(o));
+                            }
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {
+                            const bool own = i0 + th + t >= own_lo && i0 + th + t < own_hi;
+#pragma unroll
+                            for (int j = 0; j < kJ; ++j) {
+                                const int k = wb * kKPerWarp + j * 4 + kq;
+                                const uint32_t o = (uint32_t)(((th + t) * KP + k) * 128 + chunk * 16);
+                                float4 v = rv[t][j];
+                                if (p.do_bias && own) bsum[j] += (v.x + v.y) + (v.z + v.w);
+                                v.x = rna(v.x);
+                                v.y = rna(v.y);
+                                v.z = rna(v.z);
+                                v.w = rna(v.w);
+                                if (p.do_dg) *reinterpret_cast<float4*>(sb + sw32(o)) = v;
+                                if (gyk) *reinterpret_cast<float4*>(gyk + sw16(o)) = v;
+                            }
                         }
                     }
                     fence_proxy_async();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&ready[stage]);
-                    if (p.do_wg) {
-                        // the wgrad operands: the same gy rows K-major (16-byte-atom swizzle) and
-                        // Xe[t][n][px] = tf32(x[c][t + r][px + s]) from the x tile (two SW128
-                        // boxes [c][row][32 px]), zero for gy rows this band does not own
-                        mbar_wait(&dfree[dstage], dphase ^ 1);
-                        uint8_t* gyk = smem + p.d_off + (size_t)dstage * p.dstage_bytes;
-#pragma unroll
-                        for (int t = 0; t < kRowsB; ++t) {
-#pragma unroll
-                            for (int j = 0; j < kJ; ++j) {
-                                const int k = wb * kKPerWarp + j * 4 + kq;
-                                const uint32_t o = (uint32_t)((t * KP + k) * 128 + chunk * 16);
-                                *reinterpret_cast<float4*>(gyk + sw16(o)) = rv[t][j];
-                            }
+                    if (lane == 0) {
+                        mbar_arrive(&ready[stage]);
+                        if (gyk) {
+                            mbar_arrive(&dready[dstage]);
+                            mbar_arrive(&empty[stage]);
                         }
+                    }
+                    if (p.do_wg && ++dstage == SD) {
+                        dstage = 0;
+                        dphase ^= 1;
+                    }
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        if (p.do_bias) {
+            // fixed-order reduce over the 8 lanes sharing k, then one write per k
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+                float v = bsum[j];
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                const int k = wb * kKPerWarp + j * 4 + kq;
+                if (chunk == 0 && k < p.K) p.part_b[(int64_t)k * gridDim.x + b] = v;
+            }
+        }
+    } else if (warp < 10) {
+        // ===== Xe warps: Xe[t][n][px] = tf32(x[c][t + r][px + s]) from the x tile (two SW128
+        // boxes [c][row][32 px]), zero for gy rows this band does not own =====
+        if (!p.do_wg) {
+        } else {
+            const int bt = (int)threadIdx.x - 192;
+            const int kWC = p.kW * p.C;
+            // Xe items of this thread (fixed per stage): 8 float4 per (t, n) row
+            constexpr int kXeIt = (kRowsB * 32 * 8 + 127) / 128;
+            int xs_row[kXeIt], xs_col[kXeIt], xs_dst[kXeIt], xs_t[kXeIt];
+            const int x_rows = kRowsB + p.kH - 1;
+#pragma unroll
+            for (int it = 0; it < kXeIt; ++it) {
+                const int e = bt + 128 * it;
+                const int qq = e & 7, tn = e >> 3;
+                const int t = tn / p.ntaps, nn = tn - t * p.ntaps;
+                const int r = nn / kWC, sc = nn - r * kWC, ss = sc / p.C, c = sc - ss * p.C;
+                xs_t[it] = e < kRowsB * p.ntaps * 8 ? t : -1;
+                xs_row[it] = (c * x_rows + t + r) * 128;
+                xs_col[it] = p.xoff - p.pW + qq * 4 + ss;
+                xs_dst[it] = (int)sw16((uint32_t)((t * 32 + nn) * 128 + qq * 16));
+            }
+            int stage = 0, dstage = 0;
+            uint32_t phase = 0, dphase = 0;
+            for (int u = lo; u < hi; ++u) {
+                const int n = u / p.nb, band = u - n * p.nb;
+                const int i_start = band * p.B + p.pH - p.kH + 1;
+                const int own_lo = max(0, band * p.B + p.pH - p.kH + 1);
+                const int own_hi = band == p.nb - 1 ? p.oH : (band + 1) * p.B + p.pH - p.kH + 1;
+                for (int rs = 0; rs < p.rstages; ++rs) {
+                    const int i0 = i_start + rs * kRowsB;
+                    for (int jb = 0; jb < p.jbs; ++jb) {
+                        mbar_wait(&full[stage], phase);  // the x tile has landed
+                        mbar_wait(&dfree[dstage], dphase ^ 1);
+                        const uint8_t* sb = smem + (size_t)stage * p.stage_bytes;
+                        uint8_t* gyk = smem + p.d_off + (size_t)dstage * p.dstage_bytes;
                         const uint8_t* xt8 = sb + p.sz_gyt;
                         uint8_t* xe = gyk + p.sz_gyk;
 #pragma unroll
@@ -373,30 +426,18 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                             dstage = 0;
                             dphase ^= 1;
                         }
-                    }
-                    if (++stage == S) {
-                        stage = 0;
-                        phase ^= 1;
+                            if (++stage == S) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
                 }
-            }
-        }
-        if (p.do_bias) {
-            // fixed-order reduce over the 8 lanes sharing k, then one write per k
-#pragma unroll
-            for (int j = 0; j < kJ; ++j) {
-                float v = bsum[j];
-                v += __shfl_xor_sync(0xffffffffu, v, 1);
-                v += __shfl_xor_sync(0xffffffffu, v, 2);
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                const int k = wb * kKPerWarp + j * 4 + kq;
-                if (chunk == 0 && k < p.K) p.part_b[(int64_t)k * gridDim.x + b] = v;
             }
         }
     } else {
         // ===== epilogue: dgrad fold into the band's gx rows, band flush, wgrad drain =====
         const uint32_t q = warp & 3;  // TMEM lane quarter = gy row t of the stage
-        const int et = (int)threadIdx.x - 192;
+        const int et = (int)threadIdx.x - 320;
         int buf = 0;
         uint32_t tphase = 0;
         const int ring_rows = p.B;
@@ -699,6 +740,7 @@ void scbwd(const Geo& g, const float* x, const float* gy, const float* w, float*
     p.xbox = pl.xbox;
     p.xoff = (int)(g.pW + 3) / 4 * 4;
     p.tx = pl.sz_gyt + (gw ? (uint32_t)(2 * (kRowsB + g.kH - 1) * g.C * 128) : 0u);
+
     if (gx && !w) fail_validation("scbwd: gradInput needs the weight");
     if (!gx) p.w = nullptr;
     once_per_device((const void*)umma_scbwd_kernel<32, 0>, [&] {
