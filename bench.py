@@ -332,7 +332,7 @@ class Workload:
         for i, s in enumerate(self.st):
             if self.graphs is None or eager:
                 self.layer(s)
-            else:
+            elif self.graphs[i] is not None:
                 self.graphs[i].replay()
             # batch-sharded DP: one allreduce(sum) of this layer's gradW||gradB bucket on the
             # comm stream, overlapping the next layer's kernels
@@ -341,11 +341,12 @@ class Workload:
             if ev is not None:
                 cur.wait_event(ev)
 
-    def capture(self):
+    def capture(self, one_graph=False):
         """Each layer's forward + combined backward (internal streams included) captured
         once as a CUDA graph on a side stream whose workspace is warmed (allocated) first,
         so nothing allocates during capture; the allreduce stays an eager NCCL call between
-        the replays, so every N runs the same kernels the same way."""
+        the replays, so every N runs the same kernels the same way. one_graph (one rank, no
+        allreduce): all layers in one graph."""
         torch, pt = self.torch, self.pt
         cur = torch.cuda.current_stream()
         side = torch.cuda.Stream(device=self.dev)
@@ -356,7 +357,16 @@ class Workload:
         side.synchronize()
         graphs = []
         c0 = pt.launch_count()
-        for s in self.st:
+        if one_graph:
+            # one rank: no allreduce between the layers, so the whole step is one graph (the
+            # same kernels; 1-2 % faster than one replay per layer, BENCH_ONE_GRAPH A/B)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=side, capture_error_mode="thread_local"):
+                for s in self.st:
+                    self.layer(s)
+            graphs = [gr] + [None] * (len(self.st) - 1)
+        else:
+          for s in self.st:
             gr = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gr, stream=side, capture_error_mode="thread_local"):
                 self.layer(s)
@@ -429,7 +439,7 @@ def main():
     graph = None
     if not args.no_graph:
         try:
-            wl.capture()
+            wl.capture(one_graph=world == 1 and os.environ.get("BENCH_ONE_GRAPH", "1") != "0")
             for _ in range(2):
                 wl.step(comm)
             torch.cuda.synchronize()
@@ -534,7 +544,9 @@ def main():
                    "parallelism": f"dp{world}", "math": args.math,
                    "sharding": "fixed global batch split over the ranks (dp.shard_range); "
                                "gradWeight||gradBias all-reduced per layer (NCCL)",
-                   "launch": "one CUDA-graph replay per layer (fwd + bwd), allreduce eager" if graph is not None else "eager",
+                   "launch": ("eager" if graph is None else
+                              "one CUDA-graph replay per step (all layers fwd + bwd; one rank)" if graph[-1] is None
+                              else "one CUDA-graph replay per layer (fwd + bwd), allreduce eager"),
                    "l2": "no flush: per-step working set "
                          f"{wl.bytes_working_set() / 1e9:.2f} GB > 126 MB L2"},
         "clocks": clk, "gpu_launches": launches, "roofline": roof,
@@ -574,14 +586,15 @@ def main():
 
 def alexnet_ms_per_batch(args, pt, torch, dist, dev, rank, world):
     """AlexNet conv stack fwd+bwd, global batch 128 sharded over the ranks, CUDA-graph
-    replay per layer, allreduce per layer: device ms per global batch (max over ranks)."""
+    replay per layer (per step on one rank), allreduce per layer: device ms per global batch
+    (max over ranks)."""
     glayers = WORKLOADS["alexnet"]
     layers = local_layers(glayers, rank, world)
     wl = Workload(pt, torch, layers, dev, rank, args.math)
     comm = torch.cuda.Stream(device=dev) if world > 1 else None
     for _ in range(3):
         wl.step(comm)
-    wl.capture()
+    wl.capture(one_graph=world == 1 and os.environ.get("BENCH_ONE_GRAPH", "1") != "0")
     for _ in range(2):
         wl.step(comm)
     steps = max(args.steps, 10)
