@@ -299,11 +299,14 @@ void bwd_core(const Geo& g, const float* x, const float* gy, const float* w, flo
             PassScope pass("bwd");
             ProfScope prof("layout", st, 0.0, 4.0 * (g.M * g.K + g.M * umma_wgrad_kp(g)));
             nchw_to_nhwc_bias(gy, gyh, g.N, g.K, g.oHW, umma_wgrad_kp(g), gb, scale, accumulate, part,
-                              st);
+                              st, /*defer_bias=*/true);
         }
         Fork fk(st, 0);  // fork: the weight gradient waits for the gy transform only
         if (inner_gw_plain) wgrad_tc_run(g, x, gy, gyh, gw, 1.f, 0, math, wws, fk.side, finput, fph, fpw);
         else wgrad_tc_run(g, x, gy, gyh, gw, scale, accumulate, math, wws, fk.side, finput, fph, fpw);
+        // gradBias from the transform's partials, behind the weight gradient on the side
+        // stream: off the input gradient's path
+        if (gb) bias_from_nhwc_partials(part, g.N, g.K, g.oHW, gb, scale, accumulate, fk.side);
         bwd_data_impl(g, gy, w, gx, math, dws, st, gyh);
         fk.join();  // the caller's stream sees both gradients
         return;

@@ -48,8 +48,13 @@ struct NhwcDst {
 void nchw_to_nhwc_padded(const float* src, const NhwcDst& d0, const NhwcDst& d1, int64_t N,
                          int64_t C, int64_t H, int64_t W, int64_t Cp, float* gb, float scale,
                          int accumulate, float* part, cudaStream_t st);
+// defer_bias: the partials are written but the gradBias reduce is left to the caller
+// (bias_from_nhwc_partials, e.g. on another stream ordered after this one)
 void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
-                       float* gb, float scale, int accumulate, float* part, cudaStream_t st);
+                       float* gb, float scale, int accumulate, float* part, cudaStream_t st,
+                       bool defer_bias = false);
+void bias_from_nhwc_partials(const float* part, int64_t N, int64_t C, int64_t HW, float* gb, float scale,
+                             int accumulate, cudaStream_t st);
 // Weight packing for the implicit GEMM B operand. W is KCRS [K][C][kH][kW].
 //  kPackFprop     : row n = k,         tap (r,s),           channel = c  (cin = C)
 //  kPackDgradFlip : row n = c,         tap (kH-1-r,kW-1-s), channel = k  (cin = K)

@@ -309,18 +309,21 @@ size_t nhwc_bias_partials_bytes(int64_t N, int64_t C, int64_t HW) {
 }
 
 void nchw_to_nhwc_bias(const float* src, float* dst, int64_t N, int64_t C, int64_t HW, int64_t Cp,
-                       float* gb, float scale, int accumulate, float* part, cudaStream_t st) {
+                       float* gb, float scale, int accumulate, float* part, cudaStream_t st, bool defer_bias) {
     PTB_REQUIRE(N <= 65535 && Cp >= C, "nchw_to_nhwc_bias: bad shape");
     const int64_t strips = ceil_div(HW, kStripPx);
     dim3 grid((unsigned)strips, (unsigned)ceil_div(Cp, 32), (unsigned)N);
     nchw_to_nhwc_kernel<false, false><<<grid, dim3(32, 8), 0, st>>>(src, NhwcDst::dense(dst, HW), NhwcDst{},
                                                                      C, HW, Cp, 1, gb ? part : nullptr);
     after_launch("nchw_to_nhwc_bias");
-    if (gb) {
-        bias_from_partials_kernel<<<(unsigned)C, 1024, 0, st>>>(part, N * strips, C, gb, scale,
-                                                               accumulate);
-        after_launch("bias_from_partials");
-    }
+    if (gb && !defer_bias) bias_from_nhwc_partials(part, N, C, HW, gb, scale, accumulate, st);
+}
+
+void bias_from_nhwc_partials(const float* part, int64_t N, int64_t C, int64_t HW, float* gb, float scale,
+                             int accumulate, cudaStream_t st) {
+    bias_from_partials_kernel<<<(unsigned)C, 1024, 0, st>>>(part, N * ceil_div(HW, kStripPx), C, gb, scale,
+                                                           accumulate);
+    after_launch("bias_from_partials");
 }
 
 void pack_weights(const float* w, float* dst, int64_t K, int64_t C, int64_t kH, int64_t kW,
