@@ -435,7 +435,7 @@ def main():
     peaks, peak_kind = load_peaks()
     clocks = ClockSampler(local)
     L.lib().pt_b200_profile_enable(0)
-    L.lib().pt_b200_set_bwd_streams(1)
+    L.lib().pt_b200_set_bwd_streams(int(os.environ.get("BENCH_BWD_STREAMS", "1")))
     graph = None
     if not args.no_graph:
         try:

@@ -81,7 +81,7 @@ std::atomic<int> g_conc{-1};  // -1: PT_B200_BWD_STREAMS (default on)
 bool concurrency_on() {
     static const bool env_on = [] {
         const char* e = std::getenv("PT_B200_BWD_STREAMS");
-        return e ? std::atoi(e) != 1 : true;
+        return e ? std::atoi(e) != 0 : true;  // PT_B200_BWD_STREAMS=0: serial
     }();
     const int v = g_conc.load(std::memory_order_relaxed);
     return v < 0 ? env_on : v != 0;
