@@ -2,7 +2,7 @@
 # compute-sanitizer memcheck / synccheck / racecheck over one small geometry per engine
 # (tests/engine_check.py: exact + real-valued runs, finput + combined backward + separate
 # passes). Output: gpurun_out/sanitize_<tool>_<cfg>.txt
-G='[[2,3,20,20,32,5,5,2,2,1,1],[1,3,35,35,64,11,11,2,2,4,4],[2,64,12,12,64,3,3,1,1,1,1],[1,32,14,14,64,9,9,0,0,1,1],[1,32,9,9,32,3,3,1,1,2,2],[2,3,18,18,16,3,3,1,1,1,1]]'
+G='[[2,3,20,20,32,3,3,1,1,1,1],[1,1,20,40,48,5,5,2,2,1,1],[2,3,20,20,32,5,5,2,2,1,1],[1,3,35,35,64,11,11,2,2,4,4],[2,64,12,12,64,3,3,1,1,1,1],[1,32,14,14,64,9,9,0,0,1,1],[1,32,9,9,32,3,3,1,1,2,2],[2,3,18,18,16,3,3,1,1,1,1]]'
 run() {  # tool cfg env...
   local tool=$1 cfg=$2; shift 2
   env "$@" timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
