@@ -5,6 +5,8 @@
   captured with torch.cuda.graph and replayed gives bitwise the eager results, also after
   the static inputs are overwritten in place. This is what a caller needs to replace a
   launch-bound inner loop by one graph launch.
+* A multi-layer step (several layers' forward + backward, as bench.py's one-rank step)
+  captured as ONE graph replays bitwise to the eager results.
 * The in-call concurrency switch (pt_b200_set_bwd_streams) never changes results.
 * Two host threads driving the library on two streams at once get their own results.
 """
@@ -92,6 +94,29 @@ def test_graph_capture_replay_bitwise(t):
     torch.cuda.synchronize()
     for name, e, o in zip(("y", "gx", "gw", "gb"), eager2, out):
         assert torch.equal(e, o), f"{name}: replay after an input update differs"
+
+
+def test_multi_layer_step_one_graph_bitwise():
+    layers = []
+    for i, t in enumerate(GEOMS):
+        G = _geom(t)
+        layers.append((G, *_inputs(t, 100 + i), _finput(G)))
+    eager = [[r.clone() for r in _step(*L)] for L in layers]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # the capture stream's workspace and plans, before capture
+        for L in layers:
+            _step(*L)
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        outs = [_step(*L) for L in layers]
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    for t, e, o in zip(GEOMS, eager, outs):
+        for name, a, b in zip(("y", "gx", "gw", "gb"), e, o):
+            assert torch.equal(a, b), f"{t} {name}: one-graph step differs from eager"
 
 
 @pytest.mark.parametrize("t", GEOMS[:2], ids=lambda t: "x".join(map(str, t)))
