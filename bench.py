@@ -229,6 +229,18 @@ def cpu_sample_run(layers, batch, threads):
     return t, fl
 
 
+def cpu_model():
+    """The host CPU model (/proc/cpuinfo), recorded beside the CPU baseline's core count."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(layers, budget_s):
     threads = os.cpu_count() or 1
     t1, f1 = cpu_sample_run(layers, 1, threads)
@@ -237,6 +249,7 @@ def cpu_baseline(layers, budget_s):
         batch = max(1, min(layers[0][1], int(budget_s / t1)))
         t1, f1 = cpu_sample_run(layers, batch, threads)
     return {"value": f1 / t1 / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{batch} image(s) per layer, fwd+bwd of every layer, oracle im2col+"
                       f"blocked SGEMM+col2im (oracle/oracle.c), {threads} OpenMP threads, "
                       f"{t1:.1f} s"}
@@ -267,6 +280,7 @@ def run_reference(args):
         "config": {"workload": args.workload, "layers": [l[0] for l in layers],
                    "sample_batch_per_layer": nimg, "full_batch": layers[0][1]},
         "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{nimg} images per layer per step, fwd+bwd, oracle port "
                                    "(im2col + blocked SGEMM + col2im); the reference ships no "
                                    "conv implementation (SURVEY.md §0)"},
