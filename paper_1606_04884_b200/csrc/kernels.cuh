@@ -85,6 +85,7 @@ struct UmmaPlan {
     int cb = 32;          // channel chunk per TMA im2col box (32: SW128, 4: no swizzle)
     int cg = 1;           // CTAs per MMA (2: cta_group::2 pair, M = 256)
     int64_t cin_p = 0;    // padded input channels of the NHWC operand
+    int64_t cin_real = 0; // the real ones (the rest of the last 32-channel chunk is zero)
     int64_t taps = 0;     // kH*kW
     int64_t slots_p = 0;  // layout-4 slot count padded to 8
     int64_t n_rows = 0;   // GEMM N (output channels)

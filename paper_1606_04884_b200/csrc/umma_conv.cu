@@ -416,6 +416,7 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
 
 void plan_channels(UmmaPlan& pl, int64_t cin) {
     const int64_t c32 = (cin + 31) / 32 * 32;
+    pl.cin_real = cin;
     if (cin % 32 == 0 || c32 * 3 <= cin * 4) {
         pl.cb = 32;
         pl.cin_p = c32;

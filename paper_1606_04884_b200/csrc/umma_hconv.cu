@@ -55,6 +55,7 @@ struct HConvParams {
     CUtensorMap tmap_a2; // same with NR - 1 rows: runs starting early in a row need one row less
     CUtensorMap tmap_b;  // packed weights, 3-D {32, n_pad, kdim/32}, box {32, rows, CPS}, SW128
     int N, kH, kW, chunks, cin_p;
+    int last_k;          // live K=8 steps of the last 32-channel chunk (the rest are zero channels)
     int aph, apw;        // zero border the TMA out-of-bounds fill supplies (top, left)
     int Wp;              // padded row width = position-space row stride
     int oH, oW;          // valid output extent
@@ -343,6 +344,8 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             const uint32_t blo = desc_lo(smem_u32(sB + (size_t)bs * p.stage_b), 16);
 #pragma unroll
                             for (int k = 0; k < 4 * CPS; ++k) {
+                                // K steps of the last chunk past the real channels multiply zeros
+                                if (cc + (k >> 2) == p.chunks - 1 && (k & 3) >= p.last_k) continue;
                                 const uint64_t bd = desc_make(blo + (k >> 2) * box_b16 + 2 * (k & 3), kHi);
 #pragma unroll
                                 for (int q = 0; q < RUNS; ++q) {
@@ -614,6 +617,14 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
     p.kW = kW;
     p.cin_p = (int)pl.cin_p;
     p.chunks = (int)(pl.cin_p / 32);
+    {
+        static const bool skip = [] {
+            const char* e = std::getenv("PT_B200_HCONV_KSKIP");
+            return e ? std::atoi(e) != 0 : true;
+        }();
+        const int64_t rem = pl.cin_real > 0 ? pl.cin_real - 32 * (p.chunks - 1) : 32;
+        p.last_k = skip ? (int)std::min<int64_t>(4, std::max<int64_t>(1, (rem + 7) / 8)) : 4;
+    }
     p.oH = (int)oH;
     p.oW = (int)oW;
     p.R = (int)((oH + 1) / 2);
