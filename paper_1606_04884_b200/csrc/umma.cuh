@@ -238,16 +238,6 @@ __device__ __forceinline__ void tma_load_3d_cg2(void* dst, const void* tmap, uin
         "l"(tmap), "r"(leader_bar(bar)), "r"(x), "r"(y), "r"(z)
         : "memory");
 }
-// 2-CTA TMA multicast: the box lands at dst in every CTA of `mask`; completion is signalled
-// on the pair-leader barrier of each destination pair
-__device__ __forceinline__ void tma_load_3d_cg2_mc(void* dst, const void* tmap, uint64_t* bar, int x, int y,
-                                                   int z, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.cta_group::2"
-        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-        "l"(tmap), "r"(leader_bar(bar)), "r"(x), "r"(y), "r"(z), "h"(mask)
-        : "memory");
-}
 __device__ __forceinline__ void tma_load_5d_cg2(void* dst, const void* tmap, uint64_t* bar, int c0, int c1,
                                                 int c2, int c3, int c4) {
     asm volatile(

@@ -82,7 +82,7 @@ struct KCursor {
     }
 };
 
-// SPS: (tap, 32-channel chunk) slots per pipeline stage on the CTA-pair path (2 or 4).
+// SPS: (tap, 32-channel chunk) slots per pipeline stage on the CTA-pair path (2).
 // Four slots (K = 128 per stage) halve the barrier round trips per MMA and keep more
 // bytes per request in flight; used when two such stages fit in shared memory.
 template <int CB, int CG, int SPS = 2>
@@ -302,14 +302,6 @@ __global__ void __launch_bounds__(kThreadsU, 1) umma_conv_kernel(const __grid_co
 }
 
 // ---- host ----
-int conv_sps_env() {
-    static const int v = [] {
-        const char* e = std::getenv("PT_B200_CONV_SPS");
-        return e ? std::atoi(e) : 2;  // 4 measured slower (convnet L3 fwd 0.255 -> 0.299 ms)
-    }();
-    return v;
-}
-
 uint32_t tmem_cols_for(int bn) {
     const int need = 2 * bn;
     uint32_t c = 32;
@@ -381,11 +373,9 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
     p.kW = kW;
     p.chunks = (int)(pl.cin_p / pl.cb);
     p.slots = (int)(pl.taps * p.chunks);
-    // CTA pairs: 4 slots per stage when two such stages fit (see umma_conv_kernel)
-    const uint32_t b_slot = (uint32_t)(pl.bn / 2) * 128u;
-    const int sps = (pl.cb == 32 && pl.cg == 2)
-                        ? ((conv_sps_env() == 4 && 2 * 4 * (kBoxA + b_slot) <= (uint32_t)kSmemLimit - 2048) ? 4 : 2)
-                        : 0;
+    // two 32-deep k slots per stage on the CTA-pair path (four measured slower: convnet L3 fwd
+    // 0.255 -> 0.299 ms, removed)
+    const int sps = 2;
     const int slots_per_stage = pl.cb == 32 ? (pl.cg == 2 ? sps : 1) : 8;
     encode_weights(&p.tmap_b, wt, pl, sps);
     p.num_kb = (int)ceil_div(p.slots, slots_per_stage);
@@ -408,7 +398,6 @@ void run_umma(const UmmaPlan& pl, const float* act, const float* wt, int64_t N, 
     const int clusters = std::min(num_tiles, sm_count() / pl.cg);
     ProfScope prof("umma_conv", st, alg_flops, 0.0);
     if (pl.cb == 4) launch_k<4, 1>(p, clusters, smem, st);
-    else if (pl.cg == 2 && sps == 4) launch_k<32, 2, 4>(p, 2 * clusters, smem, st);
     else if (pl.cg == 2) launch_k<32, 2>(p, 2 * clusters, smem, st);
     else launch_k<32, 1>(p, clusters, smem, st);
     after_launch("umma_conv");

@@ -72,7 +72,6 @@ struct HConvParams {
     uint32_t box_a, box_b;      // bytes per 32-channel box
     uint32_t tmem_cols;
     int nacc;            // TMEM accumulator buffers (2 or 4)
-    int mc;              // 1: clusters of two CTA pairs sharing each weight stage by TMA multicast
     int a_run;           // 1: A = the exact pixel run by TMA im2col traversal (tmap_run), else NR full rows
     int run_px;          // a_run: pixels per run (128 + kW - 1)
     int flat;            // a_run: CTA tiles are consecutive 129-G position runs of a whole image (pair
@@ -119,10 +118,10 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t crank = cluster_rank();
     const uint32_t rank = crank & 1;          // rank in the CTA pair
-    const uint32_t pr = crank >> 1;           // pair in the cluster (mc)
+    const uint32_t pr = 0;                    // one CTA pair per cluster
     const bool leader = rank == 0;
-    const uint16_t pair_mask = (uint16_t)(3u << (2 * pr));
-    const uint16_t bmask = p.mc ? (uint16_t)0xF : pair_mask;  // who consumes a weight stage
+    const uint16_t pair_mask = (uint16_t)3u;
+    const uint16_t bmask = pair_mask;         // who consumes a weight stage
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.tmap_a);
         tma_prefetch(&p.tmap_a2);
@@ -133,7 +132,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
         }
         for (int i = 0; i < p.sb; ++i) {
             mbar_init(&bfull[i], 1);
-            mbar_init(&bempty[i], p.mc ? 2 : 1);  // mc: both pairs release a shared weight stage
+            mbar_init(&bempty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
@@ -149,9 +148,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const int num_units = (int)(((int64_t)p.tiles + RUNS - 1) / RUNS) * p.n_tiles;
-    // pairs per cluster PPC; the pairs of a cluster walk their tiles in lockstep (same count:
-    // a pair past the end runs a dummy tile) because they consume the same weight stages
-    const int PPC = p.mc ? 2 : 1;
+    const int PPC = 1;  // CTA pairs per cluster
     const int cid = blockIdx.x / (2 * PPC), ncl = gridDim.x / (2 * PPC);
     constexpr int kCtaSpan = 129 - G;  // positions a CTA advances per tile
     // flat tiling: CTA tile c of pair tile t; clamped past the end (a dummy: loads anything
@@ -272,20 +269,7 @@ __global__ void __launch_bounds__(kThreadsH, 1) umma_hconv_kernel(const __grid_c
                             mbar_wait(&bempty[bs], bph ^ 1);
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], btx);
                             uint8_t* bdst = sB + (size_t)bs * p.stage_b;
-                            if (p.mc) {
-                                // pair 0 loads each CTA-rank half once, multicast to that rank
-                                // in both pairs
-                                if (pr == 0) {
-                                    const uint16_t m = (uint16_t)(rank ? 0xA : 0x5);
-                                    if constexpr (G == 1)
-                                        tma_load_3d_cg2_mc(bdst, &p.tmap_b, &bfull[bs], 0, brow,
-                                                           (r * p.kW + s) * (p.cin_p / 32) + cc, m);
-                                    else
-                                        tma_load_3d_cg2_mc(bdst, &p.tmap_b, &bfull[bs], 0,
-                                                           ((r * p.ngroups + s / G) * G) * p.bn + (int)rank * (G * p.bn / 2),
-                                                           cc, m);
-                                }
-                            } else if constexpr (G == 1) {
+                            if constexpr (G == 1) {
                                 tma_load_3d_cg2(bdst, &p.tmap_b, &bfull[bs], 0, brow,
                                                 (r * p.kW + s) * (p.cin_p / 32) + cc);
                             } else {
@@ -664,12 +648,12 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
                         (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn) + (size_t)sbias_n * 4;
     p.sbias_n = sbias_n;
     p.xch_bytes_ = (uint32_t)xch_bytes(G, pl.bn);
-    // flat tiling (run mode, no multicast clusters): consecutive CTA tiles over whole images
+    // flat tiling (run mode): consecutive CTA tiles over whole images
     // only where border filter rows are worth skipping (>= 5% of the (row, filter row)
     // pairs: convnet L2 dgrad, 8-row zero border, 0.82 -> 0.78 ms); elsewhere the image-halves
     // pairing measured slightly faster (L1 dgrad 0.37 vs 0.40 ms)
     const bool skip_pays = (double)aph * (aph + 1) >= 0.05 * (double)oH * kH;
-    p.flat = (p.a_run && skip_pays && std::getenv("PT_B200_HCONV_MC") == nullptr) ? 1 : 0;
+    p.flat = (p.a_run && skip_pays) ? 1 : 0;
     if (p.flat) {
         const int64_t P_img = oH * Wp;
         p.m = (int)P_img;
@@ -680,15 +664,11 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
         p.tiles = (int)ceil_div(ct, 2);
     }
     const int units = (int)ceil_div(p.tiles, runs) * p.n_tiles;
-    {
-        // two pairs per cluster sharing each weight stage by multicast: correct, but measured
-        // 1.8x slower (convnet L2 dgrad 0.85 -> 1.51 ms; the pairs' lockstep couples their
-        // stalls), so opt-in only
-        const char* e = std::getenv("PT_B200_HCONV_MC");
-        p.mc = (e && std::atoi(e) == 1 && units >= 2 && runs == 1) ? 1 : 0;
-    }
-    const int cl_ctas = p.mc ? 4 : 2;
-    const int ncl = std::min(p.mc ? (units + 1) / 2 : units, sm_count() / cl_ctas);
+    // (two CTA pairs per cluster sharing each weight stage by TMA multicast measured 1.8x
+    // slower — convnet L2 dgrad 0.85 -> 1.51 ms, the pairs' lockstep couples their stalls —
+    // and was removed)
+    const int cl_ctas = 2;
+    const int ncl = std::min(units, sm_count() / cl_ctas);
     once_per_device((const void*)umma_hconv_kernel<1, 1, 1>, [&] {  // the smem limit is a per-device attribute
         for (auto fn : {umma_hconv_kernel<1, 1, 1>, umma_hconv_kernel<1, 2, 1>, umma_hconv_kernel<1, 3, 1>,
                         umma_hconv_kernel<1, 4, 1>, umma_hconv_kernel<2, 1, 1>, umma_hconv_kernel<2, 2, 1>,
