@@ -1,5 +1,5 @@
-"""GPU debug probe (not collected): VGG-A conv1 combined backward once, for the
-PT_B200_SCBWD_DBG=16 timeline dump."""
+"""GPU timing probe (not collected): VGG-A conv1 combined backward (the fused small-C
+backward, umma_scbwd) timed with CUDA events over three calls."""
 import os
 import sys
 sys.path[:0] = [os.path.dirname(os.path.dirname(os.path.abspath(__file__)))]
