@@ -625,17 +625,27 @@ SCPlan scplan(const Geo& g) {
     const uint32_t wt_bytes = (uint32_t)(pl.Kp * 128);
     const uint32_t sd_bytes = (uint32_t)align_up((size_t)kRowsB * pl.ntaps * 32 * 4, 1024);  // D staging
     const int sms = sm_count();
-    // band rows: B + kH - 1 fills whole 4-row stages (4 by default: 16 gy rows, B = 17 - kH). The
-    // choice depends on the geometry only, never on N — the banding fixes the summation order
-    // of gx, so a batch and its single images must band alike (batched == per-image bitwise)
-    int j = 4;
-    while (4 * j - (int)(g.kH - 1) < 8) ++j;
+    // band rows: B + kH - 1 fills whole 4-row stages (j stages: 4 by default, 16 gy rows,
+    // B = 17 - kH; at least 8 gx rows). The choice depends on the geometry only, never on N —
+    // the banding fixes the summation order of gx, so a batch and its single images must band
+    // alike (batched == per-image bitwise).
+    // A 2-deep derived ring (K-major copy + Xe) decouples the rounding warps from the previous
+    // stage's wgrad MMA; one 4-row stage less per band buys the smem for it where needed
+    // (VGG-A conv1: j = 3 with 2 derived + 2 TMA stages 0.447 ms vs j = 4 with 1 + 3 0.456 ms;
+    // j = 5 0.497 ms)
+    int j0 = 4;
+    while (4 * j0 - (int)(g.kH - 1) < 8) ++j0;
+    auto ring_of = [&](int jj) {
+        return (uint32_t)align_up((size_t)g.C * (4 * jj - (int)(g.kH - 1)) * g.W * 4, 1024);
+    };
+    auto budget_of = [&](int jj) { return kSmemLimitB - 1024 - (int)(wt_bytes + ring_of(jj) + sd_bytes + 1024); };
     auto fits = [&](int jj) {
         const int B = 4 * jj - (int)(g.kH - 1);
-        const uint32_t ring_bytes = (uint32_t)align_up((size_t)g.C * B * g.W * 4, 1024);
-        return B >= 1 && (int)(wt_bytes + ring_bytes + sd_bytes + 1024 + 2 * pl.stage_bytes + pl.dstage_bytes) + 1024 <=
-                             kSmemLimitB;
+        return B >= 1 && budget_of(jj) >= (int)(2 * pl.stage_bytes + pl.dstage_bytes);
     };
+    const int two_sd = (int)(2 * pl.stage_bytes + 2 * pl.dstage_bytes);
+    int j = j0;
+    if (budget_of(j0) < two_sd && 4 * (j0 - 1) - (int)(g.kH - 1) >= 8 && budget_of(j0 - 1) >= two_sd) j = j0 - 1;
     while (j > 1 && !fits(j)) --j;
     if (!fits(j)) return pl;
     pl.B = 4 * j - (int)(g.kH - 1);
@@ -643,10 +653,9 @@ SCPlan scplan(const Geo& g) {
     pl.rstages = j;
     pl.units = (int)(g.N * pl.nb);
     pl.ctas = std::min(pl.units, sms);
-    const uint32_t ring_bytes = (uint32_t)align_up((size_t)g.C * pl.B * g.W * 4, 1024);
-    const int budget = kSmemLimitB - 1024 - (int)(wt_bytes + ring_bytes + sd_bytes + 1024);
-    // the derived ring: 2 stages when 3 TMA stages still fit beside them, else 1
-    pl.dstages = budget >= (int)(3 * pl.stage_bytes + 2 * pl.dstage_bytes) ? 2 : 1;
+    const uint32_t ring_bytes = ring_of(j);
+    const int budget = budget_of(j);
+    pl.dstages = budget >= two_sd ? 2 : 1;
     pl.stages = std::min(6, (budget - pl.dstages * (int)pl.dstage_bytes) / (int)pl.stage_bytes);
     if (pl.stages < 2) return pl;
     pl.d_off = (uint32_t)pl.stages * pl.stage_bytes;
