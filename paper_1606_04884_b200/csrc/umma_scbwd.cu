@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
                             dstage = 0;
                             dphase ^= 1;
                         }
-                            if (++stage == S) {
+                        if (++stage == S) {
                             stage = 0;
                             phase ^= 1;
                         }
