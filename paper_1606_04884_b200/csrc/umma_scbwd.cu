@@ -364,8 +364,7 @@ __global__ void __launch_bounds__(kThreadsB, 1) umma_scbwd_kernel(const __grid_c
     } else if (warp < 10) {
         // ===== Xe warps: Xe[t][n][px] = tf32(x[c][t + r][px + s]) from the x tile (two SW128
         // boxes [c][row][32 px]), zero for gy rows this band does not own =====
-        if (!p.do_wg) {
-        } else {
+        if (p.do_wg) {
             const int bt = (int)threadIdx.x - 192;
             const int kWC = p.kW * p.C;
             // Xe items of this thread (fixed per stage): 8 float4 per (t, n) row
