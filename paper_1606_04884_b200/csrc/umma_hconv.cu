@@ -648,12 +648,18 @@ void run_hconv(const UmmaPlan& pl, const float* act, const float* wt, int64_t N,
                         (2 * sa + 2 * sb + 8) * 8 + 16 + xch_bytes(G, pl.bn) + (size_t)sbias_n * 4;
     p.sbias_n = sbias_n;
     p.xch_bytes_ = (uint32_t)xch_bytes(G, pl.bn);
-    // flat tiling (run mode): consecutive CTA tiles over whole images
-    // only where border filter rows are worth skipping (>= 5% of the (row, filter row)
-    // pairs: convnet L2 dgrad, 8-row zero border, 0.82 -> 0.78 ms); elsewhere the image-halves
-    // pairing measured slightly faster (L1 dgrad 0.37 vs 0.40 ms)
-    const bool skip_pays = (double)aph * (aph + 1) >= 0.05 * (double)oH * kH;
-    p.flat = (p.a_run && skip_pays) ? 1 : 0;
+    // flat tiling (run mode): consecutive CTA tiles over whole images. It skips the filter
+    // rows of a large zero border (convnet L2 dgrad 0.82 -> 0.78 ms) and rounds tiles once
+    // per image instead of once per half: interleaved per-launch A/B, flat vs halves: VGG-A
+    // conv3 fwd 157 -> 146 us, conv4 fwd/dgrad 293 -> 271 us, AlexNet conv1/conv2 and
+    // Overfeat conv1 -2..-3 %; the exception is the row-expanded small-C dgrad (kH = 1:
+    // nothing to skip, one filter row per tile), where the image halves stay faster (convnet
+    // L1 dgrad 275 vs 284 us). PT_B200_HCONV_FLAT=1 / 2 forces flat / halves.
+    static const int flat_env = [] {
+        const char* e = std::getenv("PT_B200_HCONV_FLAT");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.flat = (p.a_run && (flat_env == 1 || (flat_env == 0 && kH > 1))) ? 1 : 0;
     if (p.flat) {
         const int64_t P_img = oH * Wp;
         p.m = (int)P_img;
