@@ -504,18 +504,24 @@ void plan_hankel(UmmaPlan& pl, int64_t N, int64_t aH, int64_t aW, int64_t ph, in
     const int64_t Hp = aH + 2 * ph, Wp = aW + (hconv_wrap() ? 1 : 2) * pw;
     if (Wp > 256 || N * aH * aW >= (1ll << 31)) return;  // a padded row is one TMA box dimension
     // efficiency from the geometry alone (not N) so a batch and its per-image slices
-    // always take the same engine (batched == per-image bitwise): each image's
-    // rows split into two halves walked in 128-position CTA runs
+    // always take the same engine (batched == per-image bitwise), for the tiling
+    // run_hconv will use: 128-position CTA runs over whole images (flat), or over image halves
+    // for one-row filters (the row-expanded small-C dgrad)
+    const int64_t kH_ = pl.taps / kW;
     const int64_t R = (oH + 1) / 2;
-    const double eff = (double)(oH * oW) / (double)(2 * ceil_div(R * Wp, 128) * 128);
+    const double eff = kH_ > 1 ? (double)(oH * oW) / (double)(ceil_div(oH * Wp, 128) * 128)
+                               : (double)(oH * oW) / (double)(2 * ceil_div(R * Wp, 128) * 128);
     // measured (convnet L2/L3/L5): the pixel-run kernel wins at >= 0.85 of positions valid,
     // ties near 0.8 and loses below, where the im2col kernel's zero waste pays for its
     // L2->SM traffic
     // With <= 64 output rows the Hankel kernel also pairs taps (N = 2*bn beats the N=64
     // MMA floor the im2col kernel sits at), which pays for more border waste: AlexNet conv2
     // dgrad (71% valid) 0.151 -> 0.122 ms.
+    // Many output channels make the im2col kernel's L2->SM traffic cheaper per MAC (VGG-A
+    // conv5/6, 87.5 % of positions valid on the flat tiling: im2col 9-15 % faster), so more
+    // than 128 rows need 0.9 (Overfeat conv2 dgrad, 96 rows at 0.9: pixel runs 10 % faster)
     const bool will_pair = pl.n_rows <= hconv_pair_max() && hconv_pair_env() != 0;
-    if (hconv_env() != 1 && eff < (will_pair ? 0.6 : 0.84)) return;
+    if (hconv_env() != 1 && eff < (will_pair ? 0.6 : pl.n_rows <= 128 ? 0.84 : 0.9)) return;
     pl.hankel = true;
     // pairing doubles N: for <= 64 rows it beats the N=64 MMA floor (L2 dgrad 1.27 ->
     // 0.92 ms). Allowed up to 128 rows (N=256) by PT_B200_HCONV_PAIR_MAX, but measured
