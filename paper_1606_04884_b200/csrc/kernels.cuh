@@ -176,9 +176,11 @@ size_t hwgrad_part_bytes(const Geo& g);
 // xh: x NHWC dense with (C+31)/32*32 channels; gyh: gy NHWC with (K+31)/32*32 channels
 void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, float scale, int accumulate,
                 float* part, double alg_flops, cudaStream_t st);
-// fixed-order split reduce of [split][(r*kW+s)*Cp + c][k] partials into KCRS gw
+// fixed-order split reduce of [split][(r*kW+s)*Cp + c][k] partials into KCRS gw; filter
+// columns s >= s_v0 sum splits_v partials instead of splits (s_v0 < 0: all columns splits)
 void wgrad_reduce_launch(const float* part, float* gw, const Geo& g, int64_t Cp, int splits, int64_t ld,
-                         int64_t split_stride, float scale, int accumulate, cudaStream_t st);
+                         int64_t split_stride, float scale, int accumulate, cudaStream_t st, int splits_v = 0,
+                         int s_v0 = -1);
 
 // ---- umma_swgrad.cu: small-C stride-1 weight gradient (planes of horizontal taps) ----
 bool swgrad_ok(const Geo& g);

@@ -31,6 +31,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "kernels.cuh"
 #include "tmap.cuh"
@@ -57,8 +58,11 @@ struct HWParams {
     int cps, n_tiles, splits, kH;
     int items;            // N * rgs * jsegs pixel items
     int per_split, rem;   // split sp covers per_split (+1 for sp < rem) consecutive items
+    int splits_v, per_split_v, rem_v;  // the same for the vertical units (their own split count)
     int bn, stages;
     uint32_t stage_a, stage_b, tx, tmem_cols;
+    int tbuf;             // TMEM accumulator buffers (1 or 2)
+    uint32_t tbuf_cols;   // column offset of buffer 1
     float* part;
     int64_t part_ld, part_split;
 };
@@ -73,9 +77,9 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
     const uint32_t stage_bytes = p.stage_a + p.stage_b;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
     uint64_t* empty = full + S;
-    uint64_t* tfull = empty + S;
-    uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint64_t* tfull = empty + S;    // [2]: one per TMEM accumulator buffer
+    uint64_t* tempty = tfull + 2;   // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const uint32_t warp = warp_id_uniform(), lane = lane_id();
     const uint32_t rank = cluster_rank();
@@ -87,8 +91,10 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
             mbar_init(&full[i], 1);   // the leader's expect_tx (the peer's bytes land on it)
             mbar_init(&empty[i], 1);  // one multicast commit
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, 16);  // 8 epilogue warps x 2 CTAs
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 16);  // 8 epilogue warps x 2 CTAs
+        }
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc_cg2(tmem_holder, p.tmem_cols);
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const int units_h = p.kH * p.cps * p.n_tiles * p.splits;
-    const int units = units_h + p.nbands * p.cps * p.n_tiles * p.splits;
+    const int units = units_h + p.nbands * p.cps * p.n_tiles * p.splits_v;
     const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
     // unit -> (r, chunk pair, n-tile, split); r fastest: concurrent pairs share gy stages in L2.
     // Units past units_h are vertical: r = the band's first filter row (4 * band), vt = true.
@@ -115,9 +121,10 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
     };
     // 32-bit only: a 64-bit division is a call, after which the compiler keeps the MMA
     // loop's descriptor state in vector registers (R2UR + elect per MMA)
-    auto range = [&](int sp, int& lo, int& hi) {
-        lo = sp * p.per_split + (sp < p.rem ? sp : p.rem);
-        hi = lo + p.per_split + (sp < p.rem ? 1 : 0);
+    auto range = [&](int sp, bool vt, int& lo, int& hi) {
+        const int ps = vt ? p.per_split_v : p.per_split, rm = vt ? p.rem_v : p.rem;
+        lo = sp * ps + (sp < rm ? sp : rm);
+        hi = lo + ps + (sp < rm ? 1 : 0);
     };
 
     if (warp == 0) {
@@ -129,7 +136,7 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
                 int r, cp, nt, sp, lo, hi;
                 bool vt;
                 decode(u, r, cp, nt, sp, vt);
-                range(sp, lo, hi);
+                range(sp, vt, lo, hi);
                 const int chunk = 2 * cp + (int)rank;
                 const int kb = (nt * p.bn + (int)rank * (p.bn / 2)) / 32;
                 for (int it = lo; it < hi; ++it) {
@@ -168,13 +175,18 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
                 int r, cp, nt, sp, lo, hi;
                 bool vt;
                 decode(u, r, cp, nt, sp, vt);
-                range(sp, lo, hi);
+                range(sp, vt, lo, hi);
                 // horizontal: quad q = taps 4q..4q+3 one pixel (128 B) apart; vertical: quad q =
                 // column 4*qh + q of filter rows r..r+3, one box row (Wbox px) apart
                 const int nq = vt ? p.ql : p.qh;
                 const uint32_t a_lbo = vt ? (uint32_t)p.Wbox * 128u : 128u;
                 const uint32_t q_step = vt ? 8u : 32u, q_base = vt ? (uint32_t)(4 * p.qh) * 8u : 0u;
-                mbar_wait(tempty, (it_u & 1) ^ 1);
+                // p.tbuf = 2: unit i accumulates in TMEM buffer i & 1, so the epilogue of one
+                // unit drains while the next one's MMAs run
+                const int tb = p.tbuf == 2 ? (it_u & 1) : 0;
+                const uint32_t tpar = p.tbuf == 2 ? (uint32_t)(it_u >> 1) & 1u : (uint32_t)it_u & 1u;
+                const uint32_t tacc = tmem_base + (uint32_t)tb * p.tbuf_cols;
+                mbar_wait(&tempty[tb], tpar ^ 1);
                 tc_fence_after();
                 uint32_t accum = 0;
                 for (int it = lo; it < hi; ++it) {
@@ -189,7 +201,7 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
 #pragma unroll
                         for (int q = 0; q < QPR; ++q)
                             if (q < nq)
-                                mma_tf32_cg2_warp(tmem_base + (uint32_t)q * bn, desc_make(alo + q_step * (uint32_t)q, kHi),
+                                mma_tf32_cg2_warp(tacc + (uint32_t)q * bn, desc_make(alo + q_step * (uint32_t)q, kHi),
                                                   bd, idesc, accum);
                         accum = 1;
                         blo += 64u;  // 8 pixel rows
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
                         phase ^= 1;
                     }
                 }
-                mma_commit_cg2_warp(tfull);
+                mma_commit_cg2_warp(&tfull[tb]);
             }
         }
     } else {
@@ -218,7 +230,9 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
             int r, cp, nt, sp;
             bool vt;
             decode(u, r, cp, nt, sp, vt);
-            mbar_wait(tfull, it_u & 1);
+            const int tb = p.tbuf == 2 ? (it_u & 1) : 0;
+            const uint32_t tpar = p.tbuf == 2 ? (uint32_t)(it_u >> 1) & 1u : (uint32_t)it_u & 1u;
+            mbar_wait(&tfull[tb], tpar);
             tc_fence_after();
             const int c = (2 * cp + (int)rank) * 32 + (int)lane;
             const int nq = vt ? p.ql : p.qh;
@@ -228,7 +242,7 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
                 const bool valid = s < p.kW && rr < p.kH && c < p.Cp;
                 float* dst = p.part + (int64_t)sp * p.part_split +
                              ((int64_t)(rr * p.kW + s) * p.Cp + c) * p.part_ld + (int64_t)nt * p.bn;
-                const uint32_t taddr = tmem_base + ((qtr * 32u) << 16) + (uint32_t)(q * p.bn);
+                const uint32_t taddr = tmem_base + ((qtr * 32u) << 16) + (uint32_t)tb * p.tbuf_cols + (uint32_t)(q * p.bn);
                 for (int c0 = half * 16; c0 < p.bn; c0 += 32) {
                     uint32_t v[16];
                     tmem_ld_32x32b_x16(taddr + c0, v);
@@ -249,8 +263,8 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (leader) mbar_arrive(tempty);
-                else mbar_arrive_cluster(tempty, 0);
+                if (leader) mbar_arrive(&tempty[tb]);
+                else mbar_arrive_cluster(&tempty[tb], 0);
             }
         }
     }
@@ -263,13 +277,44 @@ __global__ void __launch_bounds__(kThreadsHW, 1) umma_hwgrad_kernel(const __grid
 }
 
 struct HWPlan {
-    int Cp, Kp, bn, n_tiles, qpr, KP, R, Wbox, jsegs, rgs, cps, splits, stages;
+    int Cp, Kp, bn, n_tiles, qpr, KP, R, Wbox, jsegs, rgs, cps, splits, splits_v, stages;
     int qh, ql, nbands;  // horizontal quads per row, leftover columns, vertical bands (0: off)
     int64_t quads;       // MMA quads per (chunk pair, n-tile, split) over all units
     int64_t items;
-    uint32_t stage_a, stage_b, tmem_cols;
+    uint32_t stage_a, stage_b, tmem_cols, tbuf_cols;
+    int tbuf;
     int64_t part_elems;
 };
+
+// relative cost per pixel item of a one-quad vertical unit against a one-quad horizontal
+// unit (its stage also stages kH-band rows of x: more TMA per MMA)
+double hwgrad_vbeta() {
+    static const double v = [] {
+        // <= 0: one split count for both; 1.2 measured best of 1.0 / 1.2 (convnet L2 wgrad
+        // 0.658 -> 0.589 ms, L3 0.254 -> 0.236 ms with the double TMEM buffer)
+        const char* e = std::getenv("PT_B200_HWGRAD_VBETA");
+        return e ? std::atof(e) : 1.2;
+    }();
+    return v;
+}
+
+int hwgrad_tbuf_env() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_HWGRAD_TBUF");  // TMEM accumulator buffers: 1 or 2
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+
+// per-unit fixed cost (pipeline fill, epilogue tail) in pixel items, with the epilogue
+// overlapped by the double TMEM buffer
+double hwgrad_unit_ovh() {
+    static const double v = [] {
+        const char* e = std::getenv("PT_B200_HWGRAD_OVH");
+        return e ? std::atof(e) : 8.0;
+    }();
+    return v;
+}
 
 int hwgrad_env() {
     static const int v = [] {
@@ -279,7 +324,28 @@ int hwgrad_env() {
     return v;
 }
 
+HWPlan hwplan_make(const Geo& g);
+
+// the split search costs ~1 ms of host time; eager callers plan the same layer several times
 HWPlan hwplan(const Geo& g) {
+    struct Entry {
+        int64_t key[12];
+        HWPlan plan;
+    };
+    thread_local Entry cache[8];
+    thread_local int next = 0, used = 0;
+    const int64_t key[12] = {g.N, g.C, g.H, g.W, g.K, g.kH, g.kW, g.pH, g.pW, g.sH, g.sW, (int64_t)sm_count()};
+    for (int i = 0; i < used; ++i)
+        if (!memcmp(cache[i].key, key, sizeof key)) return cache[i].plan;
+    Entry& e = cache[next];
+    memcpy(e.key, key, sizeof key);
+    e.plan = hwplan_make(g);
+    next = (next + 1) % 8;
+    used = std::min(used + 1, 8);
+    return e.plan;
+}
+
+HWPlan hwplan_make(const Geo& g) {
     HWPlan w;
     w.Cp = (int)((g.C + 31) / 32 * 32);
     w.Kp = (int)((g.K + 31) / 32 * 32);
@@ -323,24 +389,46 @@ HWPlan hwplan(const Geo& g) {
     w.stages = std::min(8, (kSmemLimitHW - 1024 - 256) / (int)(w.stage_a + w.stage_b));
     uint32_t cols = 32;
     while ((int)cols < w.qpr * w.bn) cols <<= 1;
-    w.tmem_cols = cols;
-    // pixel splits: enough units for every CTA pair with a small tail (static schedule)
+    // two accumulator buffers where they fit the 512 TMEM columns: a unit's epilogue then
+    // overlaps the next unit's MMAs
+    w.tbuf = hwgrad_tbuf_env() == 2 && 2 * cols <= 512 ? 2 : 1;
+    w.tbuf_cols = cols;
+    w.tmem_cols = cols * (uint32_t)w.tbuf;
+    // pixel splits: enough units for every CTA pair with a small tail (static round-robin
+    // schedule: unit i runs on pair i mod P). Vertical units issue ql quads per stage against
+    // the horizontal units' qh, so they get their own (smaller) split count: with one count
+    // the pairs holding a vertical unit idle for the second half of the launch (convnet L2:
+    // 54 two-quad + 18 one-quad units on 74 pairs).
     const int64_t pairs = sm_count() / 2;
-    const int64_t base = (int64_t)(g.kH + w.nbands) * w.cps * w.n_tiles;
-    int best = 1;
+    const int64_t bh = g.kH * w.cps * w.n_tiles, bv = (int64_t)w.nbands * w.cps * w.n_tiles;
+    const bool sep = w.nbands && hwgrad_vbeta() > 0.0;
+    const double beta = sep ? hwgrad_vbeta() * w.ql / w.qh : 1.0;
+    int best = 1, best_v = 1;
     double best_cost = 1e30;
     for (int sp = 1; sp <= 96; ++sp) {
         if (sp > w.items) break;
-        const int64_t units = base * sp;
-        const double waves = (double)ceil_div(units, pairs);
-        // time ~ waves * (work per unit) + a per-unit epilogue / pipeline-fill overhead
-        const double cost = waves * ((double)w.items / sp + 24.0);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = sp;
+        for (int sv = sep ? 1 : sp; sv <= sp; ++sv) {
+            const int64_t uh = bh * sp, uv = bv * sv;
+            // time ~ per-pair sum of (work per unit + a per-unit epilogue / pipeline-fill overhead)
+            const double ovh = w.tbuf == 2 ? hwgrad_unit_ovh() : 24.0;
+            const double ch = (double)w.items / sp + ovh, cv = beta * w.items / sv + ovh;
+            double cost = 0.0;
+            for (int64_t c = 0; c < std::min(pairs, uh + uv); ++c) {
+                const int64_t nh = c < uh ? (uh - 1 - c) / pairs + 1 : 0;
+                // vertical unit indices uh .. uh+uv-1 congruent to c mod pairs
+                const int64_t first = uh + ((c - uh % pairs) % pairs + pairs) % pairs;
+                const int64_t nv = first < uh + uv ? (uh + uv - 1 - first) / pairs + 1 : 0;
+                cost = std::max(cost, nh * ch + nv * cv);
+            }
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = sp;
+                best_v = sv;
+            }
         }
     }
     w.splits = best;
+    w.splits_v = best_v;
     w.part_elems = (int64_t)w.splits * g.kH * g.kW * w.Cp * w.n_tiles * w.bn;
     return w;
 }
@@ -416,6 +504,9 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
     p.items = (int)w.items;
     p.per_split = (int)(w.items / w.splits);
     p.rem = (int)(w.items % w.splits);
+    p.splits_v = w.splits_v;
+    p.per_split_v = (int)(w.items / w.splits_v);
+    p.rem_v = (int)(w.items % w.splits_v);
     p.bn = w.bn;
     p.stages = w.stages;
     p.stage_a = w.stage_a;
@@ -423,11 +514,13 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
     p.tx = (uint32_t)(2 * ((size_t)w.R * w.Wbox * 128 + (size_t)(w.bn / 64) * w.R * w.KP * 128));
     p.tx_v = (uint32_t)(2 * ((size_t)(w.R + 3) * w.Wbox * 128 + (size_t)(w.bn / 64) * w.R * w.KP * 128));
     p.tmem_cols = w.tmem_cols;
+    p.tbuf = w.tbuf;
+    p.tbuf_cols = w.tbuf_cols;
     p.part = part;
     p.part_ld = (int64_t)w.n_tiles * w.bn;
     p.part_split = g.kH * g.kW * w.Cp * p.part_ld;
     const size_t smem = 1024 + (size_t)w.stages * (w.stage_a + w.stage_b) + (2 * w.stages + 4) * 8 + 16;
-    const int units = (int)((g.kH + w.nbands) * w.cps * w.n_tiles * w.splits);
+    const int units = (int)((g.kH * w.splits + w.nbands * w.splits_v) * w.cps * w.n_tiles);
     const int pairs = std::min(units, sm_count() / 2);
     once_per_device((const void*)umma_hwgrad_kernel<1>, [&] {  // the smem limit is a per-device attribute
         PTB_CUDA(cudaFuncSetAttribute(umma_hwgrad_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -459,7 +552,8 @@ void hwgrad_run(const Geo& g, const float* xh, const float* gyh, float* gw, floa
         else PTB_CUDA(cudaLaunchKernelEx(&cfg, umma_hwgrad_kernel<4>, p));
         after_launch("umma_hwgrad");
     }
-    wgrad_reduce_launch(part, gw, g, w.Cp, w.splits, p.part_ld, p.part_split, scale, accumulate, st);
+    wgrad_reduce_launch(part, gw, g, w.Cp, w.splits, p.part_ld, p.part_split, scale, accumulate, st, w.splits_v,
+                        w.nbands ? 4 * w.qh : -1);
 }
 
 }  // namespace ptb

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kThreadsW, 1) umma_wgrad_kernel(const __grid_c
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ gw,
                                     int K, int C, int kH, int kW, int Cp,
                                     int splits, int64_t ld, int64_t split_stride, float scale,
-                                    int accumulate) {
+                                    int accumulate, int splits_v, int s_v0) {
     const int K4 = K / 4;
     const int taps = kH * kW;
     const int total = K4 * C * taps;
@@ -254,9 +254,11 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
         const int crs = i / K4, k = (i - crs * K4) * 4;
         const int c = crs / taps, rs = crs - c * taps;  // rs = r*kW + s
         const float* src = part + ((int64_t)rs * Cp + c) * ld + k;
+        // filter columns s >= s_v0 (umma_hwgrad's vertical quads) carry splits_v partials
+        const int ns = rs % kW >= s_v0 ? splits_v : splits;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-        for (int sp = 0; sp < splits; ++sp) {
+        for (int sp = 0; sp < ns; ++sp) {
             const float4 v = ld_f4_l2hint(reinterpret_cast<const float4*>(src + (int64_t)sp * split_stride), pol);
             acc.x += v.x;
             acc.y += v.y;
@@ -276,7 +278,7 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
 __global__ void wgrad_reduce1_kernel(const float* __restrict__ part, float* __restrict__ gw,
                                      int K, int C, int kH, int kW, int Cp,
                                      int splits, int64_t ld, int64_t split_stride, float scale,
-                                     int accumulate) {
+                                     int accumulate, int splits_v, int s_v0) {
     const int total = K * C * kH * kW;
     const int taps = kH * kW;
     const uint64_t pol = l2_evict_first_policy();
@@ -284,9 +286,10 @@ __global__ void wgrad_reduce1_kernel(const float* __restrict__ part, float* __re
         const int crs = i / K, k = i - crs * K;
         const int c = crs / taps, rs = crs - c * taps;
         const float* src = part + ((int64_t)rs * Cp + c) * ld + k;
+        const int ns = rs % kW >= s_v0 ? splits_v : splits;
         float acc = 0.f;
 #pragma unroll 8
-        for (int sp = 0; sp < splits; ++sp) acc += ld_f_l2hint(src + (int64_t)sp * split_stride, pol);
+        for (int sp = 0; sp < ns; ++sp) acc += ld_f_l2hint(src + (int64_t)sp * split_stride, pol);
         const int64_t o = (int64_t)k * C * taps + crs;
         gw[o] = (accumulate ? gw[o] : 0.f) + scale * acc;
     }
@@ -295,16 +298,22 @@ __global__ void wgrad_reduce1_kernel(const float* __restrict__ part, float* __re
 }  // namespace
 
 void wgrad_reduce_launch(const float* part, float* gw, const Geo& g, int64_t Cp, int splits, int64_t ld,
-                         int64_t split_stride, float scale, int accumulate, cudaStream_t st) {
+                         int64_t split_stride, float scale, int accumulate, cudaStream_t st, int splits_v,
+                         int s_v0) {
+    if (s_v0 < 0) {  // one split count for every tap
+        splits_v = splits;
+        s_v0 = (int)g.kW;
+    }
     const int64_t n = g.K * g.CRS;
     PTB_REQUIRE(n < (1ll << 31), "wgrad_reduce: weights too large");
     if (g.K % 4 == 0 && ld % 4 == 0 && split_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(part) & 15) == 0) {
         wgrad_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n / 4, 256), 8 * (int64_t)sm_count()), 256, 0,
                               st>>>(part, gw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, (int)Cp, splits, ld,
-                                    split_stride, scale, accumulate);
+                                    split_stride, scale, accumulate, splits_v, s_v0);
     } else {
         wgrad_reduce1_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * (int64_t)sm_count()), 256, 0, st>>>(
-            part, gw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, (int)Cp, splits, ld, split_stride, scale, accumulate);
+            part, gw, (int)g.K, (int)g.C, (int)g.kH, (int)g.kW, (int)Cp, splits, ld, split_stride, scale, accumulate,
+            splits_v, s_v0);
     }
     after_launch("wgrad_reduce");
 }
