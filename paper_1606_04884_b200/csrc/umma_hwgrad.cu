@@ -410,7 +410,9 @@ HWPlan hwplan_make(const Geo& g) {
         for (int sv = sep ? 1 : sp; sv <= sp; ++sv) {
             const int64_t uh = bh * sp, uv = bv * sv;
             // time ~ per-pair sum of (work per unit + a per-unit epilogue / pipeline-fill overhead)
-            const double ovh = w.tbuf == 2 ? hwgrad_unit_ovh() : 24.0;
+            // (the smaller overhead only re-measured with vertical units: the s2d conv1s'
+            // split choice stays as it was)
+            const double ovh = w.tbuf == 2 && w.nbands ? hwgrad_unit_ovh() : 24.0;
             const double ch = (double)w.items / sp + ovh, cv = beta * w.items / sv + ovh;
             double cost = 0.0;
             for (int64_t c = 0; c < std::min(pairs, uh + uv); ++c) {

@@ -332,6 +332,14 @@ int wgrad_kp_env() {
     return v;
 }
 
+int wgrad_sched_env() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_WGRAD_SCHED");  // 0: ~4 units per pair, rounded up
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 struct WPlan {
     int64_t Cp, Kp, kdim;
     int mt;  // m-tiles per unit (1 or 2)
@@ -368,6 +376,23 @@ WPlan wplan(const Geo& g) {
     int64_t splits = ceil_div(target_units, tiles);
     int64_t kbps = ceil_div(w.total_kb, splits);
     if (kbps < 8 * w.mt) kbps = 8 * w.mt;  // >= 512 pixels per unit to amortise the epilogue
+    if (wgrad_sched_env()) {
+        // units run round-robin over the pairs (static): ~4 per pair rounded UP left a last
+        // wave a quarter full on most layers (e.g. 301 units = 4.07 waves of 74). Pick the
+        // split count minimising waves x (k-blocks per unit + a per-unit fixed cost of two
+        // k-blocks), ties to more units.
+        const int64_t pairs = sm_count() / 2;
+        double best = 1e30;
+        for (int64_t s = 1; s <= 4 * ceil_div(target_units, tiles); ++s) {
+            const int64_t kb = std::max<int64_t>(ceil_div(w.total_kb, s), 8 * w.mt);
+            const int64_t s2 = ceil_div(w.total_kb, kb);
+            const double cost = (double)ceil_div(tiles * s2, pairs) * (double)(kb + 2);
+            if (cost <= best) {
+                best = cost;
+                kbps = kb;
+            }
+        }
+    }
     w.kb_per_split = (int)kbps;
     w.splits = (int)ceil_div(w.total_kb, kbps);
     const int box = kp * 128;
