@@ -257,6 +257,16 @@ struct SWPlan {
     int64_t xe_elems, part_elems;
 };
 
+// least ring depth for more rows per stage (each stage re-fetches the kH - 1 halo rows of
+// the tap planes, so fewer rows per stage cost L2->SM bytes)
+int swgrad_min_stages() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_SWGRAD_MINST");
+        return e ? std::max(2, std::atoi(e)) : 3;
+    }();
+    return v;
+}
+
 SWPlan swplan(const Geo& g) {
     SWPlan w;
     w.P = (int)(g.kW * g.C);
@@ -284,7 +294,7 @@ SWPlan swplan(const Geo& g) {
         w.pad = (uint32_t)align_up((size_t)std::max<int64_t>(1024, std::max(b_over, a_over)), 1024);
         const int budget = kSmemLimitS - 1024 - (int)w.pad - 256;
         w.stages = std::min(8, budget / (int)(w.stage_a + w.stage_b));
-        if (R == 2 || (w.stages >= 3 && R <= g.oH && R + g.kH - 1 <= 256)) break;
+        if (R == 2 || (w.stages >= swgrad_min_stages() && R <= g.oH && R + g.kH - 1 <= 256)) break;
     }
     uint32_t cols = 32;
     while ((int)cols < w.npad) cols <<= 1;

@@ -340,6 +340,15 @@ int wgrad_sched_env() {
     return v;
 }
 
+// per-unit fixed cost (k-blocks) in the whole-wave split search
+int wgrad_unit_ovh() {
+    static const int v = [] {
+        const char* e = std::getenv("PT_B200_WGRAD_OVH");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+
 struct WPlan {
     int64_t Cp, Kp, kdim;
     int mt;  // m-tiles per unit (1 or 2)
@@ -386,7 +395,7 @@ WPlan wplan(const Geo& g) {
         for (int64_t s = 1; s <= 4 * ceil_div(target_units, tiles); ++s) {
             const int64_t kb = std::max<int64_t>(ceil_div(w.total_kb, s), 8 * w.mt);
             const int64_t s2 = ceil_div(w.total_kb, kb);
-            const double cost = (double)ceil_div(tiles * s2, pairs) * (double)(kb + 2);
+            const double cost = (double)ceil_div(tiles * s2, pairs) * (double)(kb + wgrad_unit_ovh());
             if (cost <= best) {
                 best = cost;
                 kbps = kb;
