@@ -52,7 +52,7 @@ def _bench_path(G, x, w, b, gy):
 
 
 @pytest.mark.parametrize("ranks", [2, 4, 8])
-@pytest.mark.parametrize("wl", ["alexnet", "vgga"])
+@pytest.mark.parametrize("wl", ["alexnet", "vgga", "convnet"])
 def test_emulated_ranks_equal_full_batch(wl, ranks):
     from paper_1606_04884_b200.dp import GradBucket, shard_range
     for i, l in enumerate(WORKLOADS[wl]):
